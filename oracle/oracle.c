@@ -1,0 +1,677 @@
+/* oracle.c — TEST INFRASTRUCTURE ONLY: the plain CPU oracle of the VoltanaLLM
+ * hot path (arXiv 2509.04827). See oracle.h for who may use it.
+ *
+ * What it computes, in the paper's order and notation:
+ *   EcoPred   eq:pred-ttft  T_ttft(f, N_bt) = a1_f N_bt + c1_f
+ *             eq:pred-itl   T_itl(f, N_req, N_kv) = a2_f N_req + b2_f N_kv + c2_f,
+ *                           per batch-size tile
+ *   EcoFreq   backlog -> max frequency; else the lowest frequency of the list
+ *             whose predicted latency meets the SLO target; prefill target =
+ *             SLO - waiting time, decode target = SLO
+ *   EcoRoute  what-if f/f' per decode instance, cases (1)-(5) with Delta
+ *   prefill routing: round robin
+ *   energy    time x power(f)                                               (eq:P-f P:187)
+ *   fit       per-frequency (and per tile) least squares
+ * The discrete-event semantics the paper leaves open are the readings A1-A39
+ * listed in DESIGN.md ("Readings of the paper"); each is marked [Axx] below.
+ *
+ * Plain data structures on purpose: the running set of a decode instance is
+ * an admission-ordered array scanned in full every iteration; queues are
+ * arrays. Nothing here is tuned.
+ */
+#include "oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- EcoPred */
+
+static int tile_index(const orc_profile *p, uint64_t n_req) {
+  /* j = min(T-1, floor((N_req-1)/W)): tile boundaries at multiples of W = 128,
+   * "increasing the batch size from 128 to 129 (crossing a boundary)" [A21] */
+  uint64_t j = (n_req - 1) / (uint64_t)p->tile_w;
+  if (j > (uint64_t)(p->n_tiles - 1)) j = (uint64_t)(p->n_tiles - 1);
+  return (int)j;
+}
+
+static double predict_ttft(const orc_profile *p, int lvl, uint64_t n_bt) {
+  /* eq:pred-ttft, evaluated as (a1 * N_bt) + c1 [A33] */
+  return (p->a1[lvl] * (double)n_bt) + p->c1[lvl];
+}
+
+static double predict_itl(const orc_profile *p, int lvl, uint64_t n_req, uint64_t n_kv) {
+  /* eq:pred-itl "(each tile)": ((a2 * N_req) + (b2 * N_kv)) + c2 [A33] */
+  int j = tile_index(p, n_req);
+  size_t idx = (size_t)j * (size_t)p->k + (size_t)lvl;
+  return ((p->a2[idx] * (double)n_req) + (p->b2[idx] * (double)n_kv)) + p->c2[idx];
+}
+
+/* ---------------------------------------------------------------- EcoFreq */
+
+/* "for all candidates in the list of frequencies, it queries EcoPred ... Finally,
+ * it selects the lowest frequency in the list whose corresponding predicted
+ * latency satisfies the SLO target". Feasible means pred <= target
+ * [A1]; if none is feasible the maximum level is used [A2]. */
+static int lowest_feasible_ttft(const orc_profile *p, const uint16_t *L, int K, uint64_t n_bt,
+                                double target) {
+  for (int k = 0; k < K; ++k)
+    if (predict_ttft(p, L[k], n_bt) <= target) return k;
+  return K - 1;
+}
+
+static int lowest_feasible_itl(const orc_profile *p, const uint16_t *L, int K, uint64_t n_req,
+                               uint64_t n_kv, double target) {
+  for (int k = 0; k < K; ++k)
+    if (predict_itl(p, L[k], n_req, n_kv) <= target) return k;
+  return K - 1;
+}
+
+/* prefill target: "subtracts the waiting time from total SLO budget" [A4] */
+static double prefill_budget(double target, double wait) {
+  double b = target - wait;
+  return b > 0.0 ? b : 0.0;
+}
+
+/* ------------------------------------------------------------ power/energy */
+
+/* busy power, eq:P-f as per-level tables with TDP clip [A22]:
+ *   P = min(TDP, P_idle + u(load) * DYN[phase][level]),  u = load / (load + u_half) */
+static double busy_power(const orc_profile *p, int phase, int lvl, uint64_t load) {
+  double uh = phase == 0 ? p->uh_prefill : p->uh_decode;
+  double u = (double)load / ((double)load + uh);
+  double w = p->p_idle + (u * p->dyn[(size_t)phase * (size_t)p->k + (size_t)lvl]);
+  return w < p->tdp ? w : p->tdp;
+}
+
+/* energy = time x power: joules from watts and milliseconds */
+static double interval_energy(double power_w, double dur_ms) { return (power_w * dur_ms) / 1000.0; }
+
+/* ------------------------------------------------------------ decision hash */
+
+static uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+/* h <- splitmix64(h ^ (kind<<48 ^ instance<<32 ^ level<<16 ^ case)) [A36] */
+static uint64_t fold(uint64_t h, uint64_t kind, uint64_t inst, uint64_t level, uint64_t cse) {
+  return splitmix64(h ^ ((kind << 48) ^ (inst << 32) ^ (level << 16) ^ cse));
+}
+
+/* ---------------------------------------------------------------- EcoRoute */
+
+/* One EcoRoute decision for a request of input length `in`.
+ * n[d], kv[d]: effective state of decode instance d (running + routed-but-not-
+ * admitted, [A9]). Returns the instance, writes the case (0 = round robin). */
+static int ecoroute(const orc_profile *p, const uint16_t *L, int K, int n_d, const uint64_t *n,
+                    const uint64_t *kv, uint64_t in, double target, int32_t delta, int policy,
+                    uint32_t *cursor, int *case_out) {
+  if (policy == 1 || n_d == 1) { /* SGLang round robin / single instance [A17] */
+    int d = (int)*cursor;
+    *cursor = (uint32_t)((d + 1) % n_d);
+    *case_out = 0;
+    return d;
+  }
+  int64_t fnow[64], faft[64];
+  int crossed[64];
+  for (int d = 0; d < n_d; ++d) {
+    /* "what-if": frequency now and after hypothetically adding the request.
+     * EcoFreq's predictor rule without the backlog override [A10, A11];
+     * an empty instance sits at the lowest level; the request adds in+1 KV [A12]. */
+    int k_now = n[d] == 0 ? 0 : lowest_feasible_itl(p, L, K, n[d], kv[d], target);
+    int k_aft = lowest_feasible_itl(p, L, K, n[d] + 1, kv[d] + in + 1, target);
+    fnow[d] = p->mhz[L[k_now]];
+    faft[d] = p->mhz[L[k_aft]];
+    crossed[d] = faft[d] > fnow[d]; /* "cross the boundaries" [A13] */
+  }
+  int n_cross = 0;
+  for (int d = 0; d < n_d; ++d) n_cross += crossed[d];
+  int in_set[64];
+  int cse;
+  if (n_cross == 0) {
+    /* (1)/(2): no instance crosses -> lowest current frequency; ties round robin [A16] */
+    int64_t m = INT64_MAX;
+    for (int d = 0; d < n_d; ++d) if (fnow[d] < m) m = fnow[d];
+    int cnt = 0;
+    for (int d = 0; d < n_d; ++d) { in_set[d] = fnow[d] == m; cnt += in_set[d]; }
+    cse = cnt == 1 ? 1 : 2;
+  } else if (n_cross < n_d) {
+    /* (3)/(4): g = (lowest unchanged f) - (lowest crossed f') compared with Delta [A14, A15] */
+    int64_t mu = INT64_MAX, mr = INT64_MAX;
+    for (int d = 0; d < n_d; ++d) {
+      if (!crossed[d] && fnow[d] < mu) mu = fnow[d];
+      if (crossed[d] && faft[d] < mr) mr = faft[d];
+    }
+    int64_t g = mu - mr;
+    if (g <= (int64_t)delta) {
+      /* (3): dispatch to the instance whose frequency would remain unchanged */
+      for (int d = 0; d < n_d; ++d) in_set[d] = !crossed[d] && fnow[d] == mu;
+      cse = 3;
+    } else {
+      /* (4): the instance with the lowest current frequency */
+      int64_t m = INT64_MAX;
+      for (int d = 0; d < n_d; ++d) if (fnow[d] < m) m = fnow[d];
+      for (int d = 0; d < n_d; ++d) in_set[d] = fnow[d] == m;
+      cse = 4;
+    }
+  } else {
+    /* (5): all cross -> the lowest resulting frequency */
+    int64_t m = INT64_MAX;
+    for (int d = 0; d < n_d; ++d) if (faft[d] < m) m = faft[d];
+    for (int d = 0; d < n_d; ++d) in_set[d] = faft[d] == m;
+    cse = 5;
+  }
+  /* ties: round robin among the candidate set, starting at the cursor [A17] */
+  int cnt = 0, best = -1;
+  uint32_t best_dist = UINT32_MAX;
+  for (int d = 0; d < n_d; ++d) {
+    if (!in_set[d]) continue;
+    cnt++;
+    uint32_t dist = (uint32_t)((d - (int)*cursor + n_d) % n_d);
+    if (dist < best_dist) { best_dist = dist; best = d; }
+  }
+  if (cnt >= 2) *cursor = (uint32_t)((best + 1) % n_d);
+  *case_out = cse;
+  return best;
+}
+
+/* --------------------------------------------------------------- simulator */
+
+typedef struct { uint32_t id; uint32_t rem; } run_entry;
+
+typedef struct {
+  /* decode instance state */
+  run_entry *run; uint64_t n_run, cap_run;   /* admission-ordered running set */
+  uint32_t *admq; uint64_t q_head, q_tail;   /* FIFO admission queue (capacity n) */
+  uint64_t nreq, nkv, pend_n, pend_kv;
+  int busy; double end, ebusy, bms; uint64_t iters;
+} dec_inst;
+
+typedef struct {
+  uint64_t qhead;          /* first id (== p mod N_P) not yet batched [A7] */
+  uint64_t bstart, bcnt;   /* ids of the batch in flight: bstart + j*N_P */
+  int busy; double end, ebusy, bms; uint64_t iters;
+} pre_inst;
+
+static int validate(const orc_scenario *s) {
+  if (!s->prof || !s->ladder || s->K < 1 || s->K > 64) return 0;
+  const orc_profile *p = s->prof;
+  if (p->k < 1 || p->n_tiles < 1 || p->tile_w < 1) return 0;
+  for (int k = 0; k < s->K; ++k) {
+    if (s->ladder[k] >= p->k) return 0;
+    if (k > 0 && s->ladder[k] <= s->ladder[k - 1]) return 0;
+  }
+  if (s->n_p < 1 || s->n_d < 1 || s->n_p > 64 || s->n_d > 64) return 0;
+  if (s->policy != 0 && s->policy != 1) return 0;
+  if (s->max_batch_tokens == 0 || s->kv_capacity == 0) return 0;
+  if (s->max_batch_tokens > 0x7fffffffu || s->kv_capacity > 0x7fffffffu) return 0;
+  if (!(s->slo_ttft > 0.0) || !(s->slo_itl > 0.0) || !(s->slo_scale > 0.0)) return 0;
+  if (!(s->kv_transfer_ms == 0.0 || s->kv_transfer_ms >= 1e-3)) return 0;
+  if (!(s->duration_ms >= 0.0)) return 0;
+  uint64_t tok = 0;
+  for (uint64_t i = 0; i < s->n; ++i) {
+    if (s->in_len[i] < 1 || s->out_len[i] < 1 || s->in_len[i] > 65535u || s->out_len[i] > 65535u)
+      return 0;
+    if (!(s->arrival[i] >= 0.0) || !(s->arrival[i] < 1e9)) return 0;
+    if (i > 0 && s->arrival[i] < s->arrival[i - 1]) return 0;
+    tok += (uint64_t)s->in_len[i] + s->out_len[i];
+  }
+  if (tok > 0x7fffffffull) return 0;
+  return 1;
+}
+
+int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
+  memset(res, 0, sizeof(*res));
+  res->n_requests = (uint32_t)s->n;
+  if (!validate(s)) { res->status = ORC_E_INPUT; return 0; }
+
+  const orc_profile *p = s->prof;
+  const uint16_t *L = s->ladder;
+  const int K = s->K, NP = s->n_p, ND = s->n_d;
+  const uint64_t N = s->n;
+  const double *arr = s->arrival;
+  const uint32_t *in = s->in_len, *out = s->out_len;
+  const double tau = s->kv_transfer_ms;
+  /* controller targets: SLO with margin s (default 1.0) [A3] */
+  const double tgt_ttft = s->slo_scale * s->slo_ttft;
+  const double tgt_itl = s->slo_scale * s->slo_itl;
+
+  pre_inst *P = calloc((size_t)NP, sizeof(pre_inst));
+  dec_inst *D = calloc((size_t)ND, sizeof(dec_inst));
+  double *tfirst = calloc(N ? N : 1, sizeof(double));
+  uint8_t *ttft_ok = calloc(N ? N : 1, 1);
+  uint32_t *xq_id = malloc((N ? N : 1) * sizeof(uint32_t)); /* KV-transfer FIFO [A18] */
+  uint32_t *xq_d = malloc((N ? N : 1) * sizeof(uint32_t));
+  uint64_t xq_head = 0, xq_tail = 0;
+  uint64_t *eff_n = malloc((size_t)ND * sizeof(uint64_t));
+  uint64_t *eff_kv = malloc((size_t)ND * sizeof(uint64_t));
+  for (int q = 0; q < NP; ++q) P[q].qhead = (uint64_t)q;
+  for (int d = 0; d < ND; ++d) {
+    D[d].cap_run = 16;
+    D[d].run = malloc(D[d].cap_run * sizeof(run_entry));
+    D[d].admq = malloc((N ? N : 1) * sizeof(uint32_t));
+  }
+
+  uint64_t a = 0;           /* next arrival */
+  uint32_t cursor = 0;      /* EcoRoute / round-robin cursor [A17] */
+  uint64_t h = s->hash_seed;
+  uint64_t steps_ctrl = 0, steps_route = 0, n_ttft_ok = 0, n_itl_ok = 0, n_both = 0;
+  double sum_ttft = 0.0, sum_itl = 0.0, top_ms = 0.0, t = 0.0, t_last = 0.0;
+  uint64_t force_pos = 0;
+  uint32_t status = ORC_OK;
+
+  for (;;) {
+    /* O1: next event time = min over pending events */
+    int have = 0;
+    double tn = 0.0;
+    if (a < N) { tn = arr[a]; have = 1; }
+    if (xq_head < xq_tail) {
+      double tx = tfirst[xq_id[xq_head]] + tau;
+      if (!have || tx < tn) { tn = tx; have = 1; }
+    }
+    for (int q = 0; q < NP; ++q)
+      if (P[q].busy && (!have || P[q].end < tn)) { tn = P[q].end; have = 1; }
+    for (int d = 0; d < ND; ++d)
+      if (D[d].busy && (!have || D[d].end < tn)) { tn = D[d].end; have = 1; }
+    if (!have) break;
+    t = tn;
+    t_last = t;
+
+    /* O2: drain every event at time t in (kind, id) order:
+     * Arrival < KvTransferDone < PrefillDone < DecodeIterDone [A18] */
+    while (a < N && arr[a] == t) a++; /* O3: request a joins prefill queue a mod N_P [A7] */
+
+    while (xq_head < xq_tail && tfirst[xq_id[xq_head]] + tau == t) { /* O4 [A12] */
+      uint32_t i = xq_id[xq_head], d = xq_d[xq_head];
+      xq_head++;
+      D[d].admq[D[d].q_tail++] = i;
+    }
+
+    for (int q = 0; q < NP; ++q) { /* O5: PrefillDone(q) */
+      if (!(P[q].busy && P[q].end == t)) continue;
+      for (uint64_t j = 0; j < P[q].bcnt; ++j) {
+        uint64_t i = P[q].bstart + j * (uint64_t)NP;
+        double ttft = t - arr[i]; /* TTFT = waiting + execution [A26] */
+        sum_ttft += ttft;
+        int ok = ttft <= s->slo_ttft;
+        n_ttft_ok += (uint64_t)ok;
+        ttft_ok[i] = (uint8_t)ok;
+        tfirst[i] = t;
+        if (diag && diag->req_tfirst) diag->req_tfirst[i] = t;
+        if (out[i] == 1) { /* first token came from prefill; nothing to decode [A8, A30] */
+          n_itl_ok++;
+          n_both += (uint64_t)ok;
+          if (diag && diag->req_tdone) diag->req_tdone[i] = t;
+          if (diag && diag->req_decode) diag->req_decode[i] = -1;
+          if (diag && diag->req_itl) diag->req_itl[i] = 0.0;
+          continue;
+        }
+        int cse, d;
+        if (diag && diag->force_decode) {
+          d = diag->force_decode[i];
+          cse = 6;
+        } else {
+          for (int e = 0; e < ND; ++e) { /* effective state = running + pending [A9] */
+            eff_n[e] = D[e].nreq + D[e].pend_n;
+            eff_kv[e] = D[e].nkv + D[e].pend_kv;
+          }
+          d = ecoroute(p, L, K, ND, eff_n, eff_kv, in[i], tgt_itl, s->delta_mhz, s->policy,
+                       &cursor, &cse);
+        }
+        steps_route++;
+        h = fold(h, 3, (uint64_t)d, 0, (uint64_t)cse);
+        if (diag && diag->req_decode) diag->req_decode[i] = d;
+        if (diag && diag->req_case) diag->req_case[i] = (uint8_t)cse;
+        D[d].pend_n += 1;
+        D[d].pend_kv += (uint64_t)in[i] + 1;
+        if (tau == 0.0) {
+          D[d].admq[D[d].q_tail++] = (uint32_t)i;
+        } else {
+          xq_id[xq_tail] = (uint32_t)i;
+          xq_d[xq_tail] = (uint32_t)d;
+          xq_tail++;
+        }
+      }
+      P[q].busy = 0;
+    }
+
+    for (int d = 0; d < ND; ++d) { /* O6: DecodeIterDone(d) [A19] */
+      dec_inst *I = &D[d];
+      if (!(I->busy && I->end == t)) continue;
+      I->nkv += I->nreq; /* every running request stored one more token */
+      uint64_t w = 0;
+      for (uint64_t r = 0; r < I->n_run; ++r) {
+        run_entry e = I->run[r];
+        e.rem -= 1;
+        if (e.rem == 0) {
+          uint32_t id = e.id;
+          /* per-request ITL = mean inter-token latency [A30] */
+          double itl = (t - tfirst[id]) / (double)(out[id] - 1);
+          sum_itl += itl;
+          int ok = itl <= s->slo_itl;
+          n_itl_ok += (uint64_t)ok;
+          n_both += (uint64_t)(ok && ttft_ok[id]);
+          I->nreq -= 1;
+          I->nkv -= (uint64_t)in[id] + out[id];
+          if (diag && diag->req_tdone) diag->req_tdone[id] = t;
+          if (diag && diag->req_itl) diag->req_itl[id] = itl;
+        } else {
+          I->run[w++] = e;
+        }
+      }
+      I->n_run = w;
+      I->busy = 0;
+    }
+
+    /* O7: START phase, prefill 0..N_P-1 then decode 0..N_D-1 [A18] */
+    for (int q = 0; q < NP && status == ORC_OK; ++q) {
+      pre_inst *I = &P[q];
+      if (I->busy || I->qhead >= a) continue;
+      /* FCFS prefix with sum(in) <= B, at least one request [A6] */
+      uint64_t id = I->qhead, nbt = 0, cnt = 0;
+      while (id < a) {
+        if (cnt > 0 && nbt + in[id] > s->max_batch_tokens) break;
+        nbt += in[id];
+        cnt++;
+        id += (uint64_t)NP;
+      }
+      int backlog = id < a; /* requests still waiting after the batch [A5] */
+      double wait = t - arr[I->qhead];
+      int k;
+      if (diag && diag->force_level && force_pos < diag->n_force_level) {
+        k = diag->force_level[force_pos++];
+      } else {
+        /* EcoFreq: backlog -> max frequency; else lowest feasible */
+        k = backlog ? K - 1 : lowest_feasible_ttft(p, L, K, nbt, prefill_budget(tgt_ttft, wait));
+      }
+      steps_ctrl++;
+      h = fold(h, 1, (uint64_t)q, (uint64_t)k, 0);
+      double dur = predict_ttft(p, L[k], nbt); /* execution time = prediction (noise 0) [A25] */
+      if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
+      if (diag && diag->iter_n < diag->iter_cap) {
+        diag->iter_inst[diag->iter_n] = q;
+        diag->iter_level[diag->iter_n] = (uint16_t)k;
+        diag->iter_dur[diag->iter_n] = dur;
+        diag->iter_target[diag->iter_n] = prefill_budget(tgt_ttft, wait);
+        diag->iter_n++;
+      }
+      I->end = t + dur;
+      I->busy = 1;
+      I->bstart = I->qhead;
+      I->bcnt = cnt;
+      I->qhead = id;
+      I->ebusy += interval_energy(busy_power(p, 0, L[k], nbt), dur);
+      I->bms += dur;
+      I->iters++;
+      if (k == K - 1) top_ms += dur;
+    }
+    for (int d = 0; d < ND && status == ORC_OK; ++d) {
+      dec_inst *I = &D[d];
+      if (I->busy) continue;
+      /* admission at the iteration boundary, FCFS while KV fits [A20] */
+      while (I->q_head < I->q_tail) {
+        uint32_t hd = I->admq[I->q_head];
+        uint64_t need = (uint64_t)in[hd] + 1;
+        if (I->nkv + need > s->kv_capacity) break;
+        I->q_head++;
+        if (I->n_run == I->cap_run) {
+          I->cap_run *= 2;
+          I->run = realloc(I->run, I->cap_run * sizeof(run_entry));
+        }
+        I->run[I->n_run].id = hd;
+        I->run[I->n_run].rem = out[hd] - 1;
+        I->n_run++;
+        I->nreq += 1;
+        I->nkv += need;
+        I->pend_n -= 1;
+        I->pend_kv -= need;
+      }
+      if (I->nreq == 0) {
+        if (I->q_head < I->q_tail) { status = ORC_E_SCENARIO_KV; break; }
+        continue;
+      }
+      int backlog = I->q_head < I->q_tail; /* KV-blocked admission queue [A5] */
+      int k;
+      if (diag && diag->force_level && force_pos < diag->n_force_level) {
+        k = diag->force_level[force_pos++];
+      } else {
+        k = backlog ? K - 1 : lowest_feasible_itl(p, L, K, I->nreq, I->nkv, tgt_itl);
+      }
+      steps_ctrl++;
+      h = fold(h, 2, (uint64_t)d, (uint64_t)k, 0);
+      double dur = predict_itl(p, L[k], I->nreq, I->nkv);
+      if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
+      if (diag && diag->time_busy) diag->time_busy[d] += dur;
+      if (diag && diag->time_le_boundary && I->nreq <= diag->boundary) diag->time_le_boundary[d] += dur;
+      if (diag && diag->max_nreq && I->nreq > diag->max_nreq[d]) diag->max_nreq[d] = (uint32_t)I->nreq;
+      if (diag && diag->tokens) diag->tokens[d] += I->nreq;
+      if (diag && diag->kv_peak && I->nkv > diag->kv_peak[d]) diag->kv_peak[d] = I->nkv;
+      if (diag && diag->iter_n < diag->iter_cap) {
+        diag->iter_inst[diag->iter_n] = NP + d;
+        diag->iter_level[diag->iter_n] = (uint16_t)k;
+        diag->iter_dur[diag->iter_n] = dur;
+        diag->iter_target[diag->iter_n] = tgt_itl;
+        diag->iter_n++;
+      }
+      I->end = t + dur;
+      I->busy = 1;
+      I->ebusy += interval_energy(busy_power(p, 1, L[k], I->nreq), dur);
+      I->bms += dur;
+      I->iters++;
+      if (k == K - 1) top_ms += dur;
+    }
+    if (status != ORC_OK) break;
+  }
+
+  if (status == ORC_OK) {
+    /* O9: horizon and idle energy [A23, A39] */
+    double horizon = s->duration_ms > t_last ? s->duration_ms : t_last;
+    double epb = 0.0, epi = 0.0, edb = 0.0, edi = 0.0, bp = 0.0, bd = 0.0;
+    for (int q = 0; q < NP; ++q) {
+      epb += P[q].ebusy;
+      epi += interval_energy(p->p_idle, horizon - P[q].bms);
+      bp += P[q].bms;
+    }
+    for (int d = 0; d < ND; ++d) {
+      edb += D[d].ebusy;
+      edi += interval_energy(p->p_idle, horizon - D[d].bms);
+      bd += D[d].bms;
+    }
+    res->status = ORC_OK;
+    res->n_ttft_ok = (uint32_t)n_ttft_ok;
+    res->n_itl_ok = (uint32_t)n_itl_ok;
+    res->n_both_ok = (uint32_t)n_both;
+    res->steps_ctrl = steps_ctrl;
+    res->steps_route = steps_route;
+    res->decision_hash = h;
+    res->sum_ttft_ms = sum_ttft;
+    res->sum_itl_mean_ms = sum_itl;
+    res->e_prefill_busy_j = epb;
+    res->e_prefill_idle_j = epi;
+    res->e_decode_busy_j = edb;
+    res->e_decode_idle_j = edi;
+    res->busy_ms_prefill = bp;
+    res->busy_ms_decode = bd;
+    res->top_level_ms = top_ms;
+    res->horizon_ms = horizon;
+    if (diag && diag->iters) {
+      for (int q = 0; q < NP; ++q) diag->iters[q] = P[q].iters;
+      for (int d = 0; d < ND; ++d) diag->iters[NP + d] = D[d].iters;
+    }
+  } else {
+    res->status = status; /* per-scenario error: status and n_requests only */
+  }
+
+  for (int d = 0; d < ND; ++d) { free(D[d].run); free(D[d].admq); }
+  free(P); free(D); free(tfirst); free(ttft_ok); free(xq_id); free(xq_d); free(eff_n); free(eff_kv);
+  return 0;
+}
+
+/* ------------------------------------------------ single-decision oracles */
+
+int oracle_control_step(const orc_profile *p, int phase, const uint16_t *L, int K,
+                        const uint32_t *load, const uint32_t *n_kv, const uint32_t *queue_len,
+                        const double *wait_ms, const double *target_ms, size_t n,
+                        uint16_t *out_level, uint8_t *out_status) {
+  for (size_t i = 0; i < n; ++i) {
+    int bad = load[i] == 0 || (phase == 1 && n_kv[i] < load[i]);
+    if (bad) { out_level[i] = 0xFFFF; out_status[i] = (uint8_t)ORC_E_CONTRACT; continue; }
+    int k;
+    if (queue_len[i] > 0) {
+      k = K - 1; /* backlog -> max frequency */
+    } else if (phase == 0) {
+      k = lowest_feasible_ttft(p, L, K, load[i], prefill_budget(target_ms[i], wait_ms[i]));
+    } else {
+      k = lowest_feasible_itl(p, L, K, load[i], n_kv[i], target_ms[i]); /* no wait subtraction */
+    }
+    out_level[i] = (uint16_t)k;
+    out_status[i] = (uint8_t)ORC_OK;
+  }
+  return 0;
+}
+
+int oracle_route_batch(const orc_profile *p, const uint16_t *L, int K, int n_d,
+                       const uint32_t *n_req, const uint32_t *n_kv, const uint32_t *req_in,
+                       const double *itl_target, int32_t delta_mhz, int policy,
+                       uint32_t *cursor, size_t n, uint16_t *out_instance,
+                       uint8_t *out_case, uint8_t *out_status) {
+  uint64_t nn[64], kk[64];
+  for (size_t i = 0; i < n; ++i) {
+    int bad = cursor[i] >= (uint32_t)n_d || req_in[i] == 0;
+    for (int d = 0; d < n_d; ++d) {
+      nn[d] = n_req[i * (size_t)n_d + (size_t)d];
+      kk[d] = n_kv[i * (size_t)n_d + (size_t)d];
+      if (kk[d] < nn[d]) bad = 1;
+    }
+    if (bad) { out_instance[i] = 0xFFFF; out_case[i] = 0xFF; out_status[i] = (uint8_t)ORC_E_CONTRACT; continue; }
+    int cse;
+    int d = ecoroute(p, L, K, n_d, nn, kk, req_in[i], itl_target[i], delta_mhz, policy, &cursor[i], &cse);
+    out_instance[i] = (uint16_t)d;
+    out_case[i] = (uint8_t)cse;
+    out_status[i] = (uint8_t)ORC_OK;
+  }
+  return 0;
+}
+
+/* ------------------------------------------------------------------ fitter */
+
+/* cell_status codes */
+#define FIT_OK 0
+#define FIT_INHERITED 1
+#define FIT_EMPTY 2
+#define FIT_DEGENERATE 3
+
+int oracle_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32_t *n_bt,
+                       const uint32_t *n_req, const uint32_t *n_kv, const double *lat_ms,
+                       size_t n, int K, int T, int W, double tile_step,
+                       double *a1, double *c1, double *a2, double *b2, double *c2,
+                       double *mae, uint8_t *cell_status) {
+  /* F1: cells. TTFT cell k (prefill, level k) = index k; ITL cell (decode, level k,
+   * tile j) = index K + j*K + k, tile j = min(T-1, (N_req-1)/W). */
+  const size_t C = (size_t)K + (size_t)T * (size_t)K;
+  for (size_t i = 0; i < n; ++i) {
+    if (phase[i] > 1 || level[i] >= K) return 1;
+    if (phase[i] == 1 && n_req[i] == 0) return 1;
+  }
+  #define CELL(i) (phase[i] == 0 ? (size_t)level[i] : \
+      (size_t)K + (size_t)((n_req[i] - 1) / (uint32_t)W < (uint32_t)(T - 1) ? (n_req[i] - 1) / (uint32_t)W : (uint32_t)(T - 1)) * (size_t)K + level[i])
+  double *cnt = calloc(C, sizeof(double));
+  double *s1 = calloc(C, sizeof(double)), *s2 = calloc(C, sizeof(double)), *sy = calloc(C, sizeof(double));
+  /* pass 1: means, sequential sums in sample order */
+  for (size_t i = 0; i < n; ++i) {
+    size_t c = CELL(i);
+    cnt[c] += 1.0;
+    if (phase[i] == 0) { s1[c] += (double)n_bt[i]; }
+    else { s1[c] += (double)n_req[i]; s2[c] += (double)n_kv[i]; }
+    sy[c] += lat_ms[i];
+  }
+  double *m1 = calloc(C, sizeof(double)), *m2 = calloc(C, sizeof(double)), *my = calloc(C, sizeof(double));
+  for (size_t c = 0; c < C; ++c) {
+    if (cnt[c] > 0.0) { m1[c] = s1[c] / cnt[c]; m2[c] = s2[c] / cnt[c]; my[c] = sy[c] / cnt[c]; }
+  }
+  /* pass 2: centred sums of squares and cross products */
+  double *S11 = calloc(C, sizeof(double)), *S12 = calloc(C, sizeof(double)), *S22 = calloc(C, sizeof(double));
+  double *S1y = calloc(C, sizeof(double)), *S2y = calloc(C, sizeof(double));
+  for (size_t i = 0; i < n; ++i) {
+    size_t c = CELL(i);
+    double dx1 = (phase[i] == 0 ? (double)n_bt[i] : (double)n_req[i]) - m1[c];
+    double dy = lat_ms[i] - my[c];
+    S11[c] += dx1 * dx1;
+    S1y[c] += dx1 * dy;
+    if (phase[i] == 1) {
+      double dx2 = (double)n_kv[i] - m2[c];
+      S12[c] += dx1 * dx2;
+      S22[c] += dx2 * dx2;
+      S2y[c] += dx2 * dy;
+    }
+  }
+  int err = 0;
+  /* F2: TTFT per level: a = Sxy / Sxx, c = ybar - a xbar; needs >= 2 distinct N_bt [A31] */
+  for (int k = 0; k < K; ++k) {
+    size_t c = (size_t)k;
+    if (cnt[c] == 0.0) { cell_status[c] = FIT_EMPTY; a1[k] = c1[k] = 0.0; err = 1; continue; }
+    if (cnt[c] < 2.0 || !(S11[c] > 0.0)) { cell_status[c] = FIT_DEGENERATE; a1[k] = c1[k] = 0.0; err = 1; continue; }
+    a1[k] = S1y[c] / S11[c];
+    c1[k] = my[c] - (a1[k] * m1[c]);
+    cell_status[c] = FIT_OK;
+  }
+  /* F3/F4: ITL per (tile, level), two regressors; empty tile j>0 inherits j-1 + step */
+  for (int j = 0; j < T; ++j) {
+    for (int k = 0; k < K; ++k) {
+      size_t c = (size_t)K + (size_t)j * (size_t)K + (size_t)k;
+      size_t o = (size_t)j * (size_t)K + (size_t)k;
+      if (cnt[c] == 0.0) {
+        if (j == 0) { cell_status[c] = FIT_EMPTY; a2[o] = b2[o] = c2[o] = 0.0; err = 1; }
+        else {
+          size_t pv = o - (size_t)K;
+          a2[o] = a2[pv]; b2[o] = b2[pv]; c2[o] = c2[pv] + tile_step;
+          cell_status[c] = FIT_INHERITED;
+        }
+        continue;
+      }
+      double pr = S11[c] * S22[c];
+      double det = (S11[c] * S22[c]) - (S12[c] * S12[c]);
+      if (cnt[c] < 3.0 || !(pr > 0.0) || !(det > 1e-10 * pr)) {
+        cell_status[c] = FIT_DEGENERATE; a2[o] = b2[o] = c2[o] = 0.0; err = 1; continue;
+      }
+      a2[o] = ((S22[c] * S1y[c]) - (S12[c] * S2y[c])) / det;
+      b2[o] = ((S11[c] * S2y[c]) - (S12[c] * S1y[c])) / det;
+      c2[o] = (my[c] - (a2[o] * m1[c])) - (b2[o] * m2[c]);
+      cell_status[c] = FIT_OK;
+    }
+  }
+  /* F5: mean absolute error per cell, same evaluation order as EcoPred */
+  double *ae = calloc(C, sizeof(double));
+  for (size_t i = 0; i < n; ++i) {
+    size_t c = CELL(i);
+    if (cell_status[c] != FIT_OK) continue;
+    double yh;
+    if (phase[i] == 0) {
+      yh = (a1[level[i]] * (double)n_bt[i]) + c1[level[i]];
+    } else {
+      size_t o = c - (size_t)K;
+      yh = ((a2[o] * (double)n_req[i]) + (b2[o] * (double)n_kv[i])) + c2[o];
+    }
+    ae[c] += fabs(lat_ms[i] - yh);
+  }
+  for (size_t c = 0; c < C; ++c) mae[c] = (cell_status[c] == FIT_OK) ? ae[c] / cnt[c] : 0.0;
+  #undef CELL
+  free(cnt); free(s1); free(s2); free(sy); free(m1); free(m2); free(my);
+  free(S11); free(S12); free(S22); free(S1y); free(S2y); free(ae);
+  return err ? 4 : 0;
+}
+
+/* ------------------------------------------------------------- pin helpers */
+
+double oracle_predict_ttft(const orc_profile *p, int level, uint32_t n_bt) { return predict_ttft(p, level, n_bt); }
+double oracle_predict_itl(const orc_profile *p, int level, uint32_t n_req, uint32_t n_kv) {
+  return predict_itl(p, level, n_req, n_kv);
+}
+int oracle_tile_index(const orc_profile *p, uint32_t n_req) { return tile_index(p, n_req); }
+double oracle_busy_power(const orc_profile *p, int phase, int level, uint32_t load) {
+  return busy_power(p, phase, level, load);
+}
+double oracle_interval_energy(double power_w, double dur_ms) { return interval_energy(power_w, dur_ms); }

@@ -1,0 +1,612 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (no GPU).
+
+Each test names the pin of DESIGN.md ("Pins") it implements and cites the
+passage. None of these re-types an oracle formula to compare with itself:
+values come from printed worked examples (tests/golden/spec_examples.json),
+closed forms, textbook queueing results, brute-force enumeration,
+numpy.linalg.lstsq, or invariants that must hold for any correct
+implementation.
+"""
+
+import itertools
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from synth.profiles import custom_profile
+from synth.workload import Layout, Slo, INF_DELTA
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def flat_profile(mhz, a1=None, c1=None, a2=None, b2=None, c2=None, dyn=None, T=1, **kw):
+    K = len(mhz)
+    z = np.zeros(K)
+    a1 = z if a1 is None else np.asarray(a1, float)
+    c1 = z + 1.0 if c1 is None else np.asarray(c1, float)
+    t = lambda v: np.tile(np.asarray(v, float), T) if np.size(v) == K else np.asarray(v, float)
+    a2 = t(z if a2 is None else a2)
+    b2 = t(z if b2 is None else b2)
+    c2 = t(z + 1.0 if c2 is None else c2)
+    dyn = np.concatenate([z + 100.0, z + 100.0]) if dyn is None else np.asarray(dyn, float)
+    return custom_profile(mhz, a1, c1, a2, b2, c2, dyn, **kw)
+
+
+# ------------------------------------------------------------------ PIN-1/2 EcoPred
+
+def test_pin1_predictor_worked_examples(orc):
+    for ex in GOLD["predict_ttft"]:
+        p = flat_profile([1005], a1=[ex["a1"]], c1=[ex["c1"]])
+        assert orc.predict_ttft(p, 0, ex["n_bt"]) == ex["expect_ms"], ex["cite"]
+    for ex in GOLD["predict_itl"]:
+        p = flat_profile([1005], a2=[ex["a2"]], b2=[ex["b2"]], c2=[ex["c2"]])
+        assert orc.predict_itl(p, 0, ex["n_req"], ex["n_kv"]) == ex["expect_ms"], ex["cite"]
+
+
+def test_pin1_predictor_affine_and_tile_clamp(orc):
+    p = synth.make_profile("L8")
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        k = int(rng.integers(p.k))
+        x, d = int(rng.integers(1, 4000)), int(rng.integers(1, 2000))
+        y0, y1, y2 = (orc.predict_ttft(p, k, x + i * d) for i in range(3))
+        assert abs((y2 - y1) - (y1 - y0)) <= 1e-9 * y2          # three-point collinearity
+        assert abs((y1 - y0) / d - p.a1[k]) <= 1e-9 * p.a1[k]     # slope = a1_f of eq:pred-ttft
+    # tiles beyond the last calibrated one are clamped
+    last = p.n_tiles * p.tile_w
+    for n in (last, last + 1, last + 1000):
+        assert orc.tile_index(p, n) == p.n_tiles - 1
+    # higher frequency is never slower on the generated profile (fig:u-shape P:174)
+    assert orc.predict_ttft(p, p.k - 1, 2000) < orc.predict_ttft(p, 0, 2000)
+
+
+def test_pin2_tile_index(orc):
+    p = flat_profile([1005], T=16)
+    for ex in GOLD["tile_index"]:
+        assert orc.tile_index(p, ex["n_req"]) == ex["tile"], ex["cite"]
+
+
+def test_pin2_staircase_jump_at_boundary(orc):
+    """128 -> 129 at equal N_kv jumps by the tile step."""
+    p = synth.make_profile("L8")
+    for k in (0, p.k - 1):
+        step = p.c2[1 * p.k + k] - p.c2[k]
+        jump = orc.predict_itl(p, k, 129, 50000) - orc.predict_itl(p, k, 128, 50000)
+        assert abs(jump - (step + p.a2[k])) < 1e-9
+
+
+# ------------------------------------------------------------------ PIN-3/4 EcoFreq
+
+def _two_level_with_preds(pred, phase):
+    """2-level ladder whose prediction at every load equals pred[k] (a=b=0, c=pred)."""
+    if phase == 0:
+        return flat_profile([1005, 1410], a1=[0, 0], c1=pred)
+    return flat_profile([1005, 1410], c2=pred)
+
+
+def test_pin3_budget_examples(orc):
+    lad = np.array([0, 1], np.uint16)
+    for ex in GOLD["slo_budget"]:
+        ph = 0 if ex["phase"] == "prefill" else 1
+        b = ex["budget"]
+        # level 0 predicts exactly the budget: feasible iff the budget is what the example prints
+        # (ties are feasible, A1); a hair above must be infeasible.
+        for pred0, expect in ((b, 0), (np.nextafter(b, np.inf), 1)):
+            if pred0 == 0.0:
+                pred0 = 0.0
+            p = _two_level_with_preds([pred0, -1.0 if ph == 0 else -1.0], ph)
+            lvl, st = orc.control_step(p, ph, lad, [1], [1], [0], [ex["wait"]], [ex["slo"]])
+            assert st[0] == 0
+            assert lvl[0] == expect, (ex["cite"], pred0)
+
+
+def test_pin4_select_frequency_examples(orc):
+    lad = np.array([0, 1], np.uint16)
+    for ex in GOLD["select_frequency"]:
+        for ph in (0, 1):
+            p = _two_level_with_preds(ex["pred"], ph)
+            lvl, _ = orc.control_step(p, ph, lad, [5], [5], [ex["queue_len"]], [0.0], [ex["budget"]])
+            assert [1005, 1410][lvl[0]] == ex["expect_mhz"], ex["cite"]
+
+
+def _rand_snapshots(rng, n, p, phase):
+    load = rng.integers(1, 4000 if phase == 0 else 2000, n).astype(np.uint32)
+    kv = (load.astype(np.int64) * rng.integers(1, 800, n)).clip(max=2**31 - 1).astype(np.uint32)
+    q = np.where(rng.random(n) < 0.2, rng.integers(1, 9, n), 0).astype(np.uint32)
+    wait = rng.uniform(0, 800, n)
+    tgt = rng.uniform(5, 700 if phase == 0 else 150, n)
+    return load, kv, q, wait, tgt
+
+
+@pytest.mark.parametrize("phase", [0, 1])
+def test_pin4_minimality_brute_force_scan(orc, phase):
+    """EcoFreq = brute-force ascending scan over every level (acceptance 2);
+    the predictions come from EcoPred (pinned above), the scan is done here."""
+    p = synth.make_profile("L8")
+    rng = np.random.default_rng(7 + phase)
+    for lad in (np.array([0, 6, 13, 20, 27], np.uint16), np.arange(28, dtype=np.uint16),
+                np.array([27], np.uint16)):
+        load, kv, q, wait, tgt = _rand_snapshots(rng, 2500, p, phase)
+        lvl, st = orc.control_step(p, phase, lad, load, kv, q, wait, tgt)
+        assert (st == 0).all()
+        for i in range(len(load)):
+            if q[i] > 0:
+                exp = len(lad) - 1                              # backlog dominance
+            else:
+                b = max(0.0, tgt[i] - wait[i]) if phase == 0 else tgt[i]
+                preds = [orc.predict_ttft(p, int(L), int(load[i])) if phase == 0 else
+                         orc.predict_itl(p, int(L), int(load[i]), int(kv[i])) for L in lad]
+                feas = [k for k, v in enumerate(preds) if v <= b]
+                exp = feas[0] if feas else len(lad) - 1
+            assert lvl[i] == exp
+
+
+@pytest.mark.parametrize("phase", [0, 1])
+def test_pin4_slo_monotonicity(orc, phase):
+    """A lower SLO target never selects a lower frequency (north_star invariant)."""
+    rng = np.random.default_rng(11)
+    for prof in (synth.make_profile("L8"), synth.make_profile("B200")):
+        lad = np.arange(prof.k, dtype=np.uint16)
+        # also a deliberately non-monotone table: the invariant holds for any table
+        bad = synth.make_profile("L8")
+        bad.c2 = bad.c2.copy()
+        bad.c2[::3] += 15.0
+        bad.c1 = bad.c1.copy()
+        bad.c1[::2] += 40.0
+        for p in (prof, bad):
+            lad = np.arange(p.k, dtype=np.uint16)
+            load, kv, q, wait, tgt = _rand_snapshots(rng, 4000, p, phase)
+            l_hi, _ = orc.control_step(p, phase, lad, load, kv, q, wait, tgt)
+            l_lo, _ = orc.control_step(p, phase, lad, load, kv, q, wait, tgt * rng.uniform(0.2, 1.0, len(tgt)))
+            assert (l_lo >= l_hi).all()
+
+
+# ------------------------------------------------------------------ PIN-5 EcoRoute
+
+def _route(orc, p, lad, n, kv, req_in, tgt, delta, cursor=0, policy=0):
+    inst, case, st, cur = orc.route_batch(p, np.asarray(lad, np.uint16), len(n), np.array([n]),
+                                          np.array([kv]), [req_in], tgt, delta, policy, [cursor])
+    assert st[0] == 0
+    return int(inst[0]), int(case[0]), int(cur[0])
+
+
+def test_pin5_route_worked_examples(orc):
+    # (2) identical states, no crossing -> round robin alternation
+    p = flat_profile([1005, 1410], c2=[30.0, 25.0])
+    d0, c0, cur = _route(orc, p, [0, 1], [10, 10], [5000, 5000], 100, 60.0, INF_DELTA, cursor=0)
+    d1, c1, cur = _route(orc, p, [0, 1], [10, 10], [5000, 5000], 100, 60.0, INF_DELTA, cursor=cur)
+    assert (d0, d1, c0, c1) == (0, 1, 2, 2)
+    # A at 256 would cross to 1410, B at 200 stays 1005, Delta large -> B
+    T = 4
+    c2 = np.array([[30, 25], [50, 40], [70, 55], [90, 58]], float).ravel()   # row = tile
+    p = flat_profile([1005, 1410], c2=c2, T=T)
+    d, c, _ = _route(orc, p, [0, 1], [256, 200], [90000, 70000], 300, 60.0, INF_DELTA)
+    assert (d, c) == (1, 3)
+    # both cross, f' = 1410 and 1305 -> the 1305 instance (case 5)
+    p = flat_profile([1005, 1305, 1410], b2=[1.0e-3, 0.8e-3, 0.7e-3])
+    d, c, _ = _route(orc, p, [0, 1, 2], [1, 1], [59000, 50000], 19999, 60.0, INF_DELTA)
+    assert (d, c) == (1, 5)
+    # A stays 1410, B 1005 -> 1200, Delta = 150: g = 210 > 150 -> B (case 4)
+    p = flat_profile([1005, 1200, 1410], b2=[1.0e-3, 0.9e-3, 0.7e-3], c2=[0.0, 0.0, 0.0])
+    args = ([0, 1, 2], [1, 1], [80000, 59500], 1000, 60.0)
+    assert _route(orc, p, *args, 150)[:2] == (1, 4)
+    assert _route(orc, p, *args, 209)[:2] == (1, 4)
+    assert _route(orc, p, *args, 210)[:2] == (0, 3)     # g == Delta is inclusive ("<=")
+    assert _route(orc, p, *args, INF_DELTA)[:2] == (0, 3)
+
+
+def _route_second_impl(fnow, faft, delta, cursor):
+    """Independent re-statement of P:446-456 (cases 1-5) over the U/R partition."""
+    nd = len(fnow)
+    R = [d for d in range(nd) if faft[d] > fnow[d]]
+    U = [d for d in range(nd) if d not in R]
+    if not R:
+        m = min(fnow[d] for d in U)
+        S = [d for d in U if fnow[d] == m]
+        case = 1 if len(S) == 1 else 2
+    elif U:
+        g = min(fnow[d] for d in U) - min(faft[d] for d in R)
+        if g <= delta:
+            m = min(fnow[d] for d in U)
+            S, case = [d for d in U if fnow[d] == m], 3
+        else:
+            m = min(fnow)
+            S, case = [d for d in range(nd) if fnow[d] == m], 4
+    else:
+        m = min(faft)
+        S, case = [d for d in range(nd) if faft[d] == m], 5
+    d = min(S, key=lambda x: (x - cursor) % nd)
+    new_cursor = (d + 1) % nd if len(S) >= 2 else cursor
+    return d, case, new_cursor
+
+
+def test_pin5_route_equivalence_random_states(orc):
+    """EcoRoute vs an independent case analysis on >= 10^4 random 2-8 instance states,
+    including g == Delta exactly (acceptance 3)."""
+    p = synth.make_profile("L8")
+    rng = np.random.default_rng(5)
+    lad = np.array([0, 6, 13, 20, 27], np.uint16)
+    mhz = p.mhz[lad]
+    tgt = 45.0
+    checked_eq = 0
+    for it in range(10000):
+        nd = int(rng.integers(2, 9))
+        n = rng.integers(0, 600, nd)
+        kv = n * rng.integers(1, 600, nd)
+        req_in = int(rng.integers(1, 3000))
+        cursor = int(rng.integers(nd))
+        fnow, faft = [], []
+        for d in range(nd):
+            def low(nn, kk):
+                pr = [orc.predict_itl(p, int(L), int(nn), int(kk)) for L in lad]
+                f = [k for k, v in enumerate(pr) if v <= tgt]
+                return f[0] if f else len(lad) - 1
+            fnow.append(int(mhz[0]) if n[d] == 0 else int(mhz[low(n[d], kv[d])]))
+            faft.append(int(mhz[low(n[d] + 1, kv[d] + req_in + 1)]))
+        R = [d for d in range(nd) if faft[d] > fnow[d]]
+        U = [d for d in range(nd) if d not in R]
+        if R and U and it % 3 == 0:
+            delta = min(fnow[d] for d in U) - min(faft[d] for d in R)   # g == Delta exactly
+            checked_eq += 1
+        else:
+            delta = int(rng.choice([0, 95, 150, 300, INF_DELTA]))
+        exp = _route_second_impl(fnow, faft, delta, cursor)
+        got = _route(orc, p, lad, list(n), list(kv), req_in, tgt, delta, cursor)
+        assert got == exp, (n, kv, req_in, delta, cursor, fnow, faft)
+    assert checked_eq > 100
+
+
+def test_pin5_route_round_robin_policy(orc):
+    for ex in GOLD["route_prefill"]:
+        nd = ex["n_instances"]
+        p = flat_profile([1005, 1410])
+        cur, seq = 0, []
+        for _ in ex["sequence"]:
+            d, c, cur = _route(orc, p, [0, 1], [5] * nd, [500] * nd, 10, 60.0, 150, cursor=cur, policy=1)
+            seq.append(d)
+            assert c == 0
+        assert seq == ex["sequence"], ex["cite"]
+
+
+# ------------------------------------------------------------------ PIN-6 power / energy
+
+def test_pin6_power_and_energy(orc):
+    p = synth.make_profile("L8")
+    assert orc.busy_power(p, 1, 5, 0) == p.p_idle
+    assert orc.busy_power(p, 0, p.level_of(1305), 10**9) == p.tdp      # S:212 / P:174 clip at 400 W
+    k5, k14 = p.level_of(1005), p.level_of(1410)
+    r = (orc.busy_power(p, 1, k5, 256) - p.p_idle) / (orc.busy_power(p, 1, k14, 256) - p.p_idle)
+    assert abs(r - (1005 / 1410) ** 1.5) < 1e-12 and abs(r - 0.601756) < 1e-6
+    for ex in GOLD["energy"]:
+        assert orc.interval_energy(ex["power_w"], ex["dur_ms"]) == ex["expect_j"], ex["cite"]
+    # busy power non-decreasing in f and in load, within [p_idle, tdp]
+    for ph in (0, 1):
+        prev = None
+        for k in range(p.k):
+            w = [orc.busy_power(p, ph, k, x) for x in (0, 1, 10, 100, 1000, 10000)]
+            assert all(p.p_idle <= v <= p.tdp for v in w) and w == sorted(w)
+            if prev is not None:
+                assert all(a <= b for a, b in zip(prev, w))
+            prev = w
+
+
+# ------------------------------------------------------------------ helpers for simulate
+
+def run(orc, arrival, in_len, out_len, prof, slo, lay, ladder, D=None, **kw):
+    arrival = np.asarray(arrival, float)
+    if D is None:
+        D = float(arrival[-1]) if len(arrival) else 0.0
+    return orc.simulate(arrival, in_len, out_len, D, slo, lay, ladder, prof, **kw)
+
+
+def total_energy(r):
+    return r["e_prefill_busy_j"] + r["e_prefill_idle_j"] + r["e_decode_busy_j"] + r["e_decode_idle_j"]
+
+
+# ------------------------------------------------------------------ PIN-7 U-shape closed form
+
+def _ushape_profile(f_grid, f_ref, T_ref, beta, alpha, D_dyn, p_idle, nbt):
+    x = np.asarray(f_grid, float) / f_ref
+    tt = T_ref * x ** -(1.0 - beta)          # eq:prefill-f / eq:decode-f (A28)
+    a1 = tt / (2.0 * nbt)                    # half of the time scales with N_bt ...
+    c1 = tt / 2.0                            # ... half is the intercept: a1*nbt + c1 = tt
+    u = nbt / (nbt + 1024.0)
+    dyn_p = D_dyn * x ** (1.0 + alpha) / u   # so that u * DYN = D x^(1+alpha)   (eq:P-f)
+    K = len(f_grid)
+    return custom_profile(f_grid, a1, c1, np.zeros(K), np.zeros(K), np.ones(K),
+                          np.concatenate([dyn_p, dyn_p]), p_idle=p_idle, tdp=1e9)
+
+
+@pytest.mark.parametrize("beta,D_dyn,grid_lo", [(0.0, 30.0, 705), (0.8, 12.0, 705), (1.0, 200.0, 1005),
+                                                 (0.3, 4.0, 1005)])
+def test_pin7_ushape_closed_form(orc, beta, D_dyn, grid_lo):
+    """Energy of a fixed batch vs frequency follows E(f) = T(f) P(f): U-shaped with the
+    continuous minimiser f* = f_ref [(1-beta) p_idle / ((alpha+beta) D)]^(1/(1+alpha))
+    (eq:P-f..eq:decode-f P:186-190)."""
+    f_ref, alpha, p_idle, T_ref, nbt = 1410.0, 0.5, 60.0, 400.0, 2000
+    grid = np.arange(grid_lo, 1411, 15)
+    prof = _ushape_profile(grid, f_ref, T_ref, beta, alpha, D_dyn, p_idle, nbt)
+    E = []
+    for k in range(len(grid)):
+        r = run(orc, [0.0], [nbt], [1], prof, Slo(1e9, 1e9), Layout(1, 1, max_batch_tokens=8192),
+                [k], D=0.0)
+        x = grid[k] / f_ref
+        closed = T_ref * x ** -(1 - beta) * (p_idle + D_dyn * x ** (1 + alpha)) / 1000.0
+        assert abs(r["e_prefill_busy_j"] - closed) <= 1e-12 * closed
+        E.append(r["e_prefill_busy_j"])
+    E = np.array(E)
+    k_min = int(np.argmin(E))
+    if beta == 1.0:
+        assert k_min == 0                                   # E increasing: lowest level wins
+        return
+    fstar = f_ref * ((1 - beta) * p_idle / ((alpha + beta) * D_dyn)) ** (1 / (1 + alpha))
+    if grid[0] < fstar < grid[-1]:
+        lo = np.searchsorted(grid, fstar) - 1
+        assert k_min in (lo, lo + 1), (fstar, grid[k_min])
+        assert 0 < k_min < len(grid) - 1                    # strict interior minimum (A38)
+    elif fstar <= grid[0]:
+        assert k_min == 0
+    else:
+        assert k_min == len(grid) - 1
+
+
+def test_pin7_sweet_point_1005_interior(orc):
+    """Parameters placing f* near 1005 MHz on a grid extending below 1005 give the paper's
+    1005-MHz energy sweet point as a strict interior minimum (A38)."""
+    f_ref, alpha, beta, p_idle = 1410.0, 0.5, 0.5, 60.0
+    x = 1005.0 / f_ref
+    D_dyn = (1 - beta) * p_idle / ((alpha + beta) * x ** (1 + alpha))   # puts f* at 1005
+    grid = np.arange(705, 1411, 15)
+    prof = _ushape_profile(grid, f_ref, 400.0, beta, alpha, D_dyn, p_idle, 2000)
+    E = [run(orc, [0.0], [2000], [1], prof, Slo(1e9, 1e9), Layout(1, 1), [k], D=0.0)["e_prefill_busy_j"]
+         for k in range(len(grid))]
+    assert grid[int(np.argmin(E))] == 1005
+
+
+# ------------------------------------------------------------------ PIN-8 single request
+
+def test_pin8_single_request_hand_trace(orc):
+    """1P1D, one isolated request: TTFT = T_ttft(k*, in), ITL mean = arithmetic series
+    of eq:pred-itl over N_kv = in+1 .. in+out-1 (one level, one tile)."""
+    p = synth.make_profile("L8_LINEAR")
+    k = p.level_of(1200)
+    in_len, out_len, D = 500, 101, 60000.0
+    r = run(orc, [0.0], [in_len], [out_len], p, Slo(600, 60), Layout(1, 1), [k], D=D)
+    ttft = p.a1[k] * in_len + p.c1[k]
+    assert abs(r["sum_ttft_ms"] - ttft) <= 1e-12 * ttft
+    itl = p.a2[k] + p.c2[k] + p.b2[k] * (in_len + 1 + (out_len - 2) / 2.0)
+    assert abs(r["sum_itl_mean_ms"] - itl) <= 1e-9 * itl
+    assert r["steps_ctrl"] == 1 + (out_len - 1) and r["steps_route"] == 1
+    assert r["n_ttft_ok"] == r["n_itl_ok"] == r["n_both_ok"] == 1
+    # energy: busy = P * time per phase; idle = p_idle * (horizon - busy)
+    u_p = in_len / (in_len + p.u_half_prefill)
+    P_pre = min(p.tdp, p.p_idle + u_p * p.dyn[k])
+    assert abs(r["e_prefill_busy_j"] - P_pre * ttft / 1000) <= 1e-12 * r["e_prefill_busy_j"]
+    P_dec = min(p.tdp, p.p_idle + (1 / (1 + p.u_half_decode)) * p.dyn[p.k + k])
+    dec_time = itl * (out_len - 1)
+    assert abs(r["e_decode_busy_j"] - P_dec * dec_time / 1000) <= 1e-9 * r["e_decode_busy_j"]
+    assert r["horizon_ms"] == D
+    assert abs(r["e_prefill_idle_j"] - p.p_idle * (D - ttft) / 1000) <= 1e-9
+    assert abs(r["e_decode_idle_j"] - p.p_idle * (D - dec_time) / 1000) <= 1e-6
+
+
+def test_pin8_empty_workload(orc):
+    """Empty trace -> zero tokens, idle-only energy p_idle x horizon."""
+    p = synth.make_profile("L8")
+    r = orc.simulate(np.zeros(0), np.zeros(0), np.zeros(0), 5000.0, Slo(600, 60), Layout(2, 2), [0, 27], p)
+    assert r["status"] == 0 and r["n_requests"] == 0 and r["steps_ctrl"] == 0
+    assert r["e_prefill_busy_j"] == 0 and r["e_prefill_idle_j"] == 2 * 60.0 * 5000 / 1000
+    assert r["decision_hash"] == 0
+
+
+# ------------------------------------------------------------------ PIN-9 M/D/1 queueing core
+
+def test_pin9_md1_pollaczek_khinchine(orc):
+    """1P1D, K=1, fixed in-length L, B = L (one request per batch), out = 1, Poisson arrivals:
+    the prefill instance is an M/D/1 queue; mean TTFT -> S + lam S^2 / (2 (1 - lam S))."""
+    L, S = 500, 50.0
+    p = flat_profile([1005], a1=[S / L], c1=[0.0])
+    lam = 0.01                                            # per ms: rho = 0.5
+    rng = np.random.default_rng(2509)
+    n = 100000
+    arr = np.cumsum(rng.exponential(1 / lam, n))
+    d = {}
+    r = run(orc, arr, np.full(n, L), np.ones(n), p, Slo(1e9, 1e9), Layout(1, 1, max_batch_tokens=L),
+            [0], diag=d)
+    ttft = d["req_tfirst"] - arr
+    assert abs(r["sum_ttft_ms"] / n - ttft.mean()) < 1e-9 * ttft.mean()
+    expect = S + lam * S * S / (2 * (1 - lam * S))       # = 75 ms
+    bm = ttft[: n // 50 * 50].reshape(50, -1).mean(axis=1)
+    se = bm.std(ddof=1) / math.sqrt(50)
+    assert abs(ttft.mean() - expect) < 4 * se + 0.5, (ttft.mean(), expect, se)
+    # deterministic service: every TTFT >= S, and a request arriving to an empty system waits 0
+    assert ttft.min() >= S - 1e-9
+
+
+# ------------------------------------------------------------------ PIN-10 bookkeeping invariants
+
+def _sample_workloads():
+    w3 = synth.build_config("C3", scenarios=[0, 40, 100, 200], duration_scale=0.25)
+    w4 = synth.build_config("C4", scenarios=[5, 700, 1500, 3000, 4095], duration_scale=0.1)
+    return [w3, w4]
+
+
+def test_pin10_invariants(orc):
+    for w in _sample_workloads():
+        for i in range(w.n):
+            s = {k: int(v[i]) for k, v in w.scen.items()}
+            a, inl, outl, D = w.traces.trace(s["trace_id"])
+            lay, slo, lad, prof = w.layouts[s["layout_id"]], w.slos[s["slo_id"]], w.grids[s["grid_id"]], w.profiles[0]
+            d = {}
+            r = orc.simulate(a, inl, outl, D, slo, lay, lad, prof, s["hash_seed"], diag=d)
+            r2 = orc.simulate(a, inl, outl, D, slo, lay, lad, prof, s["hash_seed"])
+            assert r.tobytes() == r2.tobytes()                              # determinism
+            assert r["status"] == 0
+            n = len(a)
+            # causality: arrival < first token <= last token
+            assert (d["req_tfirst"] > a).all() and (d["req_tdone"] >= d["req_tfirst"]).all()
+            assert (d["req_tdone"][outl > 1] > d["req_tfirst"][outl > 1]).all()
+            # token conservation: decode iterations generate sum(out - 1) tokens
+            assert int(d["tokens"].sum()) == int((outl.astype(np.int64) - 1).sum())
+            # KV capacity never exceeded
+            assert (d["kv_peak"] <= lay.kv_capacity).all()
+            # counts: every request routed once (eq:formulation-routing-end P:308), steps (A34)
+            assert r["steps_route"] == int((outl > 1).sum())
+            assert r["steps_ctrl"] == int(d["iters"].sum())
+            assert (d["req_decode"][outl > 1] >= 0).all() and (d["req_decode"][outl > 1] < lay.n_d).all()
+            # attainment counts re-derived from per-request times
+            ttft = d["req_tfirst"] - a
+            assert r["n_ttft_ok"] == int((ttft <= slo.ttft).sum())
+            itl_ok = (outl == 1) | (d["req_itl"] <= slo.itl)
+            assert r["n_itl_ok"] == int(itl_ok.sum())
+            assert r["n_both_ok"] == int((itl_ok & (ttft <= slo.ttft)).sum())
+            assert abs(r["sum_ttft_ms"] - ttft.sum()) <= 1e-9 * r["sum_ttft_ms"]
+            # busy time per phase bounded by instances x horizon; idle energy = p_idle x idle time
+            H = r["horizon_ms"]
+            assert H >= D and r["busy_ms_prefill"] <= lay.n_p * H and r["busy_ms_decode"] <= lay.n_d * H
+            assert abs(r["e_prefill_idle_j"] - prof.p_idle * (lay.n_p * H - r["busy_ms_prefill"]) / 1000) < 1e-6 * H
+            assert abs(r["e_decode_idle_j"] - prof.p_idle * (lay.n_d * H - r["busy_ms_decode"]) / 1000) < 1e-6 * H
+            # busy energy between p_idle and TDP times busy time (energy additivity bounds)
+            for ph in ("prefill", "decode"):
+                e, b = r[f"e_{ph}_busy_j"], r[f"busy_ms_{ph}"]
+                assert prof.p_idle * b / 1000 * (1 - 1e-12) <= e <= prof.tdp * b / 1000 * (1 + 1e-12)
+            assert 0 <= r["top_level_ms"] <= r["busy_ms_prefill"] + r["busy_ms_decode"] + 1e-6
+            del n
+
+
+def test_pin10_prefill_batch_and_round_robin(orc):
+    ex = GOLD["prefill_batch"][0]
+    p = flat_profile([1005], a1=[0.01], c1=[1.0])
+    d = {}
+    q = ex["queue_in"]
+    r = run(orc, [0.0] * len(q), q, [1] * len(q), p, Slo(1e9, 1e9), Layout(1, 1, max_batch_tokens=ex["budget"]),
+            [0], diag=d, iter_cap=10)
+    t_b1 = 0.01 * ex["n_bt"] + 1.0
+    assert list(d["req_tfirst"]) == [t_b1, t_b1, t_b1 + (0.01 * q[2] + 1.0)], ex["cite"]
+    ex = GOLD["prefill_batch"][1]
+    r = run(orc, [0.0], ex["queue_in"], [1], p, Slo(1e9, 1e9), Layout(1, 1, max_batch_tokens=ex["budget"]), [0])
+    assert r["sum_ttft_ms"] == 0.01 * ex["n_bt"] + 1.0 and r["steps_ctrl"] == 1
+    # prefill round robin by arrival: isolated requests alternate instances
+    for ex in GOLD["route_prefill"]:
+        m = len(ex["sequence"])
+        d = {}
+        run(orc, np.arange(m) * 1000.0, [100] * m, [1] * m, p, Slo(1e9, 1e9), Layout(ex["n_instances"], 1),
+            [0], diag=d, iter_cap=64)
+        assert list(d["iter_inst"]) == ex["sequence"], ex["cite"]
+
+
+def test_pin10_kv_capacity_error(orc):
+    """A request that can never fit an empty decode instance is a scenario error (A20)."""
+    p = synth.make_profile("L8")
+    r = run(orc, [0.0, 1.0], [1000, 50000], [5, 5], p, Slo(600, 60), Layout(1, 1, kv_capacity=40000), [0, 27])
+    assert r["status"] == 1 and r["n_requests"] == 2 and r["steps_ctrl"] == 0 and r["e_decode_busy_j"] == 0
+
+
+# ------------------------------------------------------------------ PIN-11 brute force
+
+def test_pin11a_frequency_brute_force(orc):
+    """Exact frequency-control formulation on a tiny trace: enumerate every level
+    for every controller decision; the min-total-energy sequence meeting every iteration's
+    SLO target equals EcoFreq's choice on a grid right of the energy minimum."""
+    p = synth.make_profile("L8")
+    lad = np.array([p.level_of(f) for f in (1005, 1200, 1410)], np.uint16)
+    arr, inl, outl = [0.0, 10000.0], [300, 300], [3, 3]
+    slo, lay, D = Slo(42.0, 21.9), Layout(1, 1), 30000.0
+    d = {}
+    eco = orc.simulate(np.array(arr), inl, outl, D, slo, lay, lad, p, diag=d, iter_cap=64)
+    n_dec = int(eco["steps_ctrl"])
+    assert n_dec == 6
+    best = None
+    for combo in itertools.product(range(3), repeat=n_dec):
+        dd = {}
+        r = orc.simulate(np.array(arr), inl, outl, D, slo, lay, lad, p, diag=dd, iter_cap=64,
+                         force_level=np.array(combo))
+        if not (dd["iter_dur"] <= dd["iter_target"]).all():
+            continue
+        e = total_energy(r)
+        if best is None or e < best[0]:
+            best = (e, combo)
+    assert best is not None
+    assert tuple(d["iter_level"]) == best[1]
+    assert abs(total_energy(eco) - best[0]) <= 1e-12 * best[0]
+    assert set(d["iter_level"]) == {1}        # 1005 infeasible, 1200 feasible everywhere
+
+
+def test_pin11b_routing_brute_force(orc):
+    """Routing assignment formulation on a tiny trace: enumerate all N_D^m decode
+    assignments. EcoRoute's own assignment replays to an identical record; the optimum is
+    reported (EcoRoute is a heuristic, not claimed optimal)."""
+    p = synth.make_profile("L8")
+    rng = np.random.default_rng(3)
+    m = 9
+    arr = np.sort(rng.uniform(0, 2000, m))
+    inl = rng.integers(50, 3000, m)
+    outl = rng.integers(5, 60, m)
+    lad = np.array([0, 6, 13, 20, 27], np.uint16)
+    slo, lay = Slo(400, 25.5), Layout(1, 2, delta_mhz=150)
+    d = {}
+    eco = orc.simulate(arr, inl, outl, 5000.0, slo, lay, lad, p, diag=d)
+    rep = orc.simulate(arr, inl, outl, 5000.0, slo, lay, lad, p, force_decode=d["req_decode"])
+    for f in eco.dtype.names:
+        if f != "decision_hash":
+            assert eco[f] == rep[f], f
+    energies = []
+    for assign in itertools.product(range(2), repeat=m):
+        r = orc.simulate(arr, inl, outl, 5000.0, slo, lay, lad, p, force_decode=np.array(assign))
+        energies.append(total_energy(r))
+    opt = min(energies)
+    assert opt <= total_energy(eco) + 1e-9
+    assert len(set(np.round(energies, 9))) > 1       # the assignment matters on this trace
+    print(f"pin11b: EcoRoute energy {total_energy(eco):.3f} J, optimum {opt:.3f} J")
+
+
+# ------------------------------------------------------------------ PIN-13 static mode
+
+def test_pin13_static_frequency(orc):
+    """K = 1 ladders are the static-frequency baselines: every decision is the top
+    level; static 1410 has lower latency and higher energy than static 1005."""
+    w = synth.build_config("C4", scenarios=[2 * 128 + 3], duration_scale=0.2)   # lam = 20
+    a, inl, outl, D = w.traces.trace(0)
+    p = w.profiles[0]
+    recs = {}
+    for f in (1005, 1410):
+        lay = Layout(2, 2, policy=1)
+        r = orc.simulate(a, inl, outl, D, w.slos[0], lay, [p.level_of(f)], p)
+        assert r["top_level_ms"] == r["busy_ms_prefill"] + r["busy_ms_decode"] or \
+            abs(r["top_level_ms"] - (r["busy_ms_prefill"] + r["busy_ms_decode"])) < 1e-6
+        recs[f] = r
+    assert recs[1410]["sum_ttft_ms"] < recs[1005]["sum_ttft_ms"]
+    assert recs[1410]["sum_itl_mean_ms"] < recs[1005]["sum_itl_mean_ms"]
+    assert total_energy(recs[1410]) > total_energy(recs[1005])
+
+
+# ------------------------------------------------------------------ PIN-14 behaviour
+
+def test_pin14_boundary_preservation(orc):
+    """Two decode instances, boundary 256, sustained concurrency ~540 (fig:bs-time
+    P:655-661; acceptance 4): EcoRoute keeps one instance at n_req <= 256 for >= 90% of
+    its busy time, round robin for <= 10%; EcoRoute's decode energy is lower, ISAR within 2 pp."""
+    T = 6
+    c2 = np.array([[30, 25], [30, 25], [45, 35], [45, 35], [60, 38], [60, 38]], float).ravel()
+    dyn = np.array([300.0, 400.0, 150.0, 238.0])
+    p = custom_profile([1005, 1410], [1e-4, 1e-4], [1.0, 1.0], np.zeros(2 * T), np.zeros(2 * T), c2, dyn)
+    lam = 0.1                                     # requests per ms: ~700 concurrent at steady state
+    n = 14000
+    arr = np.arange(n) / lam
+    out = np.full(n, 200)
+    res = {}
+    for pol in (0, 1):
+        d = {}
+        r = run(orc, arr, np.full(n, 100), out, p, Slo(1e4, 40.0), Layout(1, 2, policy=pol, delta_mhz=INF_DELTA),
+                [0, 1], diag=d, boundary=256)
+        frac = d["time_le_boundary"] / d["time_busy"]
+        res[pol] = (r, frac)
+    eco, rr = res[0], res[1]
+    assert eco[1].max() >= 0.90, eco[1]
+    assert rr[1].max() <= 0.10, rr[1]
+    assert eco[0]["e_decode_busy_j"] < rr[0]["e_decode_busy_j"]
+    assert abs(eco[0]["n_itl_ok"] - rr[0]["n_itl_ok"]) <= 0.02 * n

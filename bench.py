@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark: scenario-steps/sec (EcoFreq controller + EcoRoute router decisions) of the
+batched VoltanaLLM policy evaluation on B200 (BASELINE.json metric).
+
+Workload (BASELINE configs[3], "SLO x arrival-rate x seed sweep, 4096 scenarios"): C4 —
+4096 scenarios = 4 SLO x 8 Poisson rates x 128 seeds, 2P2D, 5-level ladder, Delta = 150,
+LLaMA-3.1-8B-shaped profile, ShareGPT-like synthetic traces of 600 s. One step = one pass
+of the whole hot path: K1 fits the EcoPred profile from 2M synthetic profiling samples,
+then K4 simulates all 4096 scenarios with the fitted tables (every controller and router
+decision, energy integration, per-scenario records); for N > 1 the records are
+all-gathered over NCCL. Weak scaling: rank r sweeps its own seed block (4096 scenarios
+per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "scenario-steps/sec (ctrl+router decisions)"
+UNIT = "steps/s"
+CONFIG_NAME = "C4"
+N_SAMPLES = 2_000_000
+FP64_LANES_PER_SM = 64          # B200 FP64 (non-tensor): 37 TFLOPS FMA = 148 SMs x 64 lanes x 2 x 1.965 GHz
+N_SM = 148
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1024, help="scenarios in the oracle sample")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload_config():
+    return {"workload": "C4: 4096 scenarios/GPU = 4 SLO x 8 Poisson rates x 128 seeds, 2P2D, 5-level ladder "
+                        "[1005..1410] MHz, Delta=150, LLaMA-3.1-8B-shaped profile fitted from 2M samples, "
+                        "ShareGPT-like traces of 600 s",
+            "scenarios_per_gpu": 4096, "l2": "flushed between timed steps (256 MiB write); traces 357 MB > L2"}
+
+
+# ---------------------------------------------------------------------------- oracle (CPU)
+_ORC_W = None
+
+
+def _orc_init():
+    import oracle
+    oracle.lib()
+
+
+def _orc_run(idx):
+    import oracle
+    t0 = time.perf_counter()
+    r = oracle.simulate_workload(_ORC_W, idx)
+    dt = time.perf_counter() - t0
+    return int((r["steps_ctrl"] + r["steps_route"]).sum()), dt
+
+
+def oracle_timed(w, idx, cores):
+    """Run the oracle over scenarios idx on `cores` processes; returns (steps, wall_s)."""
+    import multiprocessing as mp
+    global _ORC_W
+    _ORC_W = w
+    chunks = [list(c) for c in np.array_split(np.asarray(idx), max(1, cores * 4)) if len(c)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores, initializer=_orc_init) as pool:
+        pool.map(_orc_run, [chunks[0][:1]])             # warm the workers
+        t0 = time.perf_counter()
+        res = pool.map(_orc_run, chunks)
+        wall = time.perf_counter() - t0
+    return sum(s for s, _ in res), wall
+
+
+def cpu_baseline(w, n_sample):
+    cores = os.cpu_count() or 1
+    idx = np.arange(0, w.n, max(1, w.n // n_sample))[:n_sample]
+    steps, wall = oracle_timed(w, idx, cores)
+    return {"value": steps / wall, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{len(idx)} of {w.n} C4 scenarios (every {max(1, w.n // n_sample)}th, all 8 rates x 4 SLOs), "
+                      f"{steps} decisions in {wall:.2f} s wall over {cores} processes"}
+
+
+# ---------------------------------------------------------------------------- clocks
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": reasons,
+                "samples": len(rows), "power_w_max": max(float(r[3]) for r in rows)}
+
+
+# ---------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from synth.samples import profile_samples
+    import paper_2509_04827_b200 as vt
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+
+    w = synth.build_config(CONFIG_NAME, seed_block=rank)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(w, args.cpu_sample)
+
+    prof = w.profiles[0]
+    s = profile_samples(prof, N_SAMPLES // (prof.k * (1 + 16)), N_SAMPLES // (prof.k * (1 + 16)),
+                        noise_sigma=0.02, seed=rank)
+    u32 = lambda a: torch.from_numpy(np.ascontiguousarray(a).view(np.int32)).to(dev).view(torch.uint32)
+    samp = dict(phase=torch.from_numpy(s["phase"]).to(dev),
+                level=torch.from_numpy(s["level"].view(np.int16)).to(dev).view(torch.uint16),
+                n_bt=u32(s["n_bt"]), n_req=u32(s["n_req"]), n_kv=u32(s["n_kv"]),
+                lat_ms=torch.from_numpy(s["lat_ms"]).to(dev))
+    n_samp = int(samp["lat_ms"].numel())
+    fit = vt.fit_profile(samp["phase"], samp["level"], samp["n_bt"], samp["n_req"], samp["n_kv"], samp["lat_ms"],
+                         prof.k, prof.n_tiles, prof.tile_w, 0.0)
+    torch.cuda.synchronize()
+    assert (fit["cell_status"].cpu().numpy() == 0).all(), "profile fit failed"
+    dprof = vt.DeviceProfile.from_fit(fit, prof.mhz, prof.dyn, prof.p_idle, prof.tdp, prof.u_half_prefill,
+                                      prof.u_half_decode, prof.n_tiles, prof.tile_w, dev)
+    wl = vt.DeviceWorkload(w.traces, w.slos, w.layouts, w.grids, [dprof], w.scen, device=dev)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+    gathered = torch.empty((world * wl.n, 128), dtype=torch.uint8, device=dev) if world > 1 else None
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        vt.fit_profile(samp["phase"], samp["level"], samp["n_bt"], samp["n_req"], samp["n_kv"], samp["lat_ms"],
+                       prof.k, prof.n_tiles, prof.tile_w, 0.0, workspace=fit["workspace"], out=fit)
+        launches = vt.last_launch_count()
+        if ev:
+            ev[1].record(stream)
+        wl.launch()
+        launches += vt.last_launch_count()
+        if ev:
+            ev[2].record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, wl.out)
+        if ev:
+            ev[3].record(stream)
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rec = wl.records()
+    assert (rec["status"] == 0).all(), "scenario errors in the bench workload"
+    steps_per_pass = int((rec["steps_ctrl"] + rec["steps_route"]).sum())
+
+    # ---------------- timed region
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(dev.index)
+    clk.start()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    launches = 0
+    for k in range(args.steps):
+        flush.fill_(k & 0xFF)                           # L2 flush between timed steps (not timed)
+        launches += step(evs[k])
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    t_step = [e[0].elapsed_time(e[3]) for e in evs]
+    t_fit = [e[0].elapsed_time(e[1]) for e in evs]
+    t_sim = [e[1].elapsed_time(e[2]) for e in evs]
+    t_gather = [e[2].elapsed_time(e[3]) for e in evs]
+    dev_ms = float(sum(t_step))
+    tot_steps = steps_per_pass * args.steps
+    if world > 1:
+        x = torch.tensor([dev_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        dev_ms = float(x.item())
+        y = torch.tensor([tot_steps], dtype=torch.int64, device=dev)
+        dist.all_reduce(y, op=dist.ReduceOp.SUM)
+        tot_steps = int(y.item())
+    value = tot_steps / (dev_ms / 1000.0)
+
+    # ---------------- end to end from pinned host memory (public API), per step: H2D + kernels + D2H
+    wl.pin_host()
+    samp_host = {k: v.cpu().pin_memory() for k, v in samp.items()}
+    h2d = d2h = 0
+    e2e_ms = 0.0
+    e_steps = max(1, args.e2e_steps)
+    if world > 1:
+        dist.barrier()
+    for k in range(e_steps):
+        flush.fill_(k & 0xFF)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        h2d = wl.stage_inputs()
+        for kk, v in samp.items():
+            v.copy_(samp_host[kk], non_blocking=True)
+            h2d += v.numel() * v.element_size()
+        step()
+        d2h = wl.fetch_records()
+        b.record(stream)
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    e2e_steps_total = steps_per_pass * e_steps
+    if world > 1:
+        x = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        e2e_ms = float(x.item())
+        e2e_steps_total *= world
+    e2e = {"value": e2e_steps_total / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(d2h),
+           "path": "DeviceWorkload.stage_inputs (pinned H2D of traces+scenario tables) -> fit_profile -> "
+                   "simulate -> fetch_records (D2H)"}
+
+    # ---------------- roofline of the dominant kernel (K4 simulate): FP64 ALU
+    K = len(w.grids[0])
+    nd = w.layouts[0].n_d
+    pre = rec["prefill_iters"].astype(np.int64)
+    dec = rec["steps_ctrl"].astype(np.int64) - pre
+    flops = int((pre * 2 * K + dec * 4 * K + rec["steps_route"].astype(np.int64) * 8 * nd * K).sum())
+    sim_s = statistics.mean(t_sim) / 1000.0
+    achieved = flops / sim_s / 1e12
+    sm_mhz = 1965.0
+    peak = N_SM * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12
+    trace_bytes = int(w.traces.arrival.nbytes + w.traces.in_len.nbytes + w.traces.out_len.nbytes)
+    comp_bytes = trace_bytes + 128 * wl.n
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": "vt::simulate_kernel<2,2>",
+            "note": "algorithmic FP64 ops of the decision procedure (prefill ctrl 2K, decode ctrl 4K, route "
+                    "8*N_D*K per decision) / mean kernel time; peak = 148 SM x 64 FP64 lanes x 1965 MHz "
+                    "(non-FMA ops); the kernel is latency/issue-bound on the serial event loop",
+            "hbm_compulsory": {"bytes": comp_bytes, "gbs": comp_bytes / sim_s / 1e9,
+                               "frac_of_measured_hbm": comp_bytes / sim_s / 1e9 / peaks["hbm_gbs"]}}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; DESIGN.md input recipe)",
+           "config": dict(workload_config(), parallelism=f"scenario-sharded x{world}"),
+           "decisions_per_step": tot_steps // args.steps,
+           "kernel_ms": {"fit_profile": statistics.mean(t_fit), "simulate": statistics.mean(t_sim),
+                         "all_gather": statistics.mean(t_gather) if world > 1 else 0.0},
+           "fit_samples": n_samp, "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roof,
+           "cpu_baseline": cpu}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import synth
+    w = synth.build_config(CONFIG_NAME, seed_block=0)
+    cores = os.cpu_count() or 1
+    per_step = 256
+    order = np.random.default_rng(0).permutation(w.n)
+    times, steps = [], []
+    for k in range(args.warmup + args.steps):
+        idx = np.sort(order[(k * per_step) % w.n:][:per_step])
+        s, wall = oracle_timed(w, idx, cores)
+        if k >= args.warmup:
+            times.append(wall)
+            steps.append(s)
+    value = sum(steps) / sum(times)
+    sample = f"{per_step} random C4 scenarios per step (disjoint across steps) over {cores} processes"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(times),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; DESIGN.md input recipe)",
+           "config": dict(workload_config(), parallelism="host cores"),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -484,6 +484,11 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
     res->n_ttft_ok = (uint32_t)n_ttft_ok;
     res->n_itl_ok = (uint32_t)n_itl_ok;
     res->n_both_ok = (uint32_t)n_both;
+    {
+      uint64_t pi = 0;
+      for (int q = 0; q < NP; ++q) pi += P[q].iters;
+      res->prefill_iters = (uint32_t)pi;
+    }
     res->steps_ctrl = steps_ctrl;
     res->steps_route = steps_route;
     res->decision_hash = h;

@@ -53,7 +53,7 @@ typedef struct {
 
 /* 128-byte per-scenario result record. */
 typedef struct {
-  uint32_t status, n_requests, n_ttft_ok, n_itl_ok, n_both_ok, reserved;
+  uint32_t status, n_requests, n_ttft_ok, n_itl_ok, n_both_ok, prefill_iters;
   uint64_t steps_ctrl, steps_route, decision_hash;
   double sum_ttft_ms, sum_itl_mean_ms, e_prefill_busy_j, e_prefill_idle_j,
          e_decode_busy_j, e_decode_idle_j, busy_ms_prefill, busy_ms_decode,

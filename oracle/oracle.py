@@ -19,7 +19,7 @@ FIT_OK, FIT_INHERITED, FIT_EMPTY, FIT_DEGENERATE = 0, 1, 2, 3
 
 RESULT_DTYPE = np.dtype([
     ("status", "<u4"), ("n_requests", "<u4"), ("n_ttft_ok", "<u4"), ("n_itl_ok", "<u4"),
-    ("n_both_ok", "<u4"), ("reserved", "<u4"),
+    ("n_both_ok", "<u4"), ("prefill_iters", "<u4"),
     ("steps_ctrl", "<u8"), ("steps_route", "<u8"), ("decision_hash", "<u8"),
     ("sum_ttft_ms", "<f8"), ("sum_itl_mean_ms", "<f8"), ("e_prefill_busy_j", "<f8"),
     ("e_prefill_idle_j", "<f8"), ("e_decode_busy_j", "<f8"), ("e_decode_idle_j", "<f8"),

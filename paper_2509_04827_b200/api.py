@@ -1,0 +1,272 @@
+"""Python binding of the four C-ABI calls (torch tensors in, torch tensors out).
+
+Argument marshalling only: every step of the path runs in libvoltana's CUDA
+kernels. torch provides device memory and the current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import RESULT_DTYPE, VOLTANA_DELTA_INF, check, lib  # noqa: F401
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev(x, dtype, device):
+    """Host array-like or tensor -> contiguous device tensor of `dtype`."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device)
+        if t.dtype != dtype:
+            t = t.to(dtype)
+        return t.contiguous()
+    a = np.ascontiguousarray(x)
+    np_dtype = {torch.float64: np.float64, torch.uint32: np.uint32, torch.uint64: np.uint64,
+                torch.uint16: np.uint16, torch.uint8: np.uint8, torch.int32: np.int32}[dtype]
+    return torch.from_numpy(np.ascontiguousarray(a, np_dtype)).to(device)
+
+
+def _require_cuda(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+
+
+class DeviceProfile:
+    """A calibrated profile with its tables in device memory (voltana_profile)."""
+
+    @classmethod
+    def from_fit(cls, fit: "FitOutput", mhz, dyn, p_idle, tdp, u_half_prefill, u_half_decode, n_tiles,
+                 tile_w=128, device="cuda"):
+        """Profile whose EcoPred tables are the (device-resident) output of fit_profile."""
+        self = cls.__new__(cls)
+        self.k = int(len(mhz))
+        self.n_tiles = int(n_tiles)
+        self.tile_w = int(tile_w)
+        self.mhz_host = np.asarray(mhz, np.int32).copy()
+        self.t = dict(mhz=_dev(mhz, torch.int32, device), a1=fit["a1"], c1=fit["c1"], a2=fit["a2"], b2=fit["b2"],
+                      c2=fit["c2"], dyn=_dev(dyn, torch.float64, device))
+        self.struct = _lib.Profile(self.k, self.n_tiles, self.tile_w, 0,
+                                   *[_p(self.t[n]) for n in ("mhz", "a1", "c1", "a2", "b2", "c2", "dyn")],
+                                   float(p_idle), float(tdp), float(u_half_prefill), float(u_half_decode))
+        return self
+
+    def __init__(self, prof, device="cuda"):
+        self.k = int(len(prof.mhz))
+        self.n_tiles = int(prof.n_tiles)
+        self.tile_w = int(prof.tile_w)
+        self.mhz_host = np.asarray(prof.mhz, np.int32).copy()
+        self.t = dict(mhz=_dev(prof.mhz, torch.int32, device), a1=_dev(prof.a1, torch.float64, device),
+                      c1=_dev(prof.c1, torch.float64, device), a2=_dev(prof.a2, torch.float64, device),
+                      b2=_dev(prof.b2, torch.float64, device), c2=_dev(prof.c2, torch.float64, device),
+                      dyn=_dev(prof.dyn, torch.float64, device))
+        self.struct = _lib.Profile(self.k, self.n_tiles, self.tile_w, 0,
+                                   *[_p(self.t[n]) for n in ("mhz", "a1", "c1", "a2", "b2", "c2", "dyn")],
+                                   float(prof.p_idle), float(prof.tdp), float(prof.u_half_prefill),
+                                   float(prof.u_half_decode))
+
+
+def _ladder(ladder):
+    lad = np.ascontiguousarray(ladder, np.uint16)
+    return lad, len(lad)
+
+
+# ---------------------------------------------------------------------------- K2
+def control_step(prof: DeviceProfile, phase: int, ladder, load, n_kv, queue_len, wait_ms, target_ms,
+                 stream=None):
+    """EcoFreq per snapshot (voltana_control_step). Returns (level uint16, status uint8) tensors."""
+    lad, k = _ladder(ladder)
+    n = int(load.numel())
+    dev = load.device
+    lvl = torch.empty(n, dtype=torch.uint16, device=dev)
+    st = torch.empty(n, dtype=torch.uint8, device=dev)
+    check(lib().voltana_control_step(C.byref(prof.struct), int(phase), lad.ctypes.data, k, _p(load), _p(n_kv),
+                                     _p(queue_len), _p(wait_ms), _p(target_ms), n, _p(lvl), _p(st),
+                                     _stream(stream)))
+    return lvl, st
+
+
+# ---------------------------------------------------------------------------- K3
+def route_batch(prof: DeviceProfile, ladder, n_d: int, n_req, n_kv, req_in, itl_target_ms, delta_mhz: int,
+                policy: int, cursor, stream=None):
+    """EcoRoute per item (voltana_route_batch). cursor is updated in place.
+    Returns (instance uint16, case uint8, status uint8) tensors."""
+    lad, k = _ladder(ladder)
+    n = int(req_in.numel())
+    dev = req_in.device
+    inst = torch.empty(n, dtype=torch.uint16, device=dev)
+    case = torch.empty(n, dtype=torch.uint8, device=dev)
+    st = torch.empty(n, dtype=torch.uint8, device=dev)
+    check(lib().voltana_route_batch(C.byref(prof.struct), lad.ctypes.data, k, int(n_d), _p(n_req), _p(n_kv),
+                                    _p(req_in), _p(itl_target_ms), int(delta_mhz), int(policy), _p(cursor), n,
+                                    _p(inst), _p(case), _p(st), _stream(stream)))
+    return inst, case, st
+
+
+# ---------------------------------------------------------------------------- K1
+class FitOutput(dict):
+    pass
+
+
+def fit_workspace_bytes(n_samples: int, k: int, n_tiles: int) -> int:
+    return int(lib().voltana_fit_workspace_bytes(int(n_samples), int(k), int(n_tiles)))
+
+
+def fit_profile(phase, level, n_bt, n_req, n_kv, lat_ms, k: int, n_tiles: int, tile_w: int = 128,
+                tile_step: float = 0.0, workspace=None, out: FitOutput | None = None, stream=None) -> FitOutput:
+    """EcoPred least-squares calibration (voltana_fit_profile) on device sample SoA."""
+    n = int(lat_ms.numel())
+    dev = lat_ms.device
+    cells = k + n_tiles * k
+    if out is None:
+        out = FitOutput(a1=torch.empty(k, dtype=torch.float64, device=dev),
+                        c1=torch.empty(k, dtype=torch.float64, device=dev),
+                        a2=torch.empty(n_tiles * k, dtype=torch.float64, device=dev),
+                        b2=torch.empty(n_tiles * k, dtype=torch.float64, device=dev),
+                        c2=torch.empty(n_tiles * k, dtype=torch.float64, device=dev),
+                        mae=torch.empty(cells, dtype=torch.float64, device=dev),
+                        cell_status=torch.empty(cells, dtype=torch.uint8, device=dev),
+                        invalid=torch.zeros(1, dtype=torch.uint64, device=dev))
+    need = fit_workspace_bytes(n, k, n_tiles)
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(need, dtype=torch.uint8, device=dev)
+    out["workspace"] = workspace
+    check(lib().voltana_fit_profile(_p(phase), _p(level), _p(n_bt), _p(n_req), _p(n_kv), _p(lat_ms), n, int(k),
+                                    int(n_tiles), int(tile_w), float(tile_step), _p(out["a1"]), _p(out["c1"]),
+                                    _p(out["a2"]), _p(out["b2"]), _p(out["c2"]), _p(out["mae"]),
+                                    _p(out["cell_status"]), _p(out["invalid"]), _p(workspace),
+                                    workspace.numel(), _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------------------- K4
+def lpt_order(n_requests_per_scenario, n_d_per_scenario=None) -> np.ndarray:
+    """Longest-processing-time-first order of scenarios (persistent warps claim in this order).
+    Cost estimate: requests (each is one route and part of a prefill batch) — stable sort."""
+    c = np.asarray(n_requests_per_scenario, np.float64)
+    if n_d_per_scenario is not None:
+        c = c * (1.0 + 0.05 * np.asarray(n_d_per_scenario, np.float64))
+    return np.argsort(-c, kind="stable")
+
+
+class DeviceWorkload:
+    """Scenario sweep resident in device memory, ready for voltana_simulate.
+
+    traces: object with arrival, in_len, out_len (concatenated), offset [n_traces+1], duration.
+    scen: dict of arrays trace_id, slo_id, layout_id, grid_id, profile_id, hash_seed.
+    slos / layouts / grids / profiles: small host tables (objects with the documented fields).
+    order: "lpt" (default) claims expensive scenarios first; records are returned in the
+    caller's scenario order either way.
+    """
+
+    def __init__(self, traces, slos, layouts, grids, profiles, scen, device="cuda", order="lpt"):
+        self.device = torch.device(device)
+        offset = np.asarray(traces.offset, np.uint64)
+        lens = np.diff(offset.astype(np.int64))
+        self.n_traces = len(offset) - 1
+        self.max_requests = int(lens.max()) if len(lens) else 0
+        self.h2d_bytes = 0
+        self.tr = dict(arrival=self._up(traces.arrival, torch.float64), in_len=self._up(traces.in_len, torch.uint32),
+                       out_len=self._up(traces.out_len, torch.uint32), offset=self._up(offset, torch.uint64),
+                       duration=self._up(traces.duration, torch.float64))
+        n = len(scen["trace_id"])
+        self.n = n
+        if order == "lpt":
+            nd = np.array([layouts[i].n_d for i in np.asarray(scen["layout_id"], np.int64)]) if n else None
+            self.perm = lpt_order(lens[np.asarray(scen["trace_id"], np.int64)], nd) if n else np.zeros(0, np.int64)
+        else:
+            self.perm = np.arange(n)
+        self.inv = np.empty_like(self.perm)
+        self.inv[self.perm] = np.arange(n)
+        sc = {k: np.asarray(v)[self.perm] for k, v in scen.items()}
+        self.sc = {k: self._up(sc[k], torch.uint32) for k in ("trace_id", "slo_id", "layout_id", "grid_id",
+                                                             "profile_id")}
+        self.sc["hash_seed"] = self._up(np.asarray(sc["hash_seed"], np.uint64), torch.uint64)
+        self.profiles = [p if isinstance(p, DeviceProfile) else DeviceProfile(p, self.device) for p in profiles]
+        self.slos = (_lib.Slo * len(slos))(*[_lib.Slo(float(s.ttft), float(s.itl), float(s.scale)) for s in slos])
+        self.layouts = (_lib.Layout * len(layouts))(*[
+            _lib.Layout(int(x.n_p), int(x.n_d), int(x.policy), int(x.delta_mhz), int(x.max_batch_tokens),
+                        int(x.kv_capacity), float(x.kv_transfer_ms)) for x in layouts])
+        gs = []
+        for g in grids:
+            g = np.asarray(g, np.uint16)
+            arr = (C.c_uint16 * _lib.MAX_LEVELS)(*([int(v) for v in g] + [0] * (_lib.MAX_LEVELS - len(g))))
+            gs.append(_lib.Grid(len(g), arr))
+        self.grids = (_lib.Grid * len(gs))(*gs)
+        self.profs = (_lib.Profile * len(self.profiles))(*[p.struct for p in self.profiles])
+        self.traces_struct = _lib.Traces(_p(self.tr["arrival"]), _p(self.tr["in_len"]), _p(self.tr["out_len"]),
+                                         _p(self.tr["offset"]), _p(self.tr["duration"]), self.n_traces,
+                                         self.max_requests)
+        self.scen_struct = _lib.Scenarios(*[_p(self.sc[k]) for k in ("trace_id", "slo_id", "layout_id", "grid_id",
+                                                                     "profile_id", "hash_seed")])
+        self.out = torch.empty((n, 128), dtype=torch.uint8, device=self.device)
+        need = int(lib().voltana_simulate_workspace_bytes(C.byref(self.traces_struct), self.layouts,
+                                                          len(layouts), n))
+        self.workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
+        self.n_layouts, self.n_slos, self.n_grids = len(layouts), len(slos), len(gs)
+
+    def _up(self, a, dtype):
+        t = _dev(a, dtype, self.device)
+        self.h2d_bytes += t.numel() * t.element_size()
+        return t
+
+    def launch(self, stream=None):
+        """Enqueue voltana_simulate; records land in self.out (LPT order)."""
+        check(lib().voltana_simulate(C.byref(self.traces_struct), self.slos, self.n_slos, self.layouts,
+                                     self.n_layouts, self.grids, self.n_grids, self.profs, len(self.profiles),
+                                     C.byref(self.scen_struct), self.n, _p(self.out), _p(self.workspace),
+                                     self.workspace.numel(), _stream(stream)))
+
+    # ---- end-to-end path from host memory (pinned staging buffers) ----------------
+    def pin_host(self):
+        """Allocate pinned host mirrors of every device input and of the output records."""
+        self.host = {("tr", k): torch.empty_like(v, device="cpu").pin_memory() for k, v in self.tr.items()}
+        self.host.update({("sc", k): torch.empty_like(v, device="cpu").pin_memory() for k, v in self.sc.items()})
+        for (grp, k), h in self.host.items():
+            h.copy_(getattr(self, grp)[k])
+        self.host_out = torch.empty_like(self.out, device="cpu").pin_memory()
+        return self
+
+    def stage_inputs(self, stream=None) -> int:
+        """Async H2D copy of all inputs from the pinned mirrors; returns bytes copied."""
+        s = torch.cuda.current_stream() if stream is None else stream
+        nbytes = 0
+        with torch.cuda.stream(s):
+            for (grp, k), h in self.host.items():
+                d = getattr(self, grp)[k]
+                d.copy_(h, non_blocking=True)
+                nbytes += h.numel() * h.element_size()
+        return nbytes
+
+    def fetch_records(self, stream=None) -> int:
+        """Async D2H copy of the records into the pinned mirror; returns bytes copied."""
+        s = torch.cuda.current_stream() if stream is None else stream
+        with torch.cuda.stream(s):
+            self.host_out.copy_(self.out, non_blocking=True)
+        return self.host_out.numel()
+
+    def records(self) -> np.ndarray:
+        """Records in the caller's scenario order (synchronises)."""
+        host = self.out.cpu().numpy().view(RESULT_DTYPE).reshape(-1)
+        return host[self.inv]
+
+
+def simulate(traces, slos, layouts, grids, profiles, scen, device="cuda", stream=None) -> np.ndarray:
+    """One-shot voltana_simulate from host arrays: upload, run, read back records."""
+    w = DeviceWorkload(traces, slos, layouts, grids, profiles, scen, device=device)
+    w.launch(stream)
+    return w.records()
+
+
+def last_launch_count() -> int:
+    return int(lib().voltana_last_launch_count())

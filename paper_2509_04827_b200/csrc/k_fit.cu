@@ -1,0 +1,265 @@
+// k_fit.cu — K1 (voltana_fit_profile): EcoPred least squares per cell.
+//
+// Three streaming passes over the sample SoA (HBM-bound, 23 B/sample/pass):
+//   pass 1: per-cell count and sums of x1, x2 (exact u64) and y       -> means
+//   pass 2: per-cell centred S11, S12, S22, S1y, S2y                  -> OLS solve
+//   pass 3: per-cell sum |y - y_hat|                                   -> MAE
+// Determinism without fp64 atomics: every warp owns a contiguous sample range and a
+// private shared-memory accumulator row per cell. Within a 32-sample chunk, lanes of
+// equal cell are ranked with __match_any_sync and add in ascending lane order (one
+// round per rank; lanes of one round touch distinct cells), so each warp's partial is
+// the sequential sum over its range. Warp partials are combined in warp order per
+// CTA, CTA partials in CTA order per cell: a fixed tree, independent of timing.
+#include <cstdint>
+
+#include "vt_device.cuh"
+#include "vt_fit.h"
+
+namespace vt {
+
+struct Sample {
+  int cell;          // -1 = invalid / out of range
+  uint32_t x1, x2;
+  double y;
+};
+
+__device__ __forceinline__ Sample load_sample(const FitParams &P, size_t i, bool in_range) {
+  Sample s;
+  s.cell = -1; s.x1 = 0; s.x2 = 0; s.y = 0.0;
+  if (!in_range) return s;
+  const uint32_t ph = P.phase[i], lv = P.level[i];
+  const uint32_t nr = P.n_req[i];
+  if (ph > 1u || lv >= (uint32_t)P.k || (ph == 1u && nr == 0u)) { s.cell = -2; return s; }
+  s.y = P.lat[i];
+  if (ph == 0u) {
+    s.cell = (int)lv;
+    s.x1 = P.n_bt[i];
+  } else {
+    uint32_t j = tile_of(nr, (uint32_t)P.tile_w, (uint32_t)P.n_tiles);
+    s.cell = P.k + (int)j * P.k + (int)lv;
+    s.x1 = nr;
+    s.x2 = P.n_kv[i];
+  }
+  return s;
+}
+
+// Ordered per-warp accumulation of NS doubles (pass 2/3) or the pass-1 record.
+template <int PASS>
+__global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __grid_constant__ FitParams P) {
+  extern __shared__ double sm[];
+  constexpr int NS = PASS == 1 ? 4 : (PASS == 2 ? 5 : 1);
+  const int C = P.cells;
+  const int lane = lane_id(), wib = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  double *acc = sm + (size_t)wib * C * NS;   // pass 1 stores u64 bit patterns in slots 0..2
+  for (int x = lane; x < C * NS; x += 32) acc[x] = 0.0;
+  __syncwarp();
+
+  const size_t gw = (size_t)blockIdx.x * wpb + wib;
+  const size_t lo = gw * P.chunk, hi = lo + P.chunk < P.n ? lo + P.chunk : P.n;
+  uint64_t invalid = 0;
+  for (size_t base = lo; base < hi; base += 32) {
+    const size_t i = base + lane;
+    Sample s = load_sample(P, i, i < hi);
+    if (s.cell == -2) invalid++;
+    double v[NS];
+    if (PASS == 1) {
+      v[0] = 0; v[1] = 0; v[2] = 0; v[3] = s.y;
+    } else if (PASS == 2) {
+      if (s.cell >= 0) {
+        const double *m = P.means + 3 * (size_t)s.cell;
+        double dx1 = sub((double)s.x1, m[0]);
+        double dy = sub(s.y, m[2]);
+        v[0] = mul(dx1, dx1);
+        v[4] = mul(dx1, dy);   // S1y
+        if (s.cell >= P.k) {
+          double dx2 = sub((double)s.x2, m[1]);
+          v[1] = mul(dx1, dx2);
+          v[2] = mul(dx2, dx2);
+          v[3] = mul(dx2, dy);
+        } else {
+          v[1] = v[2] = v[3] = 0.0;
+        }
+      }
+    } else {
+      if (s.cell >= 0 && P.status[s.cell] == 0) {
+        double yh;
+        if (s.cell < P.k) {
+          yh = ttft_pred(P.a1[s.cell], P.c1[s.cell], s.x1);
+        } else {
+          int o = s.cell - P.k;
+          yh = itl_pred(P.a2[o], P.b2[o], P.c2[o], s.x1, s.x2);
+        }
+        v[0] = fabs(sub(s.y, yh));
+      } else {
+        v[0] = 0.0;
+      }
+    }
+    const bool act = s.cell >= 0 && (PASS != 3 || P.status[s.cell] == 0);
+    const int key = act ? s.cell : -1 - lane;
+    const unsigned peers = __match_any_sync(FULL, key);
+    const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+    const unsigned maxr = __reduce_max_sync(FULL, act ? rank : 0u);
+    for (unsigned r = 0; r <= maxr; ++r) {
+      if (act && rank == r) {
+        double *a = acc + (size_t)s.cell * NS;
+        if (PASS == 1) {
+          uint64_t *u = (uint64_t *)a;
+          u[0] += 1u;
+          u[1] += s.x1;
+          u[2] += s.x2;
+          a[3] = add(a[3], v[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NS; ++q) a[q] = add(a[q], v[q]);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (PASS == 1) {
+    for (int o = 16; o > 0; o >>= 1) invalid += __shfl_xor_sync(FULL, invalid, o);
+    if (lane == 0 && invalid && P.invalid_count) atomicAdd((unsigned long long *)P.invalid_count, invalid);
+  }
+  __syncthreads();
+  // CTA partial: warps combined in warp order, one thread per (cell, stat)
+  double *out = P.part + (size_t)blockIdx.x * C * NS;
+  for (int x = threadIdx.x; x < C * NS; x += blockDim.x) {
+    const int stat = x % NS;
+    if (PASS == 1 && stat < 3) {
+      uint64_t s = 0;
+      for (int w = 0; w < wpb; ++w) s += ((const uint64_t *)(sm + (size_t)w * C * NS))[x];
+      ((uint64_t *)out)[x] = s;
+    } else {
+      double s = 0.0;
+      for (int w = 0; w < wpb; ++w) s = add(s, sm[(size_t)w * C * NS + x]);
+      out[x] = s;
+    }
+  }
+}
+
+// grid reduction of CTA partials in CTA order, one thread per (cell, stat): red[c][q]
+template <int NS>
+__global__ void fit_reduce_kernel(const __grid_constant__ FitParams P, int nblocks) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= P.cells * NS) return;
+  const size_t stride = (size_t)P.cells * NS;
+  if (NS == 4 && (x % NS) < 3) {
+    uint64_t s = 0;
+    for (int b = 0; b < nblocks; ++b) s += ((const uint64_t *)P.part)[(size_t)b * stride + x];
+    ((uint64_t *)P.red)[x] = s;
+  } else {
+    double s = 0.0;
+    for (int b = 0; b < nblocks; ++b) s = add(s, P.part[(size_t)b * stride + x]);
+    P.red[x] = s;
+  }
+}
+
+__global__ void fit_means_kernel(const __grid_constant__ FitParams P) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P.cells) return;
+  const uint64_t *u = (const uint64_t *)(P.red + 4 * (size_t)c);
+  const uint64_t cnt = u[0];
+  P.cnt[c] = cnt;
+  double *m = P.means + 3 * (size_t)c;
+  if (cnt > 0) {
+    const double dc = (double)cnt;
+    m[0] = div((double)u[1], dc);
+    m[1] = div((double)u[2], dc);
+    m[2] = div(P.red[4 * (size_t)c + 3], dc);
+  } else {
+    m[0] = m[1] = m[2] = 0.0;
+  }
+}
+
+__global__ void fit_solve_kernel(const __grid_constant__ FitParams P) {
+  // thread k < K: TTFT level k; thread K + k: ITL level k over tiles j = 0..T-1 (F4 chains)
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = P.k, T = P.n_tiles;
+  if (t >= 2 * K) return;
+  if (t < K) {
+    const int c = t;
+    const double *m = P.means + 3 * (size_t)c;
+    const double *r = P.red + 5 * (size_t)c;
+    double a = 0.0, cc = 0.0;
+    uint8_t st;
+    const double s11 = r[0], s1y = r[4];
+    if (P.cnt[c] == 0) st = 2;
+    else if (P.cnt[c] < 2 || !(s11 > 0.0)) st = 3;   // A31
+    else {
+      a = div(s1y, s11);
+      cc = sub(m[2], mul(a, m[0]));
+      st = 0;
+    }
+    P.a1[c] = a; P.c1[c] = cc; P.status[c] = st;
+    return;
+  }
+  const int k = t - K;
+  for (int j = 0; j < T; ++j) {
+    const int c = K + j * K + k, o = j * K + k;
+    const double *m = P.means + 3 * (size_t)c;
+    const double *r = P.red + 5 * (size_t)c;
+    double a = 0.0, b = 0.0, cc = 0.0;
+    uint8_t st;
+    if (P.cnt[c] == 0) {
+      if (j == 0) st = 2;
+      else {                                 // inherit tile j-1 plus the step (F4)
+        a = P.a2[o - K]; b = P.b2[o - K]; cc = add(P.c2[o - K], P.tile_step);
+        st = 1;
+      }
+    } else {
+      const double s11 = r[0], s12 = r[1], s22 = r[2], s2y = r[3], s1y = r[4];
+      const double pr = mul(s11, s22);
+      const double det = sub(mul(s11, s22), mul(s12, s12));
+      if (P.cnt[c] < 3 || !(pr > 0.0) || !(det > mul(1e-10, pr))) {
+        st = 3;
+      } else {
+        a = div(sub(mul(s22, s1y), mul(s12, s2y)), det);
+        b = div(sub(mul(s11, s2y), mul(s12, s1y)), det);
+        cc = sub(sub(m[2], mul(a, m[0])), mul(b, m[1]));
+        st = 0;
+      }
+    }
+    P.a2[o] = a; P.b2[o] = b; P.c2[o] = cc; P.status[c] = st;
+  }
+}
+
+__global__ void fit_mae_kernel(const __grid_constant__ FitParams P) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P.cells) return;
+  P.mae[c] = P.status[c] == 0 ? div(P.red[c], (double)P.cnt[c]) : 0.0;
+}
+
+int fit_warps_per_block(int cells) {
+  // pass 2 needs 40 B per cell per warp; keep <= 200 KB of shared memory per CTA
+  int w = (int)(200 * 1024 / ((size_t)cells * 40));
+  if (w > FIT_MAX_WARPS) w = FIT_MAX_WARPS;
+  return w < 1 ? 1 : w;
+}
+
+template <int PASS>
+static cudaError_t launch_pass(const FitParams &P, int blocks, int wpb, cudaStream_t st) {
+  constexpr int NS = PASS == 1 ? 4 : (PASS == 2 ? 5 : 1);
+  size_t smem = (size_t)wpb * P.cells * NS * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(fit_pass_kernel<PASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  fit_pass_kernel<PASS><<<blocks, wpb * 32, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fit(const FitParams &P, int blocks, int wpb, cudaStream_t st, int *launches) {
+  cudaError_t e;
+  const int cb = (P.cells + 127) / 128;
+  if ((e = launch_pass<1>(P, blocks, wpb, st)) != cudaSuccess) return e;
+  fit_reduce_kernel<4><<<(4 * P.cells + 127) / 128, 128, 0, st>>>(P, blocks);
+  fit_means_kernel<<<cb, 128, 0, st>>>(P);
+  if ((e = launch_pass<2>(P, blocks, wpb, st)) != cudaSuccess) return e;
+  fit_reduce_kernel<5><<<(5 * P.cells + 127) / 128, 128, 0, st>>>(P, blocks);
+  fit_solve_kernel<<<(2 * P.k + 127) / 128, 128, 0, st>>>(P);
+  if ((e = launch_pass<3>(P, blocks, wpb, st)) != cudaSuccess) return e;
+  fit_reduce_kernel<1><<<(P.cells + 127) / 128, 128, 0, st>>>(P, blocks);
+  fit_mae_kernel<<<cb, 128, 0, st>>>(P);
+  *launches = 9;
+  return cudaGetLastError();
+}
+
+}  // namespace vt

@@ -1,0 +1,385 @@
+// voltana_api.cu — host side of the C ABI declared in include/voltana.h:
+// synchronous argument validation, workspace sizing, launch configuration.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/voltana.h"
+#include "vt_decide.h"
+#include "vt_device.cuh"
+#include "vt_fit.h"
+#include "vt_sim.h"
+
+using namespace vt;
+
+namespace {
+
+thread_local char g_detail[512] = "";
+thread_local int g_launches = 0;
+
+voltana_status fail(voltana_status s, const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_detail, sizeof(g_detail), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+voltana_status ok() {
+  g_detail[0] = 0;
+  return VOLTANA_OK;
+}
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int sm_count() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+voltana_status check_profile(const voltana_profile *p, const char *what) {
+  if (!p) return fail(VOLTANA_E_INVALID_ARG, "%s: null profile", what);
+  if (p->k < 1 || p->k > 1024) return fail(VOLTANA_E_INVALID_ARG, "%s: profile.k=%d outside 1..1024", what, p->k);
+  if (p->n_tiles < 1 || p->n_tiles > 64)
+    return fail(VOLTANA_E_INVALID_ARG, "%s: profile.n_tiles=%d outside 1..64", what, p->n_tiles);
+  if (p->tile_w < 1) return fail(VOLTANA_E_INVALID_ARG, "%s: profile.tile_w=%d < 1", what, p->tile_w);
+  if (!p->mhz || !p->a1 || !p->c1 || !p->a2 || !p->b2 || !p->c2 || !p->dyn)
+    return fail(VOLTANA_E_INVALID_ARG, "%s: profile table pointer is null", what);
+  if (!std::isfinite(p->p_idle) || !std::isfinite(p->tdp) || !(p->u_half_prefill > 0) || !(p->u_half_decode > 0))
+    return fail(VOLTANA_E_INVALID_ARG, "%s: profile power scalars invalid", what);
+  return VOLTANA_OK;
+}
+
+voltana_status check_ladder(const uint16_t *lad, int k, int prof_k, const char *what) {
+  if (!lad) return fail(VOLTANA_E_INVALID_ARG, "%s: null ladder", what);
+  if (k < 1 || k > VOLTANA_MAX_LEVELS) return fail(VOLTANA_E_LADDER, "%s: ladder has %d levels (1..64)", what, k);
+  for (int i = 0; i < k; ++i) {
+    if (lad[i] >= prof_k)
+      return fail(VOLTANA_E_COVERAGE, "%s: ladder[%d]=%u not on the profile grid (k=%d)", what, i, lad[i], prof_k);
+    if (i > 0 && lad[i] <= lad[i - 1])
+      return fail(VOLTANA_E_LADDER, "%s: ladder not strictly increasing at index %d", what, i);
+  }
+  return VOLTANA_OK;
+}
+
+voltana_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(VOLTANA_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+int decide_grid(size_t n) {
+  size_t want = (n + DECIDE_THREADS - 1) / DECIDE_THREADS;
+  size_t cap = (size_t)sm_count() * 8;
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *voltana_status_string(voltana_status s) {
+  switch (s) {
+    case VOLTANA_OK: return "ok";
+    case VOLTANA_E_INVALID_ARG: return "invalid argument";
+    case VOLTANA_E_LADDER: return "invalid frequency ladder";
+    case VOLTANA_E_COVERAGE: return "ladder level not on the profile grid";
+    case VOLTANA_E_CALIBRATION: return "calibration error";
+    case VOLTANA_E_CONFIG: return "invalid layout configuration";
+    case VOLTANA_E_WORKSPACE: return "workspace too small";
+    case VOLTANA_E_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char *voltana_last_error_detail(void) { return g_detail; }
+int voltana_last_launch_count(void) { return g_launches; }
+
+// ------------------------------------------------------------------ K2
+voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, const uint16_t *ladder_h, int k,
+                                    const uint32_t *load, const uint32_t *n_kv, const uint32_t *queue_len,
+                                    const double *wait_ms, const double *target_ms, size_t n,
+                                    uint16_t *out_level, uint8_t *out_status, void *stream) {
+  g_launches = 0;
+  voltana_status s;
+  if ((s = check_profile(prof_h, "control_step")) != VOLTANA_OK) return s;
+  if (phase != 0 && phase != 1) return fail(VOLTANA_E_INVALID_ARG, "control_step: phase=%d", phase);
+  if ((s = check_ladder(ladder_h, k, prof_h->k, "control_step")) != VOLTANA_OK) return s;
+  if (n == 0) return ok();
+  if (!load || !queue_len || !target_ms || !out_level || !out_status || (phase == 0 && !wait_ms) ||
+      (phase == 1 && !n_kv))
+    return fail(VOLTANA_E_INVALID_ARG, "control_step: null array pointer");
+  ControlParams P;
+  memset(&P, 0, sizeof(P));
+  P.prof = to_dev(*prof_h);
+  P.lad.k = k;
+  for (int i = 0; i < k; ++i) P.lad.level[i] = ladder_h[i];
+  P.load = load; P.n_kv = n_kv; P.queue_len = queue_len; P.wait = wait_ms; P.target = target_ms;
+  P.n = n; P.out_level = out_level; P.out_status = out_status;
+  cudaError_t e = launch_control(P, phase, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles),
+                                 (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "control_step launch");
+  g_launches = 1;
+  return ok();
+}
+
+// ------------------------------------------------------------------ K3
+voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t *ladder_h, int k, int n_d,
+                                   const uint32_t *n_req, const uint32_t *n_kv, const uint32_t *req_in,
+                                   const double *itl_target_ms, int32_t delta_mhz, int policy,
+                                   uint32_t *cursor, size_t n, uint16_t *out_instance, uint8_t *out_case,
+                                   uint8_t *out_status, void *stream) {
+  g_launches = 0;
+  voltana_status s;
+  if ((s = check_profile(prof_h, "route_batch")) != VOLTANA_OK) return s;
+  if ((s = check_ladder(ladder_h, k, prof_h->k, "route_batch")) != VOLTANA_OK) return s;
+  if (n_d < 1 || n_d > VOLTANA_MAX_INSTANCES) return fail(VOLTANA_E_CONFIG, "route_batch: n_d=%d outside 1..8", n_d);
+  if (policy != 0 && policy != 1) return fail(VOLTANA_E_INVALID_ARG, "route_batch: policy=%d", policy);
+  if (n == 0) return ok();
+  if (!n_req || !n_kv || !req_in || !itl_target_ms || !cursor || !out_instance || !out_case || !out_status)
+    return fail(VOLTANA_E_INVALID_ARG, "route_batch: null array pointer");
+  RouteParams P;
+  memset(&P, 0, sizeof(P));
+  P.prof = to_dev(*prof_h);
+  P.lad.k = k;
+  for (int i = 0; i < k; ++i) P.lad.level[i] = ladder_h[i];
+  P.n_d = n_d; P.policy = policy; P.delta = delta_mhz;
+  P.n_req = n_req; P.n_kv = n_kv; P.req_in = req_in; P.target = itl_target_ms; P.cursor = cursor;
+  P.n = n; P.out_instance = out_instance; P.out_case = out_case; P.out_status = out_status;
+  cudaError_t e = launch_route(P, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "route_batch launch");
+  g_launches = 1;
+  return ok();
+}
+
+// ------------------------------------------------------------------ K1
+namespace {
+struct FitLayout { int cells, wpb, blocks; size_t chunk, part, red, means, cnt, total; };
+
+FitLayout fit_layout(size_t n, int k, int n_tiles) {
+  FitLayout L;
+  L.cells = k + n_tiles * k;
+  L.wpb = fit_warps_per_block(L.cells);
+  size_t warps_want = (n + 2047) / 2048;               // >= 2048 samples per warp
+  size_t cap = (size_t)sm_count() * 2 * L.wpb;         // two CTAs per SM at most
+  size_t warps = warps_want < 1 ? 1 : (warps_want < cap ? warps_want : cap);
+  L.blocks = (int)((warps + L.wpb - 1) / L.wpb);
+  size_t tw = (size_t)L.blocks * L.wpb;
+  L.chunk = (n + tw - 1) / tw;
+  L.chunk = (L.chunk + 31) & ~(size_t)31;
+  if (L.chunk == 0) L.chunk = 32;
+  L.part = 0;
+  L.red = align256(L.part + (size_t)L.blocks * L.cells * 5 * sizeof(double));
+  L.means = align256(L.red + (size_t)L.cells * 5 * sizeof(double));
+  L.cnt = align256(L.means + (size_t)L.cells * 3 * sizeof(double));
+  L.total = align256(L.cnt + (size_t)L.cells * sizeof(uint64_t));
+  return L;
+}
+}  // namespace
+
+size_t voltana_fit_workspace_bytes(size_t n_samples, int k, int n_tiles) {
+  if (k < 1 || n_tiles < 1) return 0;
+  return fit_layout(n_samples, k, n_tiles).total;
+}
+
+voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32_t *n_bt,
+                                   const uint32_t *n_req, const uint32_t *n_kv, const double *lat_ms, size_t n,
+                                   int k, int n_tiles, int tile_w, double tile_step, double *a1, double *c1,
+                                   double *a2, double *b2, double *c2, double *mae, uint8_t *cell_status,
+                                   uint64_t *invalid_count, void *workspace, size_t ws_bytes, void *stream) {
+  g_launches = 0;
+  if (k < 1 || k > 1024 || n_tiles < 1 || n_tiles > 64 || tile_w < 1)
+    return fail(VOLTANA_E_INVALID_ARG, "fit_profile: k=%d n_tiles=%d tile_w=%d", k, n_tiles, tile_w);
+  if (!a1 || !c1 || !a2 || !b2 || !c2 || !mae || !cell_status)
+    return fail(VOLTANA_E_INVALID_ARG, "fit_profile: null output pointer");
+  if (n > 0 && (!phase || !level || !n_bt || !n_req || !n_kv || !lat_ms))
+    return fail(VOLTANA_E_INVALID_ARG, "fit_profile: null sample pointer");
+  if (!std::isfinite(tile_step)) return fail(VOLTANA_E_INVALID_ARG, "fit_profile: tile_step not finite");
+  FitLayout L = fit_layout(n, k, n_tiles);
+  if (L.cells * 5 * sizeof(double) * (size_t)L.wpb > 227 * 1024)
+    return fail(VOLTANA_E_INVALID_ARG, "fit_profile: %d cells exceed shared memory", L.cells);
+  if (!workspace || ws_bytes < L.total)
+    return fail(VOLTANA_E_WORKSPACE, "fit_profile: workspace %zu < %zu bytes", ws_bytes, L.total);
+  FitParams P;
+  memset(&P, 0, sizeof(P));
+  P.phase = phase; P.level = level; P.n_bt = n_bt; P.n_req = n_req; P.n_kv = n_kv; P.lat = lat_ms;
+  P.n = n; P.chunk = L.chunk; P.k = k; P.n_tiles = n_tiles; P.tile_w = tile_w; P.cells = L.cells;
+  P.tile_step = tile_step;
+  P.a1 = a1; P.c1 = c1; P.a2 = a2; P.b2 = b2; P.c2 = c2; P.mae = mae; P.status = cell_status;
+  P.invalid_count = invalid_count;
+  char *ws = (char *)workspace;
+  P.part = (double *)(ws + L.part);
+  P.red = (double *)(ws + L.red);
+  P.means = (double *)(ws + L.means);
+  P.cnt = (uint64_t *)(ws + L.cnt);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (invalid_count) {
+    cudaError_t e = cudaMemsetAsync(invalid_count, 0, sizeof(uint64_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "fit_profile memset");
+  }
+  int launches = 0;
+  cudaError_t e = launch_fit(P, L.blocks, L.wpb, st, &launches);
+  if (e != cudaSuccess) return cuda_fail(e, "fit_profile launch");
+  g_launches = launches;
+  return ok();
+}
+
+// ------------------------------------------------------------------ K4
+namespace {
+
+struct SimShape { int maxp, maxd; };
+
+SimShape sim_shape(const voltana_layout *lays, int n_layouts) {
+  int mp = 1, md = 1;
+  for (int i = 0; i < n_layouts; ++i) {
+    if (lays[i].n_p > mp) mp = lays[i].n_p;
+    if (lays[i].n_d > md) md = lays[i].n_d;
+  }
+  int m = mp > md ? mp : md;
+  int t = m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : 8;
+  return {t, t};
+}
+
+const void *sim_ptr(int t) {
+  switch (t) {
+    case 1: return sim_kernel_ptr<1, 1>();
+    case 2: return sim_kernel_ptr<2, 2>();
+    case 4: return sim_kernel_ptr<4, 4>();
+    default: return sim_kernel_ptr<8, 8>();
+  }
+}
+
+int resident_warps(int t) {
+  static std::mutex mu;
+  static int cache[9] = {0};
+  std::lock_guard<std::mutex> g(mu);
+  if (!cache[t]) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_ptr(t), SIM_THREADS, 0) != cudaSuccess || nb < 1)
+      nb = 1;
+    cache[t] = nb * sm_count() * (SIM_THREADS / 32);
+  }
+  return cache[t];
+}
+
+struct SimLayout { size_t node, xd, wheel, slot, slots, total; uint32_t n_slots; };
+
+SimLayout sim_layout(uint64_t max_requests, int maxd, size_t n) {
+  SimLayout L;
+  L.node = align256((size_t)max_requests * 16);
+  L.xd = align256((size_t)max_requests);
+  L.wheel = (size_t)maxd * WHEEL_BUCKETS * 8;
+  L.slot = align256(L.node + L.xd + L.wheel);
+  size_t rw = (size_t)resident_warps(maxd);
+  L.n_slots = (uint32_t)(n < rw ? (n < 1 ? 1 : n) : rw);
+  L.slots = 256;
+  L.total = L.slots + (size_t)L.n_slots * L.slot;
+  return L;
+}
+
+}  // namespace
+
+size_t voltana_simulate_workspace_bytes(const voltana_traces *traces_h, const voltana_layout *layouts_h,
+                                        int n_layouts, size_t n_scenarios) {
+  if (!traces_h || !layouts_h || n_layouts < 1) return 0;
+  SimShape sh = sim_shape(layouts_h, n_layouts);
+  return sim_layout(traces_h->max_requests, sh.maxd, n_scenarios).total;
+}
+
+voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_slo *slos_h, int n_slos,
+                                const voltana_layout *layouts_h, int n_layouts, const voltana_grid *grids_h,
+                                int n_grids, const voltana_profile *profiles_h, int n_profiles,
+                                const voltana_scenarios *scen_h, size_t n, voltana_result *out, void *workspace,
+                                size_t ws_bytes, void *stream) {
+  g_launches = 0;
+  if (!traces_h || !slos_h || !layouts_h || !grids_h || !profiles_h || !scen_h)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: null table pointer");
+  if (n_slos < 1 || n_slos > MAX_SLOS) return fail(VOLTANA_E_INVALID_ARG, "simulate: n_slos=%d (1..64)", n_slos);
+  if (n_layouts < 1 || n_layouts > MAX_LAYOUTS)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: n_layouts=%d (1..16)", n_layouts);
+  if (n_grids < 1 || n_grids > MAX_GRIDS) return fail(VOLTANA_E_INVALID_ARG, "simulate: n_grids=%d (1..16)", n_grids);
+  if (n_profiles < 1 || n_profiles > MAX_PROFILES)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: n_profiles=%d (1..8)", n_profiles);
+  if (n > 0xffffffffull) return fail(VOLTANA_E_INVALID_ARG, "simulate: n=%zu too large", n);
+  if (traces_h->max_requests > 0x7fffffffull)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_requests too large");
+  voltana_status s;
+  for (int i = 0; i < n_slos; ++i) {
+    const voltana_slo &x = slos_h[i];
+    if (!(x.ttft_ms > 0) || !(x.itl_ms > 0) || !(x.scale > 0) || !std::isfinite(x.ttft_ms) ||
+        !std::isfinite(x.itl_ms) || !std::isfinite(x.scale))
+      return fail(VOLTANA_E_INVALID_ARG, "simulate: slos[%d] must be positive and finite", i);
+  }
+  for (int i = 0; i < n_layouts; ++i) {
+    const voltana_layout &x = layouts_h[i];
+    if (x.n_p < 1 || x.n_p > VOLTANA_MAX_INSTANCES || x.n_d < 1 || x.n_d > VOLTANA_MAX_INSTANCES)
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d] n_p=%d n_d=%d (1..8)", i, x.n_p, x.n_d);
+    if (x.policy != 0 && x.policy != 1) return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].policy=%d", i, x.policy);
+    if (x.max_batch_tokens == 0 || x.max_batch_tokens > 0x7fffffffu || x.kv_capacity == 0 ||
+        x.kv_capacity > 0x7fffffffu)
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d] B or C outside 1..2^31-1", i);
+    if (!(x.kv_transfer_ms == 0.0 || x.kv_transfer_ms >= 1e-3) || !std::isfinite(x.kv_transfer_ms))
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].kv_transfer_ms must be 0 or >= 1e-3", i);
+  }
+  for (int i = 0; i < n_profiles; ++i) {
+    char what[64];
+    snprintf(what, sizeof(what), "simulate: profiles[%d]", i);
+    if ((s = check_profile(&profiles_h[i], what)) != VOLTANA_OK) return s;
+  }
+  for (int i = 0; i < n_grids; ++i) {
+    char what[64];
+    snprintf(what, sizeof(what), "simulate: grids[%d]", i);
+    // each grid must be valid on every profile it may be paired with: check against the smallest
+    int kmin = profiles_h[0].k;
+    for (int j = 1; j < n_profiles; ++j) kmin = profiles_h[j].k < kmin ? profiles_h[j].k : kmin;
+    if ((s = check_ladder(grids_h[i].level, grids_h[i].k, kmin, what)) != VOLTANA_OK) return s;
+  }
+  if (n == 0) return ok();
+  if (!out || !traces_h->arrival || !traces_h->in_len || !traces_h->out_len || !traces_h->offset ||
+      !traces_h->duration_ms || !scen_h->trace_id || !scen_h->slo_id || !scen_h->layout_id || !scen_h->grid_id ||
+      !scen_h->profile_id || !scen_h->hash_seed)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: null device array");
+  SimShape sh = sim_shape(layouts_h, n_layouts);
+  SimLayout L = sim_layout(traces_h->max_requests, sh.maxd, n);
+  if (!workspace || ws_bytes < L.total)
+    return fail(VOLTANA_E_WORKSPACE, "simulate: workspace %zu < %zu bytes", ws_bytes, L.total);
+
+  static_assert(sizeof(SimParams) < 32000, "kernel parameter block too large");
+  SimParams *P = new SimParams;
+  memset(P, 0, sizeof(SimParams));
+  P->arrival = traces_h->arrival; P->in_len = traces_h->in_len; P->out_len = traces_h->out_len;
+  P->offset = traces_h->offset; P->duration = traces_h->duration_ms;
+  P->trace_id = scen_h->trace_id; P->slo_id = scen_h->slo_id; P->layout_id = scen_h->layout_id;
+  P->grid_id = scen_h->grid_id; P->profile_id = scen_h->profile_id; P->hash_seed = scen_h->hash_seed;
+  P->n = (uint32_t)n; P->nb = WHEEL_BUCKETS; P->out = out;
+  char *ws = (char *)workspace;
+  P->counter = (uint32_t *)ws;
+  P->slots = ws + L.slots;
+  P->slot_bytes = L.slot; P->node_bytes = L.node; P->xd_bytes = L.xd;
+  P->max_requests = traces_h->max_requests;
+  for (int i = 0; i < n_slos; ++i) P->slo[i] = slos_h[i];
+  for (int i = 0; i < n_layouts; ++i) P->lay[i] = layouts_h[i];
+  for (int i = 0; i < n_grids; ++i) P->grid[i] = grids_h[i];
+  for (int i = 0; i < n_profiles; ++i) P->prof[i] = to_dev(profiles_h[i]);
+  P->n_slots = L.n_slots;
+  P->n_slos = (uint32_t)n_slos; P->n_layouts = (uint32_t)n_layouts; P->n_grids = (uint32_t)n_grids;
+  P->n_profiles = (uint32_t)n_profiles; P->n_traces = traces_h->n_traces;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(P->counter, 0, sizeof(uint32_t), st);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
+  const int grid = (int)((L.n_slots + (SIM_THREADS / 32) - 1) / (SIM_THREADS / 32));
+  switch (sh.maxd) {
+    case 1: e = launch_sim<1, 1>(*P, grid, st); break;
+    case 2: e = launch_sim<2, 2>(*P, grid, st); break;
+    case 4: e = launch_sim<4, 4>(*P, grid, st); break;
+    default: e = launch_sim<8, 8>(*P, grid, st); break;
+  }
+  delete P;
+  if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
+  g_launches = 1;
+  return ok();
+}
+
+}  // extern "C"

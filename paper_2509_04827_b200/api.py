@@ -216,6 +216,8 @@ class DeviceWorkload:
         self.n_layouts, self.n_slos, self.n_grids = len(layouts), len(slos), len(gs)
 
     def _up(self, a, dtype):
+        if not isinstance(a, torch.Tensor) and np.size(a) == 0:
+            a = np.zeros(1, np.asarray(a).dtype)      # keep device pointers non-null for empty inputs
         t = _dev(a, dtype, self.device)
         self.h2d_bytes += t.numel() * t.element_size()
         return t

@@ -188,12 +188,18 @@ typedef struct {
   uint32_t *admq; uint64_t q_head, q_tail;   /* FIFO admission queue (capacity n) */
   uint64_t nreq, nkv, pend_n, pend_kv;
   int busy; double end, ebusy, bms; uint64_t iters;
+  uint64_t h;       /* decision-hash chain of this instance's controller decisions [A36] */
+  double sum_itl;   /* ITL-mean sum of this instance's completions, completion order [A37] */
+  double top;       /* ms at the top level [A37] */
 } dec_inst;
 
 typedef struct {
   uint64_t qhead;          /* first id (== p mod N_P) not yet batched [A7] */
   uint64_t bstart, bcnt;   /* ids of the batch in flight: bstart + j*N_P */
   int busy; double end, ebusy, bms; uint64_t iters;
+  uint64_t h;       /* decision-hash chain of this instance's controller decisions [A36] */
+  double sum_ttft;  /* TTFT sum of this instance's completions, completion order [A37] */
+  double top;       /* ms at the top level [A37] */
 } pre_inst;
 
 static int validate(const orc_scenario *s) {
@@ -248,8 +254,9 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
   uint64_t xq_head = 0, xq_tail = 0;
   uint64_t *eff_n = malloc((size_t)ND * sizeof(uint64_t));
   uint64_t *eff_kv = malloc((size_t)ND * sizeof(uint64_t));
-  for (int q = 0; q < NP; ++q) P[q].qhead = (uint64_t)q;
+  for (int q = 0; q < NP; ++q) { P[q].qhead = (uint64_t)q; P[q].h = s->hash_seed; }
   for (int d = 0; d < ND; ++d) {
+    D[d].h = s->hash_seed;
     D[d].cap_run = 16;
     D[d].run = malloc(D[d].cap_run * sizeof(run_entry));
     D[d].admq = malloc((N ? N : 1) * sizeof(uint32_t));
@@ -257,9 +264,9 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
 
   uint64_t a = 0;           /* next arrival */
   uint32_t cursor = 0;      /* EcoRoute / round-robin cursor [A17] */
-  uint64_t h = s->hash_seed;
+  uint64_t h = s->hash_seed; /* routing-decision chain [A36] */
   uint64_t steps_ctrl = 0, steps_route = 0, n_ttft_ok = 0, n_itl_ok = 0, n_both = 0;
-  double sum_ttft = 0.0, sum_itl = 0.0, top_ms = 0.0, t = 0.0, t_last = 0.0;
+  double t = 0.0, t_last = 0.0;
   uint64_t force_pos = 0;
   uint32_t status = ORC_OK;
 
@@ -295,7 +302,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       for (uint64_t j = 0; j < P[q].bcnt; ++j) {
         uint64_t i = P[q].bstart + j * (uint64_t)NP;
         double ttft = t - arr[i]; /* TTFT = waiting + execution [A26] */
-        sum_ttft += ttft;
+        P[q].sum_ttft += ttft;
         int ok = ttft <= s->slo_ttft;
         n_ttft_ok += (uint64_t)ok;
         ttft_ok[i] = (uint8_t)ok;
@@ -350,7 +357,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
           uint32_t id = e.id;
           /* per-request ITL = mean inter-token latency [A30] */
           double itl = (t - tfirst[id]) / (double)(out[id] - 1);
-          sum_itl += itl;
+          I->sum_itl += itl;
           int ok = itl <= s->slo_itl;
           n_itl_ok += (uint64_t)ok;
           n_both += (uint64_t)(ok && ttft_ok[id]);
@@ -388,7 +395,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         k = backlog ? K - 1 : lowest_feasible_ttft(p, L, K, nbt, prefill_budget(tgt_ttft, wait));
       }
       steps_ctrl++;
-      h = fold(h, 1, (uint64_t)q, (uint64_t)k, 0);
+      I->h = fold(I->h, 1, (uint64_t)q, (uint64_t)k, 0);
       double dur = predict_ttft(p, L[k], nbt); /* execution time = prediction (noise 0) [A25] */
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
       if (diag && diag->iter_n < diag->iter_cap) {
@@ -406,7 +413,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       I->ebusy += interval_energy(busy_power(p, 0, L[k], nbt), dur);
       I->bms += dur;
       I->iters++;
-      if (k == K - 1) top_ms += dur;
+      if (k == K - 1) I->top += dur;
     }
     for (int d = 0; d < ND && status == ORC_OK; ++d) {
       dec_inst *I = &D[d];
@@ -441,7 +448,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         k = backlog ? K - 1 : lowest_feasible_itl(p, L, K, I->nreq, I->nkv, tgt_itl);
       }
       steps_ctrl++;
-      h = fold(h, 2, (uint64_t)d, (uint64_t)k, 0);
+      I->h = fold(I->h, 2, (uint64_t)d, (uint64_t)k, 0);
       double dur = predict_itl(p, L[k], I->nreq, I->nkv);
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
       if (diag && diag->time_busy) diag->time_busy[d] += dur;
@@ -461,7 +468,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       I->ebusy += interval_energy(busy_power(p, 1, L[k], I->nreq), dur);
       I->bms += dur;
       I->iters++;
-      if (k == K - 1) top_ms += dur;
+      if (k == K - 1) I->top += dur;
     }
     if (status != ORC_OK) break;
   }
@@ -470,6 +477,14 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
     /* O9: horizon and idle energy [A23, A39] */
     double horizon = s->duration_ms > t_last ? s->duration_ms : t_last;
     double epb = 0.0, epi = 0.0, edb = 0.0, edi = 0.0, bp = 0.0, bd = 0.0;
+    double sum_ttft = 0.0, sum_itl = 0.0, top_ms = 0.0;
+    /* decision identity: route chain, then every prefill chain, then every decode chain [A36] */
+    uint64_t hh = splitmix64(h);
+    for (int q = 0; q < NP; ++q) hh = splitmix64(hh ^ P[q].h);
+    for (int d = 0; d < ND; ++d) hh = splitmix64(hh ^ D[d].h);
+    /* report-only totals: per-instance sums added in instance order [A37] */
+    for (int q = 0; q < NP; ++q) { sum_ttft += P[q].sum_ttft; top_ms += P[q].top; }
+    for (int d = 0; d < ND; ++d) { sum_itl += D[d].sum_itl; top_ms += D[d].top; }
     for (int q = 0; q < NP; ++q) {
       epb += P[q].ebusy;
       epi += interval_energy(p->p_idle, horizon - P[q].bms);
@@ -491,7 +506,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
     }
     res->steps_ctrl = steps_ctrl;
     res->steps_route = steps_route;
-    res->decision_hash = h;
+    res->decision_hash = hh;
     res->sum_ttft_ms = sum_ttft;
     res->sum_itl_mean_ms = sum_itl;
     res->e_prefill_busy_j = epb;

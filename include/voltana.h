@@ -169,6 +169,9 @@ typedef struct {
   const double *duration_ms;/* device [n_traces] nominal trace duration [A39]           */
   uint64_t n_traces;
   uint64_t max_requests;    /* host bound on any trace's request count (workspace size) */
+  uint32_t max_out;         /* host bound on out_len, 1..65535 (decode timing-wheel size);
+                               a scenario with a longer request gets status E_INPUT      */
+  uint32_t reserved;
 } voltana_traces;
 
 typedef struct {            /* device arrays [n]                                        */

@@ -53,7 +53,8 @@ class Grid(C.Structure):
 
 class Traces(C.Structure):
     _fields_ = [("arrival", vp), ("in_len", vp), ("out_len", vp), ("offset", vp), ("duration_ms", vp),
-                ("n_traces", C.c_uint64), ("max_requests", C.c_uint64)]
+                ("n_traces", C.c_uint64), ("max_requests", C.c_uint64), ("max_out", C.c_uint32),
+                ("reserved", C.c_uint32)]
 
 
 class Scenarios(C.Structure):

@@ -175,6 +175,7 @@ class DeviceWorkload:
         lens = np.diff(offset.astype(np.int64))
         self.n_traces = len(offset) - 1
         self.max_requests = int(lens.max()) if len(lens) else 0
+        self.max_out = int(np.max(traces.out_len)) if np.size(traces.out_len) else 1
         self.h2d_bytes = 0
         self.tr = dict(arrival=self._up(traces.arrival, torch.float64), in_len=self._up(traces.in_len, torch.uint32),
                        out_len=self._up(traces.out_len, torch.uint32), offset=self._up(offset, torch.uint64),
@@ -206,7 +207,7 @@ class DeviceWorkload:
         self.profs = (_lib.Profile * len(self.profiles))(*[p.struct for p in self.profiles])
         self.traces_struct = _lib.Traces(_p(self.tr["arrival"]), _p(self.tr["in_len"]), _p(self.tr["out_len"]),
                                          _p(self.tr["offset"]), _p(self.tr["duration"]), self.n_traces,
-                                         self.max_requests)
+                                         self.max_requests, max(1, min(self.max_out, 65535)), 0)
         self.scen_struct = _lib.Scenarios(*[_p(self.sc[k]) for k in ("trace_id", "slo_id", "layout_id", "grid_id",
                                                                      "profile_id", "hash_seed")])
         self.out = torch.empty((n, 128), dtype=torch.uint8, device=self.device)

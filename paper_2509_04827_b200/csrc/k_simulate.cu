@@ -1,18 +1,28 @@
 // k_simulate.cu — K4: batched trace-driven evaluation of EcoFreq + EcoRoute (north_star).
 //
-// One warp per scenario, persistent warps claiming scenarios in array order.
-// The event loop (A4-A23) runs warp-uniformly: every lane holds the
-// same scenario state in registers, so control flow never diverges; the lanes split
-// only the EcoPred evaluations across frequency levels (lane l evaluates ladder
-// levels l and l+32) and reduce "lowest feasible level" with one __ballot_sync —
-// an exact integer reduction, so decisions are bit-identical to the sequential scan.
+// One warp per scenario (persistent warps claim scenarios in array order). The scenario
+// is evaluated through its exact causal decomposition:
 //
-// Decode running sets use a per-instance timing wheel of NB buckets keyed by the
-// iteration index at which a request finishes (admission iteration + out - 2); all
-// running requests advance together (+1 token per iteration), so a
-// completion is O(1) instead of a scan of the running set. Buckets are singly
-// linked lists through per-request 16-byte nodes, appended in admission order, so
-// completions are processed in the oracle's order (A37) and sums are bit-exact.
+//  Phase A  Prefill instances never read decode state: requests go round robin by id
+//            and batches are FCFS (A6). Each prefill instance p is simulated
+//           by lane p, independently: batch formation, EcoFreq with the waiting-time budget
+//           (P:377-388), TTFT accounting, energy. Output: every request's first-token time,
+//           and per instance the chain of routed requests (out > 1) in completion order.
+//  Phase B  Routing happens at prefill completions, in (time, instance, id)
+//           order: a warp-wide min over the N_P stream heads picks the next request. Before
+//           routing at time t, decode lane d advances its own instance through every event
+//           strictly before t (iteration END/START, admission, EcoFreq, energy) — decode
+//           instances interact only through routing, and at equal times a PrefillDone drains
+//           before a DecodeIterDone and before every START (A18), so this order is exact.
+//           The what-if (f, f') of instance d is evaluated by lane d on its own state; the
+//           case analysis is a handful of warp reductions (ballot / reduce_min).
+// Decisions therefore match the sequential oracle bit for bit; the record's report-only
+// accumulators are per instance (A36/A37), so they match bit for bit too.
+//
+// Decode running sets: a per-instance timing wheel of NB >= max(out) buckets keyed by the
+// iteration index at which a request finishes (admission iteration + out - 2). All running
+// requests advance together (+1 token per iteration), so completions are O(1) per
+// request; buckets are lists appended in admission order (oracle order, A37).
 #include <cstdint>
 
 #include "vt_device.cuh"
@@ -20,95 +30,220 @@
 
 namespace vt {
 
-struct Node {       // 16 B per request of the scenario (workspace)
-  double tfirst;    // first-token time (prefill end)
-  uint32_t next;    // FIFO / wheel link
-  uint32_t tag;     // bit 31: TTFT met; bits 0..30: finishing iteration index
+struct Node {       // 16 B per request (workspace)
+  double tf;        // +t_first if the TTFT SLO was met, -t_first otherwise (t_first > 0)
+  uint32_t next;    // phase A: next routed request of the same prefill stream; later: queue/wheel link
+  uint16_t in, out;
 };
 
-// Lowest feasible ladder index given per-lane predictions for levels lane and lane+32.
-__device__ __forceinline__ int lowest_from(bool f0, bool f1, int K) {
-  unsigned m0 = __ballot_sync(FULL, f0);
-  if (m0) return ffs0(m0);
-  if (K > 32) {
-    unsigned m1 = __ballot_sync(FULL, f1);
-    if (m1) return 32 + ffs0(m1);
-  }
-  return K - 1;  // nothing feasible -> top level (A2)
-}
-
-// value held by the lane owning ladder index k (v0: levels 0..31, v1: 32..63)
-__device__ __forceinline__ double pick(double v0, double v1, int k) {
-  double x0 = __shfl_sync(FULL, v0, k & 31);
-  double x1 = __shfl_sync(FULL, v1, k & 31);
-  return k < 32 ? x0 : x1;
-}
-__device__ __forceinline__ int pick_i(int v0, int v1, int k) {
-  int x0 = __shfl_sync(FULL, v0, k & 31);
-  int x1 = __shfl_sync(FULL, v1, k & 31);
-  return k < 32 ? x0 : x1;
-}
-
-// Per-lane view of the scenario's ladder: lane l owns levels l and l+32.
-struct LaneLevels {
-  int K;
-  int lv0, lv1;          // profile-level index (0 if lane beyond K)
-  bool ok0, ok1;         // lane owns a level
-  double a1_0, c1_0, a1_1, c1_1;
-  double dp0, dp1, dd0, dd1;  // busy dynamic power prefill / decode
-  int mhz0, mhz1;
+// ------------------------------------------------------------------ per-warp tables (smem)
+struct Tables {
+  int K, T, W, kp;
+  bool itl_smem, mono_tt, mono_it;
+  const uint16_t *lad;     // [K] profile levels
+  const double *tt;        // [K][2] a1, c1
+  const double *dyn;       // [2][K] prefill, decode
+  const int *mhz;          // [K]
+  const double *it;        // [T][K][3] (itl_smem)
+  const double *a2g, *b2g, *c2g;
 };
 
-// eq:pred-itl for ladder index (lane, lane+32) at (n, kv): predictions and feasibility.
-struct ItlEval { double p0, p1; bool f0, f1; };
-
-__device__ __forceinline__ ItlEval itl_eval(const DevProfile &PR, const LaneLevels &L, uint32_t n,
-                                            uint32_t kv, double target) {
-  uint32_t j = tile_of(n, (uint32_t)PR.tile_w, (uint32_t)PR.n_tiles);
-  size_t row = (size_t)j * (size_t)PR.k;
-  ItlEval e;
-  e.p0 = 0.0; e.p1 = 0.0;
-  if (L.ok0) {
-    size_t o = row + (size_t)L.lv0;
-    e.p0 = itl_pred(__ldg(PR.a2 + o), __ldg(PR.b2 + o), __ldg(PR.c2 + o), n, kv);
-  }
-  if (L.ok1) {
-    size_t o = row + (size_t)L.lv1;
-    e.p1 = itl_pred(__ldg(PR.a2 + o), __ldg(PR.b2 + o), __ldg(PR.c2 + o), n, kv);
-  }
-  e.f0 = L.ok0 && e.p0 <= target;
-  e.f1 = L.ok1 && e.p1 <= target;
-  return e;
+__device__ __forceinline__ uint32_t tile_j(const Tables &S, uint32_t n) {
+  uint32_t j = (n - 1u) / (uint32_t)S.W;
+  return j < (uint32_t)(S.T - 1) ? j : (uint32_t)(S.T - 1);
 }
 
-template <int MAXP, int MAXD>
-__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot) {
-  const int lane = lane_id();
-  voltana_result R;
-  R = voltana_result{};
-  // ---------------------------------------------------------------- scenario tables
-  {
-    const bool ids_ok = P.trace_id[s] < P.n_traces && P.slo_id[s] < P.n_slos && P.layout_id[s] < P.n_layouts &&
-                        P.grid_id[s] < P.n_grids && P.profile_id[s] < P.n_profiles;
-    if (!ids_ok) {
-      R.status = VOLTANA_ITEM_E_INPUT;
-      if (lane == 0) P.out[s] = R;
-      return;
+__device__ __forceinline__ double itl_at(const Tables &S, uint32_t j, int k, uint32_t n, uint32_t kv) {
+  if (S.itl_smem) {
+    const double *r = S.it + 3 * ((size_t)j * S.K + k);
+    return itl_pred(r[0], r[1], r[2], n, kv);
+  }
+  const size_t o = (size_t)j * S.kp + S.lad[k];
+  return itl_pred(__ldg(S.a2g + o), __ldg(S.b2g + o), __ldg(S.c2g + o), n, kv);
+}
+
+__device__ __forceinline__ double ttft_at(const Tables &S, int k, uint32_t nbt) {
+  return ttft_pred(S.tt[2 * k], S.tt[2 * k + 1], nbt);
+}
+
+// Lowest ladder index whose prediction meets `target` (A1), else K-1 (A2);
+// *pred = the prediction at the returned index. Ascending scan with early exit, or an
+// exact binary search when the tables are coefficient-monotone in f (A32).
+__device__ int lowest_itl(const Tables &S, uint32_t n, uint32_t kv, double target, double *pred) {
+  const uint32_t j = tile_j(S, n);
+  if (S.mono_it && S.K > 8) {
+    int lo = 0, hi = S.K;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (itl_at(S, j, mid, n, kv) <= target) hi = mid; else lo = mid + 1;
     }
+    int k = lo < S.K ? lo : S.K - 1;
+    *pred = itl_at(S, j, k, n, kv);
+    return k;
+  }
+  for (int k = 0; k < S.K - 1; ++k) {
+    double p = itl_at(S, j, k, n, kv);
+    if (p <= target) { *pred = p; return k; }
+  }
+  *pred = itl_at(S, j, S.K - 1, n, kv);
+  return S.K - 1;
+}
+
+__device__ int lowest_ttft(const Tables &S, uint32_t nbt, double budget, double *pred) {
+  if (S.mono_tt && S.K > 8) {
+    int lo = 0, hi = S.K;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (ttft_at(S, mid, nbt) <= budget) hi = mid; else lo = mid + 1;
+    }
+    int k = lo < S.K ? lo : S.K - 1;
+    *pred = ttft_at(S, k, nbt);
+    return k;
+  }
+  for (int k = 0; k < S.K - 1; ++k) {
+    double p = ttft_at(S, k, nbt);
+    if (p <= budget) { *pred = p; return k; }
+  }
+  *pred = ttft_at(S, S.K - 1, nbt);
+  return S.K - 1;
+}
+
+// ------------------------------------------------------------------ scenario context
+struct Ctx {
+  Node *node;
+  uint2 *wheel;            // this lane's decode instance: [NB] {head, tail}
+  uint32_t nbm;
+  double tau, slo_itl, tgt_itl, p_idle, tdp, uh_d;
+  uint32_t kvcap;
+};
+
+struct Err {               // first error of one lane in its own event order
+  double t;                // +inf = none
+  uint32_t code;
+};
+
+// Decode instance state: owned by lane d.
+struct Dec {
+  uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both;
+  bool busy, dead;
+  double end, ebusy, bms, top, sitl, tlast;
+  uint64_t h;
+};
+
+__device__ __forceinline__ double avail_time(const Ctx &C, uint32_t i) {
+  return add(fabs(C.node[i].tf), C.tau);  // KvTransferDone time = t_first + tau (A18); tau = 0: routing time
+}
+
+// Advance decode instance `d` through every event with time < t_lim (END, START).
+__device__ void dec_advance(Dec &D, int d, const Ctx &C, const Tables &S, double t_lim, Err &E) {
+  if (D.dead) return;
+  for (;;) {
+    double tnow;
+    if (D.busy) {
+      if (!(D.end < t_lim)) return;
+      tnow = D.end;
+      // ---- O6 DecodeIterDone: +1 KV token per running request, completions of this iteration
+      D.nkv += D.nreq;
+      uint2 *bk = C.wheel + (D.cur & C.nbm);
+      const uint2 b = *bk;
+      uint32_t r = b.x;
+      while (r != NIL) {
+        const Node nd = C.node[r];
+        const double itl = div(sub(tnow, fabs(nd.tf)), (double)(nd.out - 1u));  // A30
+        D.sitl = add(D.sitl, itl);
+        const bool ok = itl <= C.slo_itl;
+        D.n_itl_ok += ok;
+        D.n_both += ok && nd.tf > 0.0;
+        D.nreq -= 1u;
+        D.nkv -= (uint32_t)nd.in + (uint32_t)nd.out;
+        r = nd.next;
+      }
+      if (b.x != NIL) *bk = make_uint2(NIL, NIL);
+      D.busy = false;
+      D.tlast = tnow;
+    } else {
+      // idle: the next START happens when the head of the admission queue becomes available
+      if (D.qh == NIL) return;
+      const double av = avail_time(C, D.qh);
+      if (!(av < t_lim)) return;
+      tnow = av;
+    }
+    // ---- O7 START_DECODE at tnow: FCFS admission while KV fits (A20)
+    while (D.qh != NIL) {
+      const uint32_t i = D.qh;
+      const Node hn = C.node[i];
+      if (!(add(fabs(hn.tf), C.tau) <= tnow)) break;  // still in KV transfer
+      const uint32_t need = (uint32_t)hn.in + 1u;
+      if (D.nkv + need > C.kvcap) break;
+      D.qh = hn.next;
+      if (D.qh == NIL) D.qt = NIL;
+      const uint32_t fin = D.iters + (uint32_t)hn.out - 2u;  // its last iteration
+      uint2 *bk = C.wheel + (fin & C.nbm);
+      uint2 b = *bk;
+      C.node[i].next = NIL;
+      if (b.y == NIL) b.x = i; else C.node[b.y].next = i;
+      b.y = i;
+      *bk = b;
+      D.nreq += 1u;
+      D.nkv += need;
+      D.pn -= 1u;
+      D.pkv -= need;
+    }
+    const bool backlog = D.qh != NIL && avail_time(C, D.qh) <= tnow;  // A5
+    if (D.nreq == 0u) {
+      if (backlog) { E.t = tnow; E.code = VOLTANA_ITEM_E_KV; D.dead = true; return; }
+      continue;  // stays idle
+    }
+    double dur;
+    int k;
+    if (backlog) { k = S.K - 1; dur = itl_at(S, tile_j(S, D.nreq), k, D.nreq, D.nkv); }
+    else k = lowest_itl(S, D.nreq, D.nkv, C.tgt_itl, &dur);
+    D.h = fold(D.h, 2, (uint64_t)d, (uint64_t)k, 0);
+    if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
+    D.end = add(tnow, dur);
+    D.busy = true;
+    D.ebusy = add(D.ebusy, energy_j(busy_power(C.p_idle, C.tdp, C.uh_d, S.dyn[S.K + k], D.nreq), dur));
+    D.bms = add(D.bms, dur);
+    if (k == S.K - 1) D.top = add(D.top, dur);
+    D.cur = D.iters;
+    D.iters += 1u;
+  }
+}
+
+// warp-wide min of a non-negative double held by lanes with `valid`; returns the lowest lane
+// attaining it, or -1 if no lane is valid. Bit patterns of non-negative doubles order as u64.
+__device__ __forceinline__ int argmin_time(double t, bool valid) {
+  const uint64_t b = __double_as_longlong(t);
+  const uint32_t hi = valid ? (uint32_t)(b >> 32) : 0xffffffffu;
+  const uint32_t mhi = __reduce_min_sync(FULL, hi);
+  const bool c1 = valid && hi == mhi;
+  const uint32_t lo = c1 ? (uint32_t)b : 0xffffffffu;
+  const uint32_t mlo = __reduce_min_sync(FULL, lo);
+  const unsigned m = __ballot_sync(FULL, c1 && lo == mlo);
+  return m ? ffs0(m) : -1;
+}
+
+__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *wheels, char *wsm) {
+  const int lane = lane_id();
+  voltana_result R = voltana_result{};
+  // ---------------------------------------------------------------- ids and table rows
+  if (!(P.trace_id[s] < P.n_traces && P.slo_id[s] < P.n_slos && P.layout_id[s] < P.n_layouts &&
+        P.grid_id[s] < P.n_grids && P.profile_id[s] < P.n_profiles)) {
+    R.status = VOLTANA_ITEM_E_INPUT;
+    if (lane == 0) P.out[s] = R;
+    return;
   }
   const uint32_t tr = P.trace_id[s];
   const voltana_slo &SL = P.slo[P.slo_id[s]];
   const voltana_layout &LY = P.lay[P.layout_id[s]];
   const voltana_grid &GR = P.grid[P.grid_id[s]];
   const DevProfile &PR = P.prof[P.profile_id[s]];
-  const uint64_t h0 = P.hash_seed[s];
   const uint64_t off = P.offset[tr];
   const uint64_t N64 = P.offset[tr + 1] - off;
   const double Dur = P.duration[tr];
   const double *arr = P.arrival + off;
   const uint32_t *inl = P.in_len + off;
   const uint32_t *outl = P.out_len + off;
-
   R.n_requests = (uint32_t)N64;
 
   // ---------------------------------------------------------------- device validation (A40)
@@ -117,9 +252,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot) {
     uint64_t tok = 0;
     if (ok) {
       for (uint64_t i = lane; i < N64; i += 32) {
-        uint32_t a = inl[i], b = outl[i];
-        double x = arr[i];
-        ok = ok && a >= 1u && a <= 65535u && b >= 1u && b <= 65535u && x >= 0.0 && x < 1e9;
+        const uint32_t a = inl[i], b = outl[i];
+        const double x = arr[i];
+        ok = ok && a >= 1u && a <= 65535u && b >= 1u && b <= P.max_out && x >= 0.0 && x < 1e9;
         if (i > 0) ok = ok && !(x < arr[i - 1]);
         tok += (uint64_t)a + b;
       }
@@ -133,401 +268,292 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot) {
     }
   }
   const uint32_t N = (uint32_t)N64;
-  const int K = GR.k;
   const int NP = LY.n_p, ND = LY.n_d;
-  const uint32_t B = LY.max_batch_tokens, C = LY.kv_capacity;
-  const double tau = LY.kv_transfer_ms;
+
+  // ---------------------------------------------------------------- stage the ladder's tables
+  Tables S;
+  S.K = GR.k; S.T = PR.n_tiles; S.W = PR.tile_w; S.kp = PR.k;
+  S.itl_smem = P.itl_smem != 0;
+  {
+    char *p = wsm;
+    uint16_t *lad = (uint16_t *)p; p += 128;
+    double *tt = (double *)p; p += 16 * VOLTANA_MAX_LEVELS;
+    double *dyn = (double *)p; p += 16 * VOLTANA_MAX_LEVELS;
+    int *mhz = (int *)p; p += 4 * VOLTANA_MAX_LEVELS;
+    double *it = (double *)p;
+    for (int k = lane; k < S.K; k += 32) {
+      const int lv = GR.level[k];
+      lad[k] = (uint16_t)lv;
+      tt[2 * k] = PR.a1[lv]; tt[2 * k + 1] = PR.c1[lv];
+      dyn[k] = PR.dyn[lv]; dyn[S.K + k] = PR.dyn[PR.k + lv];
+      mhz[k] = PR.mhz[lv];
+    }
+    if (S.itl_smem) {
+      for (int x = lane; x < S.T * S.K; x += 32) {
+        const int j = x / S.K, k = x - j * S.K;
+        const size_t o = (size_t)j * PR.k + GR.level[k];
+        it[3 * x] = PR.a2[o]; it[3 * x + 1] = PR.b2[o]; it[3 * x + 2] = PR.c2[o];
+      }
+    }
+    __syncwarp();
+    S.lad = lad; S.tt = tt; S.dyn = dyn; S.mhz = mhz; S.it = it;
+    S.a2g = PR.a2; S.b2g = PR.b2; S.c2g = PR.c2;
+    // coefficient-monotone (non-increasing in f) tables allow the exact binary search (A32)
+    bool mt = true, mi = true;
+    for (int k = lane; k + 1 < S.K; k += 32)
+      mt = mt && tt[2 * k + 2] <= tt[2 * k] && tt[2 * k + 3] <= tt[2 * k + 1];
+    for (int x = lane; x < S.T * (S.K - 1); x += 32) {
+      const int j = x / (S.K - 1), k = x - j * (S.K - 1);
+      const size_t o0 = (size_t)j * PR.k + GR.level[k], o1 = (size_t)j * PR.k + GR.level[k + 1];
+      mi = mi && PR.a2[o1] <= PR.a2[o0] && PR.b2[o1] <= PR.b2[o0] && PR.c2[o1] <= PR.c2[o0];
+    }
+    S.mono_tt = __all_sync(FULL, mt);
+    S.mono_it = __all_sync(FULL, mi);
+  }
+  Node *node = (Node *)slot;
   const double tgt_ttft = mul(SL.scale, SL.ttft_ms);  // A3
   const double tgt_itl = mul(SL.scale, SL.itl_ms);
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
 
-  LaneLevels L;
-  L.K = K;
-  L.ok0 = lane < K;
-  L.ok1 = lane + 32 < K;
-  L.lv0 = L.ok0 ? GR.level[lane] : 0;
-  L.lv1 = L.ok1 ? GR.level[lane + 32] : 0;
-  L.a1_0 = __ldg(PR.a1 + L.lv0); L.c1_0 = __ldg(PR.c1 + L.lv0);
-  L.a1_1 = __ldg(PR.a1 + L.lv1); L.c1_1 = __ldg(PR.c1 + L.lv1);
-  L.dp0 = __ldg(PR.dyn + L.lv0); L.dp1 = __ldg(PR.dyn + L.lv1);
-  L.dd0 = __ldg(PR.dyn + PR.k + L.lv0); L.dd1 = __ldg(PR.dyn + PR.k + L.lv1);
-  L.mhz0 = __ldg(PR.mhz + L.lv0); L.mhz1 = __ldg(PR.mhz + L.lv1);
-
-  // ---------------------------------------------------------------- workspace views
-  Node *node = (Node *)slot;
-  uint8_t *xd = (uint8_t *)(slot + P.node_bytes);
-  uint2 *wheel = (uint2 *)(slot + P.node_bytes + P.xd_bytes);
-  const uint32_t NB = P.nb, NBM = P.nb - 1;
-  for (uint32_t i = lane; i < (uint32_t)ND * NB; i += 32) wheel[i] = make_uint2(NIL, NIL);
-  __syncwarp();
-
-  // ---------------------------------------------------------------- state (warp-uniform)
-  uint32_t p_qhead[MAXP], p_bstart[MAXP], p_bcnt[MAXP];
-  bool p_busy[MAXP];
-  double p_end[MAXP], p_ebusy[MAXP], p_bms[MAXP];
-#pragma unroll
-  for (int q = 0; q < MAXP; ++q) {
-    p_qhead[q] = q; p_bstart[q] = 0; p_bcnt[q] = 0; p_busy[q] = false;
-    p_end[q] = 0.0; p_ebusy[q] = 0.0; p_bms[q] = 0.0;
-  }
-  uint32_t d_nreq[MAXD], d_nkv[MAXD], d_pn[MAXD], d_pkv[MAXD], d_iters[MAXD], d_cur[MAXD];
-  uint32_t d_qh[MAXD], d_qt[MAXD];
-  bool d_busy[MAXD];
-  double d_end[MAXD], d_ebusy[MAXD], d_bms[MAXD];
-#pragma unroll
-  for (int d = 0; d < MAXD; ++d) {
-    d_nreq[d] = 0; d_nkv[d] = 0; d_pn[d] = 0; d_pkv[d] = 0; d_iters[d] = 0; d_cur[d] = 0;
-    d_qh[d] = NIL; d_qt[d] = NIL; d_busy[d] = false;
-    d_end[d] = 0.0; d_ebusy[d] = 0.0; d_bms[d] = 0.0;
-  }
-  uint32_t a = 0, cursor = 0, xh = NIL, xt = NIL, status = 0;
-  uint64_t h = h0, steps_ctrl = 0, steps_route = 0;
-  uint32_t n_ttft_ok = 0, n_itl_ok = 0, n_both = 0, prefill_iters = 0;
-  double sum_ttft = 0.0, sum_itl = 0.0, top_ms = 0.0, t = 0.0, t_last = 0.0;
-  double next_arr = N > 0 ? arr[0] : 0.0;
-
-  for (;;) {
-    // ------------------------------------------------------------ O1: next event time
-    bool have = false;
-    double tn = 0.0;
-    if (a < N) { tn = next_arr; have = true; }
-    if (xh != NIL) {
-      double tx = add(node[xh].tfirst, tau);
-      if (!have || tx < tn) { tn = tx; have = true; }
-    }
-#pragma unroll
-    for (int q = 0; q < MAXP; ++q)
-      if (q < NP && p_busy[q] && (!have || p_end[q] < tn)) { tn = p_end[q]; have = true; }
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d)
-      if (d < ND && d_busy[d] && (!have || d_end[d] < tn)) { tn = d_end[d]; have = true; }
-    if (!have) break;
-    t = tn;
-    t_last = t;
-
-    // ------------------------------------------------------------ O2/O3: arrivals at t
-    while (a < N && next_arr == t) {
-      ++a;
-      next_arr = a < N ? arr[a] : 0.0;
-    }
-    // ------------------------------------------------------------ O4: KV transfers done
-    while (xh != NIL) {
-      Node nd = node[xh];
-      if (!(add(nd.tfirst, tau) == t)) break;
-      uint32_t i = xh, dd = xd[i];
-      xh = nd.next;
-      if (xh == NIL) xt = NIL;
-#pragma unroll
-      for (int d = 0; d < MAXD; ++d) {
-        if (d == (int)dd) {
-          if (d_qt[d] == NIL) d_qh[d] = i; else node[d_qt[d]].next = i;
-          d_qt[d] = i;
-        }
+  // ================================================================ PHASE A: prefill lanes
+  double p_ebusy = 0.0, p_bms = 0.0, p_top = 0.0, p_sttft = 0.0, p_tlast = 0.0;
+  uint64_t p_h = P.hash_seed[s];
+  uint32_t p_iters = 0, p_ttft_ok = 0, p_itl_ok = 0, p_both = 0, p_head = NIL;
+  Err pE = {INF, 0};
+  if (lane < NP) {
+    const uint32_t p = (uint32_t)lane, NPu = (uint32_t)NP;
+    double tfree = 0.0;
+    uint32_t nxt = p, prev = NIL;
+    Node pend;
+    pend.tf = 0.0; pend.next = NIL; pend.in = 0; pend.out = 0;
+    while (nxt < N) {
+      const double a0 = arr[nxt];
+      const double ts = tfree > a0 ? tfree : a0;  // START: instance idle and queue non-empty
+      // FCFS prefix of the arrived queue with sum(in) <= B, at least one request (A6)
+      uint32_t nbt = inl[nxt], cnt = 1, id = nxt + NPu;
+      bool backlog = false;
+      while (id < N) {
+        if (!(arr[id] <= ts)) break;
+        const uint32_t x = inl[id];
+        if (nbt + x > LY.max_batch_tokens) { backlog = true; break; }
+        nbt += x; cnt++; id += NPu;
       }
-      node[i].next = NIL;
-    }
-    // ------------------------------------------------------------ O5: PrefillDone
-#pragma unroll
-    for (int q = 0; q < MAXP; ++q) {
-      if (!(q < NP && p_busy[q] && p_end[q] == t)) continue;
-      for (uint32_t jj = 0; jj < p_bcnt[q]; ++jj) {
-        uint32_t i = p_bstart[q] + jj * (uint32_t)NP;
-        double ttft = sub(t, arr[i]);  // A26
-        sum_ttft = add(sum_ttft, ttft);
-        bool tok = ttft <= SL.ttft_ms;
-        n_ttft_ok += tok;
-        uint32_t oi = outl[i], ii = inl[i];
-        if (oi == 1u) {  // finished at prefill (A8, A30)
-          n_itl_ok += 1;
-          n_both += tok;
+      // (A5) backlog: requests still queued after the batch
+      double budget = sub(tgt_ttft, sub(ts, a0));  // A4: SLO minus the oldest request's wait
+      budget = budget > 0.0 ? budget : 0.0;
+      double dur;
+      int k;
+      if (backlog) { k = S.K - 1; dur = ttft_at(S, k, nbt); }
+      else k = lowest_ttft(S, nbt, budget, &dur);
+      p_h = fold(p_h, 1, (uint64_t)p, (uint64_t)k, 0);
+      p_iters++;
+      if (!(dur > 0.0)) { pE.t = ts; pE.code = VOLTANA_ITEM_E_CONTRACT; break; }
+      const double end = add(ts, dur);
+      p_ebusy = add(p_ebusy, energy_j(busy_power(PR.p_idle, PR.tdp, PR.uh[0], S.dyn[k], nbt), dur));
+      p_bms = add(p_bms, dur);
+      if (k == S.K - 1) p_top = add(p_top, dur);
+      // ---- O5 PrefillDone at `end`, batch in FCFS order
+      for (uint32_t q = 0, i = nxt; q < cnt; ++q, i += NPu) {
+        const double ttft = sub(end, arr[i]);  // A26
+        p_sttft = add(p_sttft, ttft);
+        const bool ok = ttft <= SL.ttft_ms;
+        p_ttft_ok += ok;
+        const uint32_t o = outl[i];
+        if (o == 1u) {  // first token came from prefill: done (A8, A30)
+          p_itl_ok++;
+          p_both += ok;
           continue;
         }
-        // ---------------------------------------------------- O8: EcoRoute
-        int dsel, cse;
-        if (LY.policy == 1 || ND == 1) {
-          dsel = (int)cursor;
-          cursor = (cursor + 1u) % (uint32_t)ND;
-          cse = 0;
-        } else {
-          int fnow[MAXD], faft[MAXD];
-#pragma unroll
-          for (int d = 0; d < MAXD; ++d) {
-            fnow[d] = 0; faft[d] = 0;
-            if (d < ND) {
-              uint32_t n = d_nreq[d] + d_pn[d];  // effective state (A9)
-              uint32_t kv = d_nkv[d] + d_pkv[d];
-              int kn = 0;
-              if (n > 0) {
-                ItlEval e = itl_eval(PR, L, n, kv, tgt_itl);
-                kn = lowest_from(e.f0, e.f1, K);
-              }
-              ItlEval e2 = itl_eval(PR, L, n + 1u, kv + ii + 1u, tgt_itl);  // A12
-              int ka = lowest_from(e2.f0, e2.f1, K);
-              fnow[d] = pick_i(L.mhz0, L.mhz1, kn);
-              faft[d] = pick_i(L.mhz0, L.mhz1, ka);
-            }
-          }
-          // U/R partition and cases (1)-(5) (A13-A16), integer MHz
-          int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
-#pragma unroll
-          for (int d = 0; d < MAXD; ++d) {
-            if (d < ND) {
-              bool cr = faft[d] > fnow[d];
-              ncross += cr;
-              if (!cr && fnow[d] < mu) mu = fnow[d];
-              if (cr && faft[d] < mr) mr = faft[d];
-              if (fnow[d] < mn) mn = fnow[d];
-              if (faft[d] < ma) ma = faft[d];
-            }
-          }
-          unsigned inset = 0;
-          if (ncross == 0) {
-#pragma unroll
-            for (int d = 0; d < MAXD; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
-            cse = __popc(inset) == 1 ? 1 : 2;
-          } else if (ncross < ND) {
-            long long g = (long long)mu - (long long)mr;
-            if (g <= (long long)LY.delta_mhz) {
-#pragma unroll
-              for (int d = 0; d < MAXD; ++d)
-                if (d < ND && !(faft[d] > fnow[d]) && fnow[d] == mu) inset |= 1u << d;
-              cse = 3;
-            } else {
-#pragma unroll
-              for (int d = 0; d < MAXD; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
-              cse = 4;
-            }
-          } else {
-#pragma unroll
-            for (int d = 0; d < MAXD; ++d) if (d < ND && faft[d] == ma) inset |= 1u << d;
-            cse = 5;
-          }
-          // round robin among the candidate set from the cursor (A17)
-          unsigned rot = ((inset >> cursor) | (inset << (ND - cursor))) & ((1u << ND) - 1u);
-          dsel = (int)((cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND);
-          if (__popc(inset) >= 2) cursor = (uint32_t)(dsel + 1) % (uint32_t)ND;
-        }
-        steps_route++;
-        h = fold(h, 3, (uint64_t)dsel, 0, (uint64_t)cse);
-        Node nw;
-        nw.tfirst = t;
-        nw.next = NIL;
-        nw.tag = tok ? 0x80000000u : 0u;
-        node[i] = nw;
-#pragma unroll
-        for (int d = 0; d < MAXD; ++d) {
-          if (d == dsel) {
-            d_pn[d] += 1u;
-            d_pkv[d] += ii + 1u;
-            if (tau == 0.0) {
-              if (d_qt[d] == NIL) d_qh[d] = i; else node[d_qt[d]].next = i;
-              d_qt[d] = i;
-            }
-          }
-        }
-        if (tau != 0.0) {
-          xd[i] = (uint8_t)dsel;
-          if (xt == NIL) xh = i; else node[xt].next = i;
-          xt = i;
-        }
+        if (prev != NIL) { pend.next = i; node[prev] = pend; } else p_head = i;
+        prev = i;
+        pend.tf = ok ? end : -end;
+        pend.next = NIL;
+        pend.in = (uint16_t)inl[i];
+        pend.out = (uint16_t)o;
       }
-      p_busy[q] = false;
+      tfree = end;
+      p_tlast = end;
+      nxt = id;
     }
-    // ------------------------------------------------------------ O6: DecodeIterDone
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      if (!(d < ND && d_busy[d] && d_end[d] == t)) continue;
-      d_nkv[d] += d_nreq[d];  // +1 KV token per running request (A19)
-      const uint32_t cur = d_cur[d];
-      uint2 *bk = wheel + (size_t)d * NB + (cur & NBM);
-      uint2 hb = *bk;
-      uint32_t r = hb.x, prev = NIL, nh = NIL;
-      while (r != NIL) {
-        Node nd = node[r];
-        uint32_t nxt = nd.next;
-        if ((nd.tag & 0x7fffffffu) == cur) {
-          uint32_t oi = outl[r], ii = inl[r];
-          double itl = div(sub(t, nd.tfirst), (double)(oi - 1u));  // A30
-          sum_itl = add(sum_itl, itl);
-          bool ok = itl <= SL.itl_ms;
-          n_itl_ok += ok;
-          n_both += ok && (nd.tag >> 31);
-          d_nreq[d] -= 1u;
-          d_nkv[d] -= ii + oi;
-          if (prev != NIL) node[prev].next = nxt;
-        } else {
-          if (nh == NIL) nh = r;
-          prev = r;
-        }
-        r = nxt;
-      }
-      *bk = make_uint2(nh, prev);
-      d_busy[d] = false;
-    }
-
-    // ------------------------------------------------------------ O7: START prefill
-#pragma unroll
-    for (int q = 0; q < MAXP; ++q) {
-      if (!(q < NP && !p_busy[q] && p_qhead[q] < a)) continue;
-      // FCFS prefix with sum(in) <= B, at least one request (A6), 32 candidates per step
-      uint32_t id = p_qhead[q], nbt = 0, cnt = 0;
-      for (;;) {
-        uint32_t idj = id + (uint32_t)lane * (uint32_t)NP;
-        bool valid = idj < a;
-        uint32_t v = valid ? inl[idj] : 0u;
-        uint32_t pre = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          uint32_t y = __shfl_up_sync(FULL, pre, o);
-          if (lane >= o) pre += y;
-        }
-        bool fits = valid && (nbt + pre <= B || (cnt == 0u && lane == 0));
-        unsigned m = __ballot_sync(FULL, fits);
-        uint32_t nfit = (uint32_t)__popc(m);
-        uint32_t add_tok = __shfl_sync(FULL, pre, (int)(nfit > 0 ? nfit - 1 : 0));
-        if (nfit > 0) nbt += add_tok;
-        cnt += nfit;
-        id += nfit * (uint32_t)NP;
-        if (nfit < 32u || id >= a) break;
-      }
-      const bool backlog = id < a;  // A5
-      const double wait = sub(t, arr[p_qhead[q]]);
-      double budget = sub(tgt_ttft, wait);
-      budget = budget > 0.0 ? budget : 0.0;  // A4
-      double p0 = ttft_pred(L.a1_0, L.c1_0, nbt), p1 = ttft_pred(L.a1_1, L.c1_1, nbt);
-      int k = lowest_from(L.ok0 && p0 <= budget, L.ok1 && p1 <= budget, K);
-      if (backlog) k = K - 1;
-      steps_ctrl++;
-      h = fold(h, 1, (uint64_t)q, (uint64_t)k, 0);
-      const double dur = pick(p0, p1, k);
-      if (!(dur > 0.0)) { status = VOLTANA_ITEM_E_CONTRACT; break; }
-      const double dyn = pick(L.dp0, L.dp1, k);
-      p_end[q] = add(t, dur);
-      p_busy[q] = true;
-      p_bstart[q] = p_qhead[q];
-      p_bcnt[q] = cnt;
-      p_qhead[q] = id;
-      p_ebusy[q] = add(p_ebusy[q], energy_j(busy_power(PR.p_idle, PR.tdp, PR.uh[0], dyn, nbt), dur));
-      p_bms[q] = add(p_bms[q], dur);
-      prefill_iters++;
-      if (k == K - 1) top_ms = add(top_ms, dur);
-    }
-    if (status) break;
-    // ------------------------------------------------------------ O7: START decode
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      if (!(d < ND && !d_busy[d])) continue;
-      // admission at the iteration boundary, FCFS while KV fits (A20)
-      while (d_qh[d] != NIL) {
-        const uint32_t hd = d_qh[d];
-        const uint32_t ii = inl[hd];
-        const uint32_t need = ii + 1u;
-        if (d_nkv[d] + need > C) break;
-        Node nd = node[hd];
-        d_qh[d] = nd.next;
-        if (d_qh[d] == NIL) d_qt[d] = NIL;
-        const uint32_t fin = d_iters[d] + outl[hd] - 2u;  // last iteration of this request
-        nd.next = NIL;
-        nd.tag = (nd.tag & 0x80000000u) | fin;
-        node[hd] = nd;
-        uint2 *bk = wheel + (size_t)d * NB + (fin & NBM);
-        uint2 w = *bk;
-        if (w.y == NIL) { w.x = hd; } else { node[w.y].next = hd; }
-        w.y = hd;
-        *bk = w;
-        d_nreq[d] += 1u;
-        d_nkv[d] += need;
-        d_pn[d] -= 1u;
-        d_pkv[d] -= need;
-      }
-      if (d_nreq[d] == 0u) {
-        if (d_qh[d] != NIL) { status = VOLTANA_ITEM_E_KV; break; }
-        continue;
-      }
-      const bool backlog = d_qh[d] != NIL;
-      ItlEval e = itl_eval(PR, L, d_nreq[d], d_nkv[d], tgt_itl);
-      int k = lowest_from(e.f0, e.f1, K);
-      if (backlog) k = K - 1;
-      steps_ctrl++;
-      h = fold(h, 2, (uint64_t)d, (uint64_t)k, 0);
-      const double dur = pick(e.p0, e.p1, k);
-      if (!(dur > 0.0)) { status = VOLTANA_ITEM_E_CONTRACT; break; }
-      const double dyn = pick(L.dd0, L.dd1, k);
-      d_end[d] = add(t, dur);
-      d_busy[d] = true;
-      d_ebusy[d] = add(d_ebusy[d], energy_j(busy_power(PR.p_idle, PR.tdp, PR.uh[1], dyn, d_nreq[d]), dur));
-      d_bms[d] = add(d_bms[d], dur);
-      d_cur[d] = d_iters[d];
-      d_iters[d] += 1u;
-      if (k == K - 1) top_ms = add(top_ms, dur);
-    }
-    if (status) break;
+    if (prev != NIL) { pend.next = NIL; node[prev] = pend; }
   }
+  __syncwarp();
 
-  if (status) {
-    R.status = status;
-  } else {
-    // ------------------------------------------------------------ O9: totals (A23)
-    const double horizon = Dur > t_last ? Dur : t_last;
-    double epb = 0.0, epi = 0.0, edb = 0.0, edi = 0.0, bp = 0.0, bd = 0.0;
-#pragma unroll
-    for (int q = 0; q < MAXP; ++q) {
-      if (q < NP) {
-        epb = add(epb, p_ebusy[q]);
-        epi = add(epi, energy_j(PR.p_idle, sub(horizon, p_bms[q])));
-        bp = add(bp, p_bms[q]);
-      }
+  // ================================================================ PHASE B: routing + decode lanes
+  Ctx C;
+  C.node = node;
+  C.wheel = wheels + (size_t)(lane < ND ? lane : 0) * P.nb;
+  C.nbm = P.nb - 1u;
+  C.tau = LY.kv_transfer_ms; C.slo_itl = SL.itl_ms; C.tgt_itl = tgt_itl;
+  C.p_idle = PR.p_idle; C.tdp = PR.tdp; C.uh_d = PR.uh[1]; C.kvcap = LY.kv_capacity;
+  Dec D;
+  D.nreq = D.nkv = D.pn = D.pkv = D.iters = D.cur = 0;
+  D.qh = D.qt = NIL;
+  D.n_itl_ok = D.n_both = 0;
+  D.busy = false; D.dead = !(lane < ND);
+  D.end = D.ebusy = D.bms = D.top = D.sitl = D.tlast = 0.0;
+  D.h = P.hash_seed[s];
+  Err dE = {INF, 0};
+
+  // stream head of prefill lane p: next routed request in its completion order
+  uint32_t hd = lane < NP ? p_head : NIL;
+  double ht = 0.0;
+  uint32_t hsucc = NIL, hin = 0;
+  if (hd != NIL) { const Node n0 = node[hd]; ht = fabs(n0.tf); hsucc = n0.next; hin = n0.in; }
+  uint64_t h_r = P.hash_seed[s];
+  uint32_t cursor = 0, steps_route = 0;
+  const bool eco = LY.policy == 0 && ND > 1;
+  for (;;) {
+    const int w = argmin_time(ht, hd != NIL);  // next PrefillDone request in (t, p, id) order
+    if (w < 0) break;
+    const double t = __shfl_sync(FULL, ht, w);
+    const uint32_t i = __shfl_sync(FULL, hd, w);
+    const uint32_t in_i = __shfl_sync(FULL, hin, w);
+    if (lane == w) {                           // advance that stream (prefetch the next head)
+      hd = hsucc;
+      if (hd != NIL) { const Node n1 = node[hd]; ht = fabs(n1.tf); hsucc = n1.next; hin = n1.in; }
     }
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d) {
-      if (d < ND) {
-        edb = add(edb, d_ebusy[d]);
-        edi = add(edi, energy_j(PR.p_idle, sub(horizon, d_bms[d])));
-        bd = add(bd, d_bms[d]);
+    // decode instances catch up to t: events strictly before t (PrefillDone drains first)
+    dec_advance(D, lane, C, S, t, dE);
+    // ---- O8 EcoRoute
+    int dsel, cse;
+    if (!eco) {
+      dsel = (int)cursor;
+      cursor = (cursor + 1u) % (uint32_t)ND;
+      cse = 0;
+    } else {
+      int fnow = 0x7fffffff, faft = 0x7fffffff;
+      if (lane < ND) {
+        const uint32_t n = D.nreq + D.pn, kv = D.nkv + D.pkv;  // A9 effective state
+        double pr;
+        const int kn = n == 0u ? 0 : lowest_itl(S, n, kv, tgt_itl, &pr);  // A10, A11
+        const int ka = lowest_itl(S, n + 1u, kv + in_i + 1u, tgt_itl, &pr);  // A12
+        fnow = S.mhz[kn];
+        faft = S.mhz[ka];
       }
+      const bool act = lane < ND;
+      const bool cr = act && faft > fnow;  // A13
+      const unsigned Rm = __ballot_sync(FULL, cr);
+      const int nc = __popc(Rm);
+      const int mn = (int)__reduce_min_sync(FULL, (unsigned)fnow);
+      unsigned inset;
+      if (nc == 0) {
+        inset = __ballot_sync(FULL, act && fnow == mn);
+        cse = __popc(inset) == 1 ? 1 : 2;
+      } else if (nc < ND) {
+        const int mu = (int)__reduce_min_sync(FULL, (unsigned)(act && !cr ? fnow : 0x7fffffff));
+        const int mr = (int)__reduce_min_sync(FULL, (unsigned)(cr ? faft : 0x7fffffff));
+        const long long g = (long long)mu - (long long)mr;  // A14, A15
+        if (g <= (long long)LY.delta_mhz) { inset = __ballot_sync(FULL, act && !cr && fnow == mu); cse = 3; }
+        else { inset = __ballot_sync(FULL, act && fnow == mn); cse = 4; }
+      } else {
+        const int ma = (int)__reduce_min_sync(FULL, (unsigned)faft);
+        inset = __ballot_sync(FULL, act && faft == ma);
+        cse = 5;
+      }
+      // round robin among the candidate set from the cursor (A17)
+      const unsigned rot = ((inset >> cursor) | (inset << (ND - (int)cursor))) & ((1u << ND) - 1u);
+      dsel = (int)((cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND);
+      if (__popc(inset) >= 2) cursor = (uint32_t)(dsel + 1) % (uint32_t)ND;
     }
-    R.n_ttft_ok = n_ttft_ok; R.n_itl_ok = n_itl_ok; R.n_both_ok = n_both; R.prefill_iters = prefill_iters;
-    R.steps_ctrl = steps_ctrl; R.steps_route = steps_route; R.decision_hash = h;
-    R.sum_ttft_ms = sum_ttft; R.sum_itl_mean_ms = sum_itl;
-    R.e_prefill_busy_j = epb; R.e_prefill_idle_j = epi;
-    R.e_decode_busy_j = edb; R.e_decode_idle_j = edi;
-    R.busy_ms_prefill = bp; R.busy_ms_decode = bd;
-    R.top_level_ms = top_ms; R.horizon_ms = horizon;
+    steps_route++;
+    h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
+    if (lane == dsel) {
+      D.pn += 1u;
+      D.pkv += in_i + 1u;
+      node[i].next = NIL;
+      if (D.qt == NIL) D.qh = i; else node[D.qt].next = i;
+      D.qt = i;
+    }
   }
+  // drain: every decode instance runs to completion
+  dec_advance(D, lane, C, S, INF, dE);
+  __syncwarp();
+
+  // ================================================================ O9: record
+  // first error in (time, prefill before decode, instance) order = the oracle's stop point
+  const int wp = argmin_time(pE.t, lane < NP && pE.t < INF);
+  const int wd = argmin_time(dE.t, lane < ND && dE.t < INF);
+  if (wp >= 0 || wd >= 0) {
+    const double tp = wp >= 0 ? __shfl_sync(FULL, pE.t, wp) : INF;
+    const double td = wd >= 0 ? __shfl_sync(FULL, dE.t, wd) : INF;
+    const uint32_t cp = __shfl_sync(FULL, pE.code, wp >= 0 ? wp : 0);
+    const uint32_t cd = __shfl_sync(FULL, dE.code, wd >= 0 ? wd : 0);
+    R.status = (wp >= 0 && tp <= td) ? cp : cd;
+    // leave the wheels clean for the next scenario of this warp
+    if (lane < ND)
+      for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint2(NIL, NIL);
+    if (lane == 0) P.out[s] = R;
+    return;
+  }
+  double tl = p_tlast > D.tlast ? p_tlast : D.tlast;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(FULL, tl, o);
+    tl = x > tl ? x : tl;
+  }
+  const double horizon = Dur > tl ? Dur : tl;  // A23
+  uint64_t hh = splitmix64(h_r);                // A36: route chain, prefill chains, decode chains
+  double sttft = 0.0, sitl = 0.0, top = 0.0, epb = 0.0, epi = 0.0, edb = 0.0, edi = 0.0, bp = 0.0, bd = 0.0;
+  for (int q = 0; q < NP; ++q) {
+    hh = splitmix64(hh ^ __shfl_sync(FULL, p_h, q));
+    sttft = add(sttft, __shfl_sync(FULL, p_sttft, q));
+    top = add(top, __shfl_sync(FULL, p_top, q));
+    epb = add(epb, __shfl_sync(FULL, p_ebusy, q));
+    const double b = __shfl_sync(FULL, p_bms, q);
+    epi = add(epi, energy_j(PR.p_idle, sub(horizon, b)));
+    bp = add(bp, b);
+  }
+  for (int d = 0; d < ND; ++d) {
+    hh = splitmix64(hh ^ __shfl_sync(FULL, D.h, d));
+    sitl = add(sitl, __shfl_sync(FULL, D.sitl, d));
+    top = add(top, __shfl_sync(FULL, D.top, d));
+    edb = add(edb, __shfl_sync(FULL, D.ebusy, d));
+    const double b = __shfl_sync(FULL, D.bms, d);
+    edi = add(edi, energy_j(PR.p_idle, sub(horizon, b)));
+    bd = add(bd, b);
+  }
+  uint32_t c_ttft = p_ttft_ok, c_itl = p_itl_ok + (lane < ND ? D.n_itl_ok : 0u);
+  uint32_t c_both = p_both + (lane < ND ? D.n_both : 0u), c_pi = lane < NP ? p_iters : 0u;
+  uint32_t c_di = lane < ND ? D.iters : 0u;
+  c_ttft = __reduce_add_sync(FULL, c_ttft);
+  c_itl = __reduce_add_sync(FULL, c_itl);
+  c_both = __reduce_add_sync(FULL, c_both);
+  c_pi = __reduce_add_sync(FULL, c_pi);
+  c_di = __reduce_add_sync(FULL, c_di);
+  R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl; R.n_both_ok = c_both; R.prefill_iters = c_pi;
+  R.steps_ctrl = (uint64_t)c_pi + c_di; R.steps_route = steps_route; R.decision_hash = hh;
+  R.sum_ttft_ms = sttft; R.sum_itl_mean_ms = sitl;
+  R.e_prefill_busy_j = epb; R.e_prefill_idle_j = epi; R.e_decode_busy_j = edb; R.e_decode_idle_j = edi;
+  R.busy_ms_prefill = bp; R.busy_ms_decode = bd; R.top_level_ms = top; R.horizon_ms = horizon;
   if (lane == 0) P.out[s] = R;
 }
 
-template <int MAXP, int MAXD>
 __global__ void __launch_bounds__(SIM_THREADS) simulate_kernel(const __grid_constant__ SimParams P) {
+  extern __shared__ __align__(16) char smem[];
   const int lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= P.n_slots) return;
   char *slot = P.slots + (size_t)warp * P.slot_bytes;
+  uint2 *wheels = P.wheels + (size_t)warp * P.wheel_per_slot;
+  char *wsm = smem + (size_t)wib * P.smem_per_warp;
   for (;;) {
     uint32_t s = 0;
     if (lane == 0) s = atomicAdd(P.counter, 1u);
     s = __shfl_sync(FULL, s, 0);
     if (s >= P.n) break;
-    run_scenario<MAXP, MAXD>(P, s, slot);
+    run_scenario(P, s, slot, wheels, wsm);
     __syncwarp();
   }
 }
 
-template <int MAXP, int MAXD>
-const void *sim_kernel_ptr() { return (const void *)simulate_kernel<MAXP, MAXD>; }
+const void *sim_kernel_ptr() { return (const void *)simulate_kernel; }
 
-template <int MAXP, int MAXD>
-cudaError_t launch_sim(const SimParams &P, int grid, cudaStream_t st) {
-  simulate_kernel<MAXP, MAXD><<<grid, SIM_THREADS, 0, st>>>(P);
+cudaError_t launch_sim(const SimParams &P, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  simulate_kernel<<<grid, SIM_THREADS, smem, st>>>(P);
   return cudaGetLastError();
 }
-
-#define VT_INST(p, d)                                                          \
-  template const void *sim_kernel_ptr<p, d>();                                  \
-  template cudaError_t launch_sim<p, d>(const SimParams &, int, cudaStream_t);
-VT_INST(1, 1)
-VT_INST(2, 2)
-VT_INST(4, 4)
-VT_INST(8, 8)
-#undef VT_INST
 
 }  // namespace vt

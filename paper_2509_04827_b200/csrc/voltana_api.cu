@@ -229,54 +229,67 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, 
 // ------------------------------------------------------------------ K4
 namespace {
 
-struct SimShape { int maxp, maxd; };
-
-SimShape sim_shape(const voltana_layout *lays, int n_layouts) {
-  int mp = 1, md = 1;
-  for (int i = 0; i < n_layouts; ++i) {
-    if (lays[i].n_p > mp) mp = lays[i].n_p;
-    if (lays[i].n_d > md) md = lays[i].n_d;
-  }
-  int m = mp > md ? mp : md;
-  int t = m <= 1 ? 1 : m <= 2 ? 2 : m <= 4 ? 4 : 8;
-  return {t, t};
+int max_nd(const voltana_layout *lays, int n_layouts) {
+  int md = 1;
+  for (int i = 0; i < n_layouts; ++i) md = lays[i].n_d > md ? lays[i].n_d : md;
+  return md;
 }
 
-const void *sim_ptr(int t) {
-  switch (t) {
-    case 1: return sim_kernel_ptr<1, 1>();
-    case 2: return sim_kernel_ptr<2, 2>();
-    case 4: return sim_kernel_ptr<4, 4>();
-    default: return sim_kernel_ptr<8, 8>();
-  }
+uint32_t wheel_buckets(uint32_t max_out) {
+  uint32_t nb = 2;
+  while (nb < max_out) nb <<= 1;
+  return nb;
 }
 
-int resident_warps(int t) {
+struct SimLayout {
+  size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem;
+  uint32_t n_slots, nb, itl_smem;
+};
+
+int resident_warps(size_t smem_per_block) {
   static std::mutex mu;
-  static int cache[9] = {0};
+  static size_t cached_smem = (size_t)-1;
+  static int cached = 0;
   std::lock_guard<std::mutex> g(mu);
-  if (!cache[t]) {
+  if (smem_per_block != cached_smem) {
     int nb = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_ptr(t), SIM_THREADS, 0) != cudaSuccess || nb < 1)
+    cudaFuncSetAttribute(sim_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_per_block);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(), SIM_THREADS, smem_per_block) !=
+            cudaSuccess || nb < 1) {
+      cudaGetLastError();
       nb = 1;
-    cache[t] = nb * sm_count() * (SIM_THREADS / 32);
+    }
+    cached = nb * sm_count() * (SIM_THREADS / 32);
+    cached_smem = smem_per_block;
   }
-  return cache[t];
+  return cached;
 }
 
-struct SimLayout { size_t node, xd, wheel, slot, slots, total; uint32_t n_slots; };
-
-SimLayout sim_layout(uint64_t max_requests, int maxd, size_t n) {
+SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n_layouts, int kmax, int tmax,
+                     size_t n) {
   SimLayout L;
-  L.node = align256((size_t)max_requests * 16);
-  L.xd = align256((size_t)max_requests);
-  L.wheel = (size_t)maxd * WHEEL_BUCKETS * 8;
-  L.slot = align256(L.node + L.xd + L.wheel);
-  size_t rw = (size_t)resident_warps(maxd);
+  L.nb = wheel_buckets(tr->max_out);
+  size_t itl_bytes = (size_t)kmax * tmax * 24;
+  L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
+  L.smem_per_warp = (SIM_SMEM_FIXED + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
+  L.smem = L.smem_per_warp * (SIM_THREADS / 32);
+  L.node = align256((size_t)tr->max_requests * 16);
+  L.slot = L.node > 256 ? L.node : 256;
+  L.wheel_per_slot = (size_t)max_nd(lays, n_layouts) * L.nb;
+  size_t rw = (size_t)resident_warps(L.smem);
   L.n_slots = (uint32_t)(n < rw ? (n < 1 ? 1 : n) : rw);
-  L.slots = 256;
-  L.total = L.slots + (size_t)L.n_slots * L.slot;
+  L.slots_off = 256;
+  L.wheels_off = align256(L.slots_off + (size_t)L.n_slots * L.slot);
+  L.total = L.wheels_off + (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint2);
   return L;
+}
+
+void table_extent(const voltana_grid *grids, int n_grids, const voltana_profile *profs, int n_profiles, int *kmax,
+                  int *tmax) {
+  *kmax = 1;
+  *tmax = 1;
+  for (int i = 0; i < n_grids; ++i) *kmax = grids[i].k > *kmax ? grids[i].k : *kmax;
+  for (int i = 0; i < n_profiles; ++i) *tmax = profs[i].n_tiles > *tmax ? profs[i].n_tiles : *tmax;
 }
 
 }  // namespace
@@ -284,8 +297,8 @@ SimLayout sim_layout(uint64_t max_requests, int maxd, size_t n) {
 size_t voltana_simulate_workspace_bytes(const voltana_traces *traces_h, const voltana_layout *layouts_h,
                                         int n_layouts, size_t n_scenarios) {
   if (!traces_h || !layouts_h || n_layouts < 1) return 0;
-  SimShape sh = sim_shape(layouts_h, n_layouts);
-  return sim_layout(traces_h->max_requests, sh.maxd, n_scenarios).total;
+  // conservative table extent (ITL table staged in shared memory or not does not change the size)
+  return sim_layout(traces_h, layouts_h, n_layouts, VOLTANA_MAX_LEVELS, 64, n_scenarios).total;
 }
 
 voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_slo *slos_h, int n_slos,
@@ -303,8 +316,10 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   if (n_profiles < 1 || n_profiles > MAX_PROFILES)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: n_profiles=%d (1..8)", n_profiles);
   if (n > 0xffffffffull) return fail(VOLTANA_E_INVALID_ARG, "simulate: n=%zu too large", n);
-  if (traces_h->max_requests > 0x7fffffffull)
+  if (traces_h->max_requests > 0x7ffffffeull)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_requests too large");
+  if (traces_h->max_out < 1 || traces_h->max_out > 65535)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_out=%u outside 1..65535", traces_h->max_out);
   voltana_status s;
   for (int i = 0; i < n_slos; ++i) {
     const voltana_slo &x = slos_h[i];
@@ -328,12 +343,12 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
     snprintf(what, sizeof(what), "simulate: profiles[%d]", i);
     if ((s = check_profile(&profiles_h[i], what)) != VOLTANA_OK) return s;
   }
+  int kmin = profiles_h[0].k;
+  for (int j = 1; j < n_profiles; ++j) kmin = profiles_h[j].k < kmin ? profiles_h[j].k : kmin;
   for (int i = 0; i < n_grids; ++i) {
     char what[64];
     snprintf(what, sizeof(what), "simulate: grids[%d]", i);
-    // each grid must be valid on every profile it may be paired with: check against the smallest
-    int kmin = profiles_h[0].k;
-    for (int j = 1; j < n_profiles; ++j) kmin = profiles_h[j].k < kmin ? profiles_h[j].k : kmin;
+    // every grid must be valid on every profile it may be paired with
     if ((s = check_ladder(grids_h[i].level, grids_h[i].k, kmin, what)) != VOLTANA_OK) return s;
   }
   if (n == 0) return ok();
@@ -341,10 +356,12 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
       !traces_h->duration_ms || !scen_h->trace_id || !scen_h->slo_id || !scen_h->layout_id || !scen_h->grid_id ||
       !scen_h->profile_id || !scen_h->hash_seed)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: null device array");
-  SimShape sh = sim_shape(layouts_h, n_layouts);
-  SimLayout L = sim_layout(traces_h->max_requests, sh.maxd, n);
-  if (!workspace || ws_bytes < L.total)
-    return fail(VOLTANA_E_WORKSPACE, "simulate: workspace %zu < %zu bytes", ws_bytes, L.total);
+  int kmax, tmax;
+  table_extent(grids_h, n_grids, profiles_h, n_profiles, &kmax, &tmax);
+  SimLayout L = sim_layout(traces_h, layouts_h, n_layouts, kmax, tmax, n);
+  const size_t need = voltana_simulate_workspace_bytes(traces_h, layouts_h, n_layouts, n);
+  if (!workspace || ws_bytes < need || ws_bytes < L.total)
+    return fail(VOLTANA_E_WORKSPACE, "simulate: workspace %zu < %zu bytes", ws_bytes, need);
 
   static_assert(sizeof(SimParams) < 32000, "kernel parameter block too large");
   SimParams *P = new SimParams;
@@ -353,29 +370,31 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   P->offset = traces_h->offset; P->duration = traces_h->duration_ms;
   P->trace_id = scen_h->trace_id; P->slo_id = scen_h->slo_id; P->layout_id = scen_h->layout_id;
   P->grid_id = scen_h->grid_id; P->profile_id = scen_h->profile_id; P->hash_seed = scen_h->hash_seed;
-  P->n = (uint32_t)n; P->nb = WHEEL_BUCKETS; P->out = out;
+  P->n = (uint32_t)n; P->nb = L.nb; P->max_out = traces_h->max_out; P->out = out;
+  P->n_slots = L.n_slots;
+  P->n_slos = (uint32_t)n_slos; P->n_layouts = (uint32_t)n_layouts; P->n_grids = (uint32_t)n_grids;
+  P->n_profiles = (uint32_t)n_profiles; P->n_traces = traces_h->n_traces;
+  P->max_requests = traces_h->max_requests;
   char *ws = (char *)workspace;
   P->counter = (uint32_t *)ws;
-  P->slots = ws + L.slots;
-  P->slot_bytes = L.slot; P->node_bytes = L.node; P->xd_bytes = L.xd;
-  P->max_requests = traces_h->max_requests;
+  P->slots = ws + L.slots_off;
+  P->slot_bytes = L.slot;
+  P->wheels = (uint2 *)(ws + L.wheels_off);
+  P->wheel_per_slot = L.wheel_per_slot;
+  P->itl_smem = L.itl_smem;
+  P->smem_per_warp = (uint32_t)L.smem_per_warp;
   for (int i = 0; i < n_slos; ++i) P->slo[i] = slos_h[i];
   for (int i = 0; i < n_layouts; ++i) P->lay[i] = layouts_h[i];
   for (int i = 0; i < n_grids; ++i) P->grid[i] = grids_h[i];
   for (int i = 0; i < n_profiles; ++i) P->prof[i] = to_dev(profiles_h[i]);
-  P->n_slots = L.n_slots;
-  P->n_slos = (uint32_t)n_slos; P->n_layouts = (uint32_t)n_layouts; P->n_grids = (uint32_t)n_grids;
-  P->n_profiles = (uint32_t)n_profiles; P->n_traces = traces_h->n_traces;
   cudaStream_t st = (cudaStream_t)stream;
+  // scenario counter = 0; every wheel bucket = {NIL, NIL} (buckets are left clean after use)
   cudaError_t e = cudaMemsetAsync(P->counter, 0, sizeof(uint32_t), st);
+  if (e == cudaSuccess)
+    e = cudaMemsetAsync(P->wheels, 0xFF, (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint2), st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
   const int grid = (int)((L.n_slots + (SIM_THREADS / 32) - 1) / (SIM_THREADS / 32));
-  switch (sh.maxd) {
-    case 1: e = launch_sim<1, 1>(*P, grid, st); break;
-    case 2: e = launch_sim<2, 2>(*P, grid, st); break;
-    case 4: e = launch_sim<4, 4>(*P, grid, st); break;
-    default: e = launch_sim<8, 8>(*P, grid, st); break;
-  }
+  e = launch_sim(*P, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
   g_launches = 1;

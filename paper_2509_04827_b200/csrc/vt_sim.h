@@ -11,7 +11,8 @@ namespace vt {
 
 constexpr int SIM_THREADS = 128;      // 4 warps per CTA, one scenario per warp
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
-constexpr uint32_t WHEEL_BUCKETS = 1024;  // per decode instance (power of two)
+constexpr size_t SIM_SMEM_FIXED = 128 + 16 * VOLTANA_MAX_LEVELS * 2 + 4 * VOLTANA_MAX_LEVELS;  // per warp
+constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size
 
 struct SimParams {
   // traces (device)
@@ -23,16 +24,21 @@ struct SimParams {
   const uint32_t *trace_id, *slo_id, *layout_id, *grid_id, *profile_id;
   const uint64_t *hash_seed;
   uint32_t n;
-  uint32_t nb;                 // wheel buckets per decode instance
+  uint32_t nb;                 // wheel buckets per decode instance (power of two >= max_out)
+  uint32_t max_out;
   uint32_t n_slots;            // workspace slots = warps that may run scenarios
   uint32_t n_slos, n_layouts, n_grids, n_profiles;
   uint64_t n_traces;
+  uint64_t max_requests;
   voltana_result *out;
   // workspace
   uint32_t *counter;
-  char *slots;
-  size_t slot_bytes, node_bytes, xd_bytes;
-  uint64_t max_requests;
+  char *slots;                 // [n_slots][slot_bytes]: request nodes
+  size_t slot_bytes;
+  uint2 *wheels;               // [n_slots][wheel_per_slot]: decode timing wheels
+  size_t wheel_per_slot;       // max N_D * nb buckets
+  uint32_t itl_smem;           // stage the ladder's ITL table in shared memory
+  uint32_t smem_per_warp;
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];
@@ -40,7 +46,7 @@ struct SimParams {
   DevProfile prof[MAX_PROFILES];
 };
 
-template <int MAXP, int MAXD> const void *sim_kernel_ptr();
-template <int MAXP, int MAXD> cudaError_t launch_sim(const SimParams &P, int grid, cudaStream_t st);
+const void *sim_kernel_ptr();
+cudaError_t launch_sim(const SimParams &P, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace vt

@@ -71,7 +71,7 @@ def test_host_validation_errors(vt):
 def test_simulate_validation_errors(vt):
     L = vt.lib()
     lib = vt._lib
-    tr = lib.Traces(1, 1, 1, 1, 1, 1, 10)
+    tr = lib.Traces(1, 1, 1, 1, 1, 1, 10, 100, 0)
     slos = (lib.Slo * 1)(lib.Slo(600.0, 60.0, 1.0))
     lays = (lib.Layout * 1)(lib.Layout(2, 9, 0, 150, 8192, 400000, 0.0))
     g = lib.Grid(2)

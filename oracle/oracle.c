@@ -187,7 +187,7 @@ typedef struct {
   run_entry *run; uint64_t n_run, cap_run;   /* admission-ordered running set */
   uint32_t *admq; uint64_t q_head, q_tail;   /* FIFO admission queue (capacity n) */
   uint64_t nreq, nkv, pend_n, pend_kv;
-  int busy; double end, ebusy, bms; uint64_t iters;
+  int busy; double end, ebusy /* W*ms */, bms; uint64_t iters;
   uint64_t h;       /* decision-hash chain of this instance's controller decisions [A36] */
   double sum_itl;   /* ITL-mean sum of this instance's completions, completion order [A37] */
   double top;       /* ms at the top level [A37] */
@@ -196,7 +196,7 @@ typedef struct {
 typedef struct {
   uint64_t qhead;          /* first id (== p mod N_P) not yet batched [A7] */
   uint64_t bstart, bcnt;   /* ids of the batch in flight: bstart + j*N_P */
-  int busy; double end, ebusy, bms; uint64_t iters;
+  int busy; double end, ebusy /* W*ms */, bms; uint64_t iters;
   uint64_t h;       /* decision-hash chain of this instance's controller decisions [A36] */
   double sum_ttft;  /* TTFT sum of this instance's completions, completion order [A37] */
   double top;       /* ms at the top level [A37] */
@@ -410,7 +410,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       I->bstart = I->qhead;
       I->bcnt = cnt;
       I->qhead = id;
-      I->ebusy += interval_energy(busy_power(p, 0, L[k], nbt), dur);
+      I->ebusy += busy_power(p, 0, L[k], nbt) * dur; /* W*ms; converted to J once [A23] */
       I->bms += dur;
       I->iters++;
       if (k == K - 1) I->top += dur;
@@ -465,7 +465,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       }
       I->end = t + dur;
       I->busy = 1;
-      I->ebusy += interval_energy(busy_power(p, 1, L[k], I->nreq), dur);
+      I->ebusy += busy_power(p, 1, L[k], I->nreq) * dur; /* W*ms [A23] */
       I->bms += dur;
       I->iters++;
       if (k == K - 1) I->top += dur;
@@ -486,12 +486,12 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
     for (int q = 0; q < NP; ++q) { sum_ttft += P[q].sum_ttft; top_ms += P[q].top; }
     for (int d = 0; d < ND; ++d) { sum_itl += D[d].sum_itl; top_ms += D[d].top; }
     for (int q = 0; q < NP; ++q) {
-      epb += P[q].ebusy;
+      epb += P[q].ebusy / 1000.0; /* J = (sum of P*dur in W*ms) / 1000 per instance [A23] */
       epi += interval_energy(p->p_idle, horizon - P[q].bms);
       bp += P[q].bms;
     }
     for (int d = 0; d < ND; ++d) {
-      edb += D[d].ebusy;
+      edb += D[d].ebusy / 1000.0;
       edi += interval_energy(p->p_idle, horizon - D[d].bms);
       bd += D[d].bms;
     }

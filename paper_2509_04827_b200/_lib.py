@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libvoltana.so")
+SO_PATH = os.environ.get("VOLTANA_SO") or os.path.join(HERE, "libvoltana.so")  # variant override (experiments)
 
 VOLTANA_DELTA_INF = 2147483647
 MAX_LEVELS = 64

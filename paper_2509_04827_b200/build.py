@@ -7,6 +7,7 @@ from __future__ import annotations
 
 import concurrent.futures as cf
 import os
+import re
 import subprocess
 import sys
 
@@ -34,37 +35,44 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src):
-    obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+def _compile(src, defines=(), tag=""):
+    obj = os.path.join(BUILD, src.replace(".cu", f"{tag}.o"))
     deps = [os.path.join(CSRC, src)] + _deps()
     if not _stale(obj, deps):
         return obj, ""
-    cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, defines=(), so: str | None = None) -> str:
+    """Compile every source and link libvoltana.so (or `so`, an experiment variant built
+    with extra -D `defines`)."""
     os.makedirs(BUILD, exist_ok=True)
     if force:
         for f in os.listdir(BUILD):
             os.remove(os.path.join(BUILD, f))
+    tag = "" if not defines else "_" + "_".join(re.sub(r"\W", "", d) for d in defines)
+    target = SO if so is None else so
     with cf.ThreadPoolExecutor(len(SOURCES)) as ex:
-        res = list(ex.map(_compile, SOURCES))
+        res = list(ex.map(lambda s: _compile(s, defines, tag), SOURCES))
     objs = [o for o, _ in res]
     if verbose:
         for _, log in res:
             if log:
                 print(log, file=sys.stderr)
-    if force or _stale(SO, objs):
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", SO, *objs, "-cudart", "static"]
+    if force or _stale(target, objs):
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", target, *objs, "-cudart",
+               "static"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return SO
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("--so=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, so=out[0] if out else None))

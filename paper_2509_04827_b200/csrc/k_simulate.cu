@@ -38,7 +38,7 @@ struct Node {       // 16 B per request (workspace)
 
 // ------------------------------------------------------------------ per-warp tables (smem)
 struct Tables {
-  int K, T, W, kp;
+  int K, T, W, kp, wshift;  // wshift >= 0: W is a power of two (tile index by shift)
   bool itl_smem, mono_tt, mono_it;
   const uint16_t *lad;     // [K] profile levels
   const double *tt;        // [K][2] a1, c1
@@ -49,7 +49,7 @@ struct Tables {
 };
 
 __device__ __forceinline__ uint32_t tile_j(const Tables &S, uint32_t n) {
-  uint32_t j = (n - 1u) / (uint32_t)S.W;
+  uint32_t j = S.wshift >= 0 ? (n - 1u) >> S.wshift : (n - 1u) / (uint32_t)S.W;
   return j < (uint32_t)(S.T - 1) ? j : (uint32_t)(S.T - 1);
 }
 
@@ -202,7 +202,7 @@ __device__ void dec_advance(Dec &D, int d, const Ctx &C, const Tables &S, double
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
     D.end = add(tnow, dur);
     D.busy = true;
-    D.ebusy = add(D.ebusy, energy_j(busy_power(C.p_idle, C.tdp, C.uh_d, S.dyn[S.K + k], D.nreq), dur));
+    D.ebusy = add(D.ebusy, mul(busy_power(C.p_idle, C.tdp, C.uh_d, S.dyn[S.K + k], D.nreq), dur));  // W*ms (A23)
     D.bms = add(D.bms, dur);
     if (k == S.K - 1) D.top = add(D.top, dur);
     D.cur = D.iters;
@@ -273,6 +273,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
   // ---------------------------------------------------------------- stage the ladder's tables
   Tables S;
   S.K = GR.k; S.T = PR.n_tiles; S.W = PR.tile_w; S.kp = PR.k;
+  S.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
   S.itl_smem = P.itl_smem != 0;
   {
     char *p = wsm;
@@ -332,11 +333,22 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
       // FCFS prefix of the arrived queue with sum(in) <= B, at least one request (A6)
       uint32_t nbt = inl[nxt], cnt = 1, id = nxt + NPu;
       bool backlog = false;
-      while (id < N) {
-        if (!(arr[id] <= ts)) break;
-        const uint32_t x = inl[id];
-        if (nbt + x > LY.max_batch_tokens) { backlog = true; break; }
-        nbt += x; cnt++; id += NPu;
+      for (bool stop = false; !stop;) {  // 4 candidates per round, loads issued together
+        double av[4];
+        uint32_t xv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t j = id + (uint32_t)u * NPu;
+          av[u] = j < N ? arr[j] : INF;     // past the trace end: "not arrived"
+          xv[u] = j < N ? inl[j] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (stop) continue;
+          if (!(av[u] <= ts)) stop = true;                                             // not arrived yet
+          else if (nbt + xv[u] > LY.max_batch_tokens) { backlog = true; stop = true; }  // does not fit
+          else { nbt += xv[u]; cnt++; id += NPu; }
+        }
       }
       // (A5) backlog: requests still queued after the batch
       double budget = sub(tgt_ttft, sub(ts, a0));  // A4: SLO minus the oldest request's wait
@@ -349,7 +361,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
       p_iters++;
       if (!(dur > 0.0)) { pE.t = ts; pE.code = VOLTANA_ITEM_E_CONTRACT; break; }
       const double end = add(ts, dur);
-      p_ebusy = add(p_ebusy, energy_j(busy_power(PR.p_idle, PR.tdp, PR.uh[0], S.dyn[k], nbt), dur));
+      p_ebusy = add(p_ebusy, mul(busy_power(PR.p_idle, PR.tdp, PR.uh[0], S.dyn[k], nbt), dur));  // W*ms (A23)
       p_bms = add(p_bms, dur);
       if (k == S.K - 1) p_top = add(p_top, dur);
       // ---- O5 PrefillDone at `end`, batch in FCFS order
@@ -396,22 +408,29 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
   Err dE = {INF, 0};
 
   // stream head of prefill lane p: next routed request in its completion order
+  // (head node hn and, loaded one step ahead, its successor nn)
   uint32_t hd = lane < NP ? p_head : NIL;
-  double ht = 0.0;
-  uint32_t hsucc = NIL, hin = 0;
-  if (hd != NIL) { const Node n0 = node[hd]; ht = fabs(n0.tf); hsucc = n0.next; hin = n0.in; }
+  Node hn, nn;
+  hn.tf = 0.0; hn.next = NIL; hn.in = 0; hn.out = 0;
+  nn = hn;
+  if (hd != NIL) {
+    hn = node[hd];
+    if (hn.next != NIL) nn = node[hn.next];
+  }
   uint64_t h_r = P.hash_seed[s];
   uint32_t cursor = 0, steps_route = 0;
   const bool eco = LY.policy == 0 && ND > 1;
   for (;;) {
+    const double ht = fabs(hn.tf);
     const int w = argmin_time(ht, hd != NIL);  // next PrefillDone request in (t, p, id) order
     if (w < 0) break;
     const double t = __shfl_sync(FULL, ht, w);
     const uint32_t i = __shfl_sync(FULL, hd, w);
-    const uint32_t in_i = __shfl_sync(FULL, hin, w);
-    if (lane == w) {                           // advance that stream (prefetch the next head)
-      hd = hsucc;
-      if (hd != NIL) { const Node n1 = node[hd]; ht = fabs(n1.tf); hsucc = n1.next; hin = n1.in; }
+    const uint32_t in_i = __shfl_sync(FULL, (uint32_t)hn.in, w);
+    if (lane == w) {                           // advance that stream; prefetch one further
+      hd = hn.next;
+      hn = nn;
+      if (hd != NIL && hn.next != NIL) nn = node[hn.next];
     }
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     dec_advance(D, lane, C, S, t, dE);
@@ -498,7 +517,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
     hh = splitmix64(hh ^ __shfl_sync(FULL, p_h, q));
     sttft = add(sttft, __shfl_sync(FULL, p_sttft, q));
     top = add(top, __shfl_sync(FULL, p_top, q));
-    epb = add(epb, __shfl_sync(FULL, p_ebusy, q));
+    epb = add(epb, div(__shfl_sync(FULL, p_ebusy, q), 1000.0));
     const double b = __shfl_sync(FULL, p_bms, q);
     epi = add(epi, energy_j(PR.p_idle, sub(horizon, b)));
     bp = add(bp, b);
@@ -507,7 +526,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
     hh = splitmix64(hh ^ __shfl_sync(FULL, D.h, d));
     sitl = add(sitl, __shfl_sync(FULL, D.sitl, d));
     top = add(top, __shfl_sync(FULL, D.top, d));
-    edb = add(edb, __shfl_sync(FULL, D.ebusy, d));
+    edb = add(edb, div(__shfl_sync(FULL, D.ebusy, d), 1000.0));
     const double b = __shfl_sync(FULL, D.bms, d);
     edi = add(edi, energy_j(PR.p_idle, sub(horizon, b)));
     bd = add(bd, b);
@@ -528,7 +547,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
   if (lane == 0) P.out[s] = R;
 }
 
-__global__ void __launch_bounds__(SIM_THREADS) simulate_kernel(const __grid_constant__ SimParams P) {
+__global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(const __grid_constant__ SimParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;

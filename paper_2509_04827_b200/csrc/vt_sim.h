@@ -10,6 +10,10 @@
 namespace vt {
 
 constexpr int SIM_THREADS = 128;      // 4 warps per CTA, one scenario per warp
+#ifndef VT_SIM_MIN_BLOCKS
+#define VT_SIM_MIN_BLOCKS 4
+#endif
+constexpr int SIM_MIN_BLOCKS = VT_SIM_MIN_BLOCKS;  // 4: <= 128 registers, 16 warps per SM
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
 constexpr size_t SIM_SMEM_FIXED = 128 + 16 * VOLTANA_MAX_LEVELS * 2 + 4 * VOLTANA_MAX_LEVELS;  // per warp
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size

@@ -45,6 +45,7 @@ typedef enum {
 #define VOLTANA_ITEM_E_KV 1u       /* a request can never fit an empty decode instance [A20] */
 #define VOLTANA_ITEM_E_CONTRACT 2u /* non-positive predicted duration, n_kv < n_req, ...   */
 #define VOLTANA_ITEM_E_INPUT 3u    /* trace invalid (unsorted, lengths outside [1,65535]...) */
+#define VOLTANA_ITEM_E_INTERNAL 4u /* watchdog: a scenario exceeded its step bound (library bug) */
 
 #define VOLTANA_MAX_LEVELS 64      /* K <= 64 levels per ladder                            */
 #define VOLTANA_MAX_INSTANCES 8    /* N_P, N_D <= 8                                        */
@@ -200,6 +201,11 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
 /* Kernel-launch statistics of the last voltana_simulate on this thread (for the bench):
  * number of kernels launched. */
 int voltana_last_launch_count(void);
+
+/* Debug/profiling hook (this thread's next voltana_simulate calls): when buf != NULL,
+ * buf[2i] (device u64, [2n]) receives the %globaltimer ns at which scenario i started and
+ * buf[2i+1] its duration in ns with the SM id in bits 56..63. NULL turns it off. */
+void voltana_debug_set_timing(uint64_t *buf);
 
 const char *voltana_status_string(voltana_status s);
 const char *voltana_last_error_detail(void); /* thread-local, names the argument        */

@@ -96,9 +96,11 @@ static uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
-/* h <- splitmix64(h ^ (kind<<48 ^ instance<<32 ^ level<<16 ^ case)) [A36] */
+/* h <- (h ^ (kind<<48 ^ instance<<32 ^ level<<16 ^ case)) * phi64 [A36]: for a fixed
+ * decision word the step is a bijection of h, so two decision sequences that differ in
+ * one decision keep differing; the chains are mixed with splitmix64 at the end. */
 static uint64_t fold(uint64_t h, uint64_t kind, uint64_t inst, uint64_t level, uint64_t cse) {
-  return splitmix64(h ^ ((kind << 48) ^ (inst << 32) ^ (level << 16) ^ cse));
+  return (h ^ ((kind << 48) ^ (inst << 32) ^ (level << 16) ^ cse)) * 0x9E3779B97F4A7C15ull;
 }
 
 /* ---------------------------------------------------------------- EcoRoute */

@@ -74,7 +74,7 @@ assert RESULT_DTYPE.itemsize == 128
 
 EXPORTS = ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_fit_workspace_bytes",
            "voltana_simulate", "voltana_simulate_workspace_bytes", "voltana_status_string",
-           "voltana_last_error_detail", "voltana_last_launch_count")
+           "voltana_last_error_detail", "voltana_last_launch_count", "voltana_debug_set_timing")
 
 _lib = None
 
@@ -104,6 +104,8 @@ def lib():
     L.voltana_status_string.restype = C.c_char_p
     L.voltana_last_error_detail.restype = C.c_char_p
     L.voltana_last_launch_count.restype = C.c_int
+    L.voltana_debug_set_timing.argtypes = [vp]
+    L.voltana_debug_set_timing.restype = None
     for name in ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_simulate"):
         getattr(L, name).restype = C.c_int
     _lib = L

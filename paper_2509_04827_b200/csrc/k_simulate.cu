@@ -19,14 +19,27 @@
 // Decisions therefore match the sequential oracle bit for bit; the record's report-only
 // accumulators are per instance (A36/A37), so they match bit for bit too.
 //
-// Decode running sets: a per-instance timing wheel of NB >= max(out) buckets keyed by the
-// iteration index at which a request finishes (admission iteration + out - 2). All running
-// requests advance together (+1 token per iteration), so completions are O(1) per
-// request; buckets are lists appended in admission order (oracle order, A37).
+// Decode running sets: a per-instance timing wheel of NB (<= 1024, L2-resident) buckets keyed
+// by the iteration at which a request finishes (admission iteration + out - 2). All running
+// requests advance together (+1 token per iteration), so a bucket's request count and
+// KV total retire the whole iteration's completions in O(1); the rare request finishing NB or
+// more iterations ahead waits on a sorted far list until its bucket enters the window. Bucket
+// lists keep admission order; the per-request ITL accounting (A30) walks them later, in
+// completion order, off the decision chain.
+//
+// Register budget: per-lane instance state lives in registers; everything cold (scenario
+// constants, staged tables, phase-A results) lives in a per-warp shared-memory block.
 #include <cstdint>
 
 #include "vt_device.cuh"
 #include "vt_sim.h"
+
+#ifndef VT_QCACHE
+#define VT_QCACHE 1    // keep the admission-queue head node in registers
+#endif
+#ifndef VT_BHPF
+#define VT_BHPF 0      // prefetch the bucket the queue head will join at the next START
+#endif
 
 namespace vt {
 
@@ -36,178 +49,317 @@ struct Node {       // 16 B per request (workspace)
   uint16_t in, out;
 };
 
-// ------------------------------------------------------------------ per-warp tables (smem)
-struct Tables {
-  int K, T, W, kp, wshift;  // wshift >= 0: W is a power of two (tile index by shift)
-  bool itl_smem, mono_tt, mono_it;
-  const uint16_t *lad;     // [K] profile levels
-  const double *tt;        // [K][2] a1, c1
-  const double *dyn;       // [2][K] prefill, decode
-  const int *mhz;          // [K]
-  const double *it;        // [T][K][3] (itl_smem)
-  const double *a2g, *b2g, *c2g;
+constexpr int ITL_FIFO = 8;  // deferred completion lists per decode lane
+constexpr int NI = VOLTANA_MAX_INSTANCES;
+
+// Per-warp shared-memory block (one scenario at a time). Sized by SIM_SMEM_FIXED.
+struct WarpSmem {
+  // ---- deferred ITL accounting: completion-list heads and times, per decode lane
+  uint32_t fid[NI][ITL_FIFO];
+  double ft[NI][ITL_FIFO];
+  // ---- phase-A results per prefill lane (read back for the record)
+  double pa_ebusy[NI], pa_bms[NI], pa_top[NI], pa_sttft[NI], pa_tlast[NI], pa_errt[NI];
+  uint64_t pa_h[NI];
+  uint32_t pa_iters[NI], pa_ttft_ok[NI], pa_itl_ok[NI], pa_both[NI], pa_errc[NI];
+  // ---- scenario constants
+  double tau, slo_itl, tgt_itl, slo_ttft, tgt_ttft, p_idle, tdp, uh_p, uh_d;
+  const double *a2g, *b2g, *c2g;   // profile ITL tables (when not staged)
+  uint32_t kvcap, max_steps, B, K, T, W, kp, nb;
+  int32_t wshift;
+  uint32_t itl_smem, mono_tt, mono_it;
+  // ---- staged ladder tables
+  uint16_t lad[VOLTANA_MAX_LEVELS];
+  int32_t mhz[VOLTANA_MAX_LEVELS];
+  double tt[2 * VOLTANA_MAX_LEVELS];   // [K][2]: a1, c1
+  double dyn[2 * VOLTANA_MAX_LEVELS];  // [2][K]: prefill, decode
+  double it[1];                        // [T][K][3]: a2, b2, c2 (flexible; itl_smem)
 };
 
-__device__ __forceinline__ uint32_t tile_j(const Tables &S, uint32_t n) {
-  uint32_t j = S.wshift >= 0 ? (n - 1u) >> S.wshift : (n - 1u) / (uint32_t)S.W;
-  return j < (uint32_t)(S.T - 1) ? j : (uint32_t)(S.T - 1);
+// ------------------------------------------------------------------ EcoPred on staged tables
+__device__ __forceinline__ uint32_t tile_j(const WarpSmem &W, uint32_t n) {
+  const uint32_t j = W.wshift >= 0 ? (n - 1u) >> W.wshift : (n - 1u) / W.W;
+  return j < W.T - 1u ? j : W.T - 1u;
 }
 
-__device__ __forceinline__ double itl_at(const Tables &S, uint32_t j, int k, uint32_t n, uint32_t kv) {
-  if (S.itl_smem) {
-    const double *r = S.it + 3 * ((size_t)j * S.K + k);
+__device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, uint32_t n, uint32_t kv) {
+  if (W.itl_smem) {
+    const double *r = W.it + 3 * ((size_t)j * W.K + k);
     return itl_pred(r[0], r[1], r[2], n, kv);
   }
-  const size_t o = (size_t)j * S.kp + S.lad[k];
-  return itl_pred(__ldg(S.a2g + o), __ldg(S.b2g + o), __ldg(S.c2g + o), n, kv);
+  const size_t o = (size_t)j * W.kp + W.lad[k];
+  return itl_pred(__ldg(W.a2g + o), __ldg(W.b2g + o), __ldg(W.c2g + o), n, kv);
 }
 
-__device__ __forceinline__ double ttft_at(const Tables &S, int k, uint32_t nbt) {
-  return ttft_pred(S.tt[2 * k], S.tt[2 * k + 1], nbt);
+__device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt) {
+  return ttft_pred(W.tt[2 * k], W.tt[2 * k + 1], nbt);
 }
 
 // Lowest ladder index whose prediction meets `target` (A1), else K-1 (A2);
-// *pred = the prediction at the returned index. Ascending scan with early exit, or an
-// exact binary search when the tables are coefficient-monotone in f (A32).
-__device__ int lowest_itl(const Tables &S, uint32_t n, uint32_t kv, double target, double *pred) {
-  const uint32_t j = tile_j(S, n);
-  if (S.mono_it && S.K > 8) {
-    int lo = 0, hi = S.K;
+// *pred = the prediction there. Ascending scan with early exit, or an exact binary search
+// when the tables are coefficient-monotone in f (A32).
+__device__ int lowest_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
+  const uint32_t j = tile_j(W, n);
+  const int K = (int)W.K;
+  if (W.mono_it && K > 8) {
+    int lo = 0, hi = K;
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (itl_at(S, j, mid, n, kv) <= target) hi = mid; else lo = mid + 1;
+      const int mid = (lo + hi) >> 1;
+      if (itl_at(W, j, mid, n, kv) <= target) hi = mid; else lo = mid + 1;
     }
-    int k = lo < S.K ? lo : S.K - 1;
-    *pred = itl_at(S, j, k, n, kv);
+    const int k = lo < K ? lo : K - 1;
+    *pred = itl_at(W, j, k, n, kv);
     return k;
   }
-  for (int k = 0; k < S.K - 1; ++k) {
-    double p = itl_at(S, j, k, n, kv);
+  for (int k = 0; k < K - 1; ++k) {
+    const double p = itl_at(W, j, k, n, kv);
     if (p <= target) { *pred = p; return k; }
   }
-  *pred = itl_at(S, j, S.K - 1, n, kv);
-  return S.K - 1;
+  *pred = itl_at(W, j, K - 1, n, kv);
+  return K - 1;
 }
 
-__device__ int lowest_ttft(const Tables &S, uint32_t nbt, double budget, double *pred) {
-  if (S.mono_tt && S.K > 8) {
-    int lo = 0, hi = S.K;
+__device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, double *pred) {
+  const int K = (int)W.K;
+  if (W.mono_tt && K > 8) {
+    int lo = 0, hi = K;
     while (lo < hi) {
-      int mid = (lo + hi) >> 1;
-      if (ttft_at(S, mid, nbt) <= budget) hi = mid; else lo = mid + 1;
+      const int mid = (lo + hi) >> 1;
+      if (ttft_at(W, mid, nbt) <= budget) hi = mid; else lo = mid + 1;
     }
-    int k = lo < S.K ? lo : S.K - 1;
-    *pred = ttft_at(S, k, nbt);
+    const int k = lo < K ? lo : K - 1;
+    *pred = ttft_at(W, k, nbt);
     return k;
   }
-  for (int k = 0; k < S.K - 1; ++k) {
-    double p = ttft_at(S, k, nbt);
+  for (int k = 0; k < K - 1; ++k) {
+    const double p = ttft_at(W, k, nbt);
     if (p <= budget) { *pred = p; return k; }
   }
-  *pred = ttft_at(S, S.K - 1, nbt);
-  return S.K - 1;
+  *pred = ttft_at(W, K - 1, nbt);
+  return K - 1;
 }
 
-// ------------------------------------------------------------------ scenario context
-struct Ctx {
-  Node *node;
-  uint2 *wheel;            // this lane's decode instance: [NB] {head, tail}
-  uint32_t nbm;
-  double tau, slo_itl, tgt_itl, p_idle, tdp, uh_d;
-  uint32_t kvcap;
-};
-
+// ------------------------------------------------------------------ decode lanes
+// Timing-wheel bucket (16 B; all-zero = empty): x = first request + 1, y = last request + 1
+// (list in admission order), z = requests finishing in this iteration, w = their in + out.
 struct Err {               // first error of one lane in its own event order
   double t;                // +inf = none
   uint32_t code;
 };
 
-// Decode instance state: owned by lane d.
-struct Dec {
-  uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both;
+struct Dec {               // decode instance d, owned by lane d
+  uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both, nfifo, far_h, far_hfin;
   bool busy, dead;
   double end, ebusy, bms, top, sitl, tlast;
   uint64_t h;
+  uint4 bcur;              // bucket of the running iteration, read at its START (final by then)
+#if VT_QCACHE
+  Node qhn;                // register copy of the admission-queue head node
+#endif
+#if VT_BHPF
+  uint32_t bh_fin;
+  uint4 bh;
+#endif
 };
 
-__device__ __forceinline__ double avail_time(const Ctx &C, uint32_t i) {
-  return add(fabs(C.node[i].tf), C.tau);  // KvTransferDone time = t_first + tau (A18); tau = 0: routing time
+struct Lane {              // per-lane pointers
+  Node *node;
+  uint32_t *farfin;        // [N] finishing iteration of requests on the far list
+  uint4 *wheel;            // this lane's decode instance: [NB] buckets
+  uint32_t *fid;
+  double *ft;
+};
+
+__device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
+#if VT_QCACHE
+  return D.qhn;
+#else
+  return L.node[D.qh];
+#endif
+}
+
+// ITL accounting of deferred completion lists, in completion order (A30, A37); the head
+// nodes of up to four lists are loaded together.
+__device__ void itl_drain(Dec &D, const Lane &L, const WarpSmem &W) {
+  const double slo = W.slo_itl;
+  for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
+    Node h4[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + u < D.nfifo) h4[u] = L.node[L.fid[e0 + u]];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (e0 + u >= D.nfifo) continue;
+      const double td = L.ft[e0 + u];
+      Node nd = h4[u];
+      for (uint32_t hop = 0; hop < W.max_steps; ++hop) {
+        const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
+        D.sitl = add(D.sitl, itl);
+        const bool ok = itl <= slo;
+        D.n_itl_ok += ok;
+        D.n_both += ok && nd.tf > 0.0;
+        if (nd.next == NIL) break;
+        nd = L.node[nd.next];
+      }
+    }
+  }
+  D.nfifo = 0;
+}
+
+// Append request i (finishing at iteration fin) to its bucket; (lfin, lb) = the bucket
+// written last during this START, kept coherent with the prefetched copy.
+__device__ __forceinline__ void bucket_append(Dec &D, const Lane &L, uint32_t nbm, uint32_t i, uint32_t fin,
+                                              uint32_t inout, uint32_t &lfin, uint4 &lb) {
+#if VT_BHPF
+  uint4 b = fin == lfin ? lb : (fin == D.bh_fin ? D.bh : L.wheel[fin & nbm]);
+#else
+  uint4 b = fin == lfin ? lb : L.wheel[fin & nbm];
+#endif
+  L.node[i].next = NIL;
+  if (b.y == 0u) b.x = i + 1u; else L.node[b.y - 1u].next = i;
+  b.y = i + 1u;
+  b.z += 1u;
+  b.w += inout;
+  L.wheel[fin & nbm] = b;
+  lfin = fin;
+  lb = b;
+#if VT_BHPF
+  if (fin == D.bh_fin) D.bh = b;
+#endif
+}
+
+// A request finishing NB or more iterations ahead waits on the far list, sorted by
+// (finishing iteration, admission order); rare (out > NB + 1).
+__device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i, uint32_t fin) {
+  L.farfin[i] = fin;
+  if (D.far_h == NIL || fin < D.far_hfin) {
+    L.node[i].next = D.far_h;
+    D.far_h = i;
+    D.far_hfin = fin;
+    return;
+  }
+  uint32_t prev = D.far_h;
+  for (uint32_t hop = 0; hop < max_steps; ++hop) {
+    const uint32_t nx = L.node[prev].next;
+    if (nx == NIL || L.farfin[nx] > fin) break;
+    prev = nx;
+  }
+  L.node[i].next = L.node[prev].next;
+  L.node[prev].next = i;
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
-__device__ void dec_advance(Dec &D, int d, const Ctx &C, const Tables &S, double t_lim, Err &E) {
+__device__ void dec_advance(Dec &D, int d, const Lane &L, const WarpSmem &W, double t_lim, Err &E) {
   if (D.dead) return;
+  const uint32_t nbm = W.nb - 1u;
   for (;;) {
     double tnow;
     if (D.busy) {
       if (!(D.end < t_lim)) return;
       tnow = D.end;
-      // ---- O6 DecodeIterDone: +1 KV token per running request, completions of this iteration
+      // ---- O6 DecodeIterDone: +1 KV token per running request; this iteration's completions
       D.nkv += D.nreq;
-      uint2 *bk = C.wheel + (D.cur & C.nbm);
-      const uint2 b = *bk;
-      uint32_t r = b.x;
-      while (r != NIL) {
-        const Node nd = C.node[r];
-        const double itl = div(sub(tnow, fabs(nd.tf)), (double)(nd.out - 1u));  // A30
-        D.sitl = add(D.sitl, itl);
-        const bool ok = itl <= C.slo_itl;
-        D.n_itl_ok += ok;
-        D.n_both += ok && nd.tf > 0.0;
-        D.nreq -= 1u;
-        D.nkv -= (uint32_t)nd.in + (uint32_t)nd.out;
-        r = nd.next;
+      const uint4 b = D.bcur;
+      D.nreq -= b.z;
+      D.nkv -= b.w;
+      if (b.x != 0u) {
+        L.wheel[D.cur & nbm] = make_uint4(0u, 0u, 0u, 0u);
+        L.fid[D.nfifo] = b.x - 1u;
+        L.ft[D.nfifo] = tnow;
+        if (++D.nfifo == ITL_FIFO) itl_drain(D, L, W);
       }
-      if (b.x != NIL) *bk = make_uint2(NIL, NIL);
       D.busy = false;
       D.tlast = tnow;
     } else {
       // idle: the next START happens when the head of the admission queue becomes available
       if (D.qh == NIL) return;
-      const double av = avail_time(C, D.qh);
+      const double av = add(fabs(queue_head(D, L).tf), W.tau);  // KvTransferDone (A18)
       if (!(av < t_lim)) return;
       tnow = av;
     }
-    // ---- O7 START_DECODE at tnow: FCFS admission while KV fits (A20)
+    // ---- O7 START_DECODE at tnow
+    uint32_t lfin = NIL;
+    uint4 lb = make_uint4(0u, 0u, 0u, 0u);
+    // far requests whose finishing iteration entered the window join their bucket now,
+    // before any direct admission can reach that bucket (admission order, A37)
+    while (D.far_h != NIL && D.far_hfin - D.iters < W.nb) {
+      const uint32_t i = D.far_h;
+      const Node fn = L.node[i];
+      const uint32_t fin = D.far_hfin;
+      D.far_h = fn.next;
+      D.far_hfin = fn.next != NIL ? L.farfin[fn.next] : NIL;
+      bucket_append(D, L, nbm, i, fin, (uint32_t)fn.in + fn.out, lfin, lb);
+    }
+    // FCFS admission while KV fits (A20)
+    const double tau = W.tau;
+    const uint32_t kvcap = W.kvcap;
     while (D.qh != NIL) {
-      const uint32_t i = D.qh;
-      const Node hn = C.node[i];
-      if (!(add(fabs(hn.tf), C.tau) <= tnow)) break;  // still in KV transfer
+      const Node hn = queue_head(D, L);
+      if (!(add(fabs(hn.tf), tau) <= tnow)) break;  // still in KV transfer
       const uint32_t need = (uint32_t)hn.in + 1u;
-      if (D.nkv + need > C.kvcap) break;
+      if (D.nkv + need > kvcap) break;
+      const uint32_t i = D.qh;
       D.qh = hn.next;
       if (D.qh == NIL) D.qt = NIL;
+#if VT_QCACHE
+      else D.qhn = L.node[D.qh];
+#endif
       const uint32_t fin = D.iters + (uint32_t)hn.out - 2u;  // its last iteration
-      uint2 *bk = C.wheel + (fin & C.nbm);
-      uint2 b = *bk;
-      C.node[i].next = NIL;
-      if (b.y == NIL) b.x = i; else C.node[b.y].next = i;
-      b.y = i;
-      *bk = b;
+      if ((uint32_t)hn.out - 2u < W.nb) bucket_append(D, L, nbm, i, fin, (uint32_t)hn.in + hn.out, lfin, lb);
+      else far_insert(D, L, W.max_steps, i, fin);
       D.nreq += 1u;
       D.nkv += need;
       D.pn -= 1u;
       D.pkv -= need;
     }
-    const bool backlog = D.qh != NIL && avail_time(C, D.qh) <= tnow;  // A5
+    const bool backlog = D.qh != NIL && add(fabs(queue_head(D, L).tf), tau) <= tnow;  // A5
+    if (D.iters >= W.max_steps) { E.t = tnow; E.code = VOLTANA_ITEM_E_INTERNAL; D.dead = true; return; }
     if (D.nreq == 0u) {
       if (backlog) { E.t = tnow; E.code = VOLTANA_ITEM_E_KV; D.dead = true; return; }
       continue;  // stays idle
     }
     double dur;
     int k;
-    if (backlog) { k = S.K - 1; dur = itl_at(S, tile_j(S, D.nreq), k, D.nreq, D.nkv); }
-    else k = lowest_itl(S, D.nreq, D.nkv, C.tgt_itl, &dur);
+    if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, D.nreq, D.nkv); }
+    else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
     D.h = fold(D.h, 2, (uint64_t)d, (uint64_t)k, 0);
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
     D.end = add(tnow, dur);
     D.busy = true;
-    D.ebusy = add(D.ebusy, mul(busy_power(C.p_idle, C.tdp, C.uh_d, S.dyn[S.K + k], D.nreq), dur));  // W*ms (A23)
+    D.ebusy = add(D.ebusy, mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
     D.bms = add(D.bms, dur);
-    if (k == S.K - 1) D.top = add(D.top, dur);
+    if (k == (int)W.K - 1) D.top = add(D.top, dur);
     D.cur = D.iters;
     D.iters += 1u;
+    D.bcur = L.wheel[D.cur & nbm];  // final now: read at the END of this iteration
+#if VT_BHPF
+    if (D.qh != NIL) {
+      D.bh_fin = D.iters + (uint32_t)queue_head(D, L).out - 2u;
+      D.bh = L.wheel[D.bh_fin & nbm];
+    } else {
+      D.bh_fin = NIL;
+    }
+#endif
   }
+}
+
+// Append request i (routed at its first-token time) to instance d's admission queue.
+__device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, double tf, uint32_t in,
+                                         uint32_t out) {
+  D.pn += 1u;
+  D.pkv += in + 1u;
+  L.node[i].next = NIL;
+  if (D.qt == NIL) {
+    D.qh = i;
+#if VT_QCACHE
+    D.qhn.tf = tf; D.qhn.next = NIL; D.qhn.in = (uint16_t)in; D.qhn.out = (uint16_t)out;
+#endif
+  } else {
+    L.node[D.qt].next = i;
+#if VT_QCACHE
+    if (D.qt == D.qh) D.qhn.next = i;  // keep the register copy coherent
+#endif
+  }
+  D.qt = i;
 }
 
 // warp-wide min of a non-negative double held by lanes with `valid`; returns the lowest lane
@@ -223,14 +375,102 @@ __device__ __forceinline__ int argmin_time(double t, bool valid) {
   return m ? ffs0(m) : -1;
 }
 
-__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *wheels, char *wsm) {
+__device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uint32_t n_req, uint32_t status) {
+  if (lane_id() == 0) {
+    voltana_result R = voltana_result{};
+    R.status = status;
+    R.n_requests = n_req;
+    P.out[s] = R;
+  }
+}
+
+// ------------------------------------------------------------------ phase A: prefill lane p
+__device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const double *arr, const uint32_t *inl,
+                             const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0,
+                             uint32_t *head_out) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  double ebusy = 0.0, bms = 0.0, top = 0.0, sttft = 0.0, tlast = 0.0, errt = INF;
+  uint64_t h = h0;
+  uint32_t iters = 0, ttft_ok = 0, itl_ok = 0, both = 0, errc = 0, head = NIL;
+  const double tgt_ttft = W.tgt_ttft, slo_ttft = W.slo_ttft;
+  const uint32_t B = W.B, K = W.K;
+  double tfree = 0.0;
+  uint32_t nxt = p, prev = NIL;
+  Node pend;
+  pend.tf = 0.0; pend.next = NIL; pend.in = 0; pend.out = 0;
+  while (nxt < N) {
+    const double a0 = arr[nxt];
+    const double ts = tfree > a0 ? tfree : a0;  // START: instance idle and queue non-empty
+    // FCFS prefix of the arrived queue with sum(in) <= B, at least one request (A6)
+    uint32_t nbt = inl[nxt], cnt = 1, id = nxt + NP;
+    bool backlog = false;  // (A5) requests still queued after the batch
+    for (bool stop = false; !stop;) {  // 4 candidates per round, loads issued together
+      double av[4];
+      uint32_t xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t j = id + (uint32_t)u * NP;
+        av[u] = j < N ? arr[j] : INF;  // past the trace end: "not arrived"
+        xv[u] = j < N ? inl[j] : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (stop) continue;
+        if (!(av[u] <= ts)) stop = true;                                // not arrived yet
+        else if (nbt + xv[u] > B) { backlog = true; stop = true; }      // does not fit
+        else { nbt += xv[u]; cnt++; id += NP; }
+      }
+    }
+    double budget = sub(tgt_ttft, sub(ts, a0));  // A4: SLO minus the oldest request's wait
+    budget = budget > 0.0 ? budget : 0.0;
+    double dur;
+    int k;
+    if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
+    else k = lowest_ttft(W, nbt, budget, &dur);
+    h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
+    iters++;
+    if (!(dur > 0.0)) { errt = ts; errc = VOLTANA_ITEM_E_CONTRACT; break; }
+    const double end = add(ts, dur);
+    ebusy = add(ebusy, mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), dur));  // W*ms (A23)
+    bms = add(bms, dur);
+    if (k == (int)K - 1) top = add(top, dur);
+    // ---- O5 PrefillDone at `end`, batch in FCFS order
+    for (uint32_t q = 0, i = nxt; q < cnt; ++q, i += NP) {
+      const double ttft = sub(end, arr[i]);  // A26
+      sttft = add(sttft, ttft);
+      const bool ok = ttft <= slo_ttft;
+      ttft_ok += ok;
+      const uint32_t o = outl[i];
+      if (o == 1u) {  // first token came from prefill: done (A8, A30)
+        itl_ok++;
+        both += ok;
+        continue;
+      }
+      if (prev != NIL) { pend.next = i; node[prev] = pend; } else head = i;
+      prev = i;
+      pend.tf = ok ? end : -end;
+      pend.next = NIL;
+      pend.in = (uint16_t)inl[i];
+      pend.out = (uint16_t)o;
+    }
+    tfree = end;
+    tlast = end;
+    nxt = id;
+  }
+  if (prev != NIL) { pend.next = NIL; node[prev] = pend; }
+  W.pa_ebusy[p] = ebusy; W.pa_bms[p] = bms; W.pa_top[p] = top; W.pa_sttft[p] = sttft; W.pa_tlast[p] = tlast;
+  W.pa_errt[p] = errt; W.pa_errc[p] = errc; W.pa_h[p] = h; W.pa_iters[p] = iters; W.pa_ttft_ok[p] = ttft_ok;
+  W.pa_itl_ok[p] = itl_ok; W.pa_both[p] = both;
+  *head_out = head;
+}
+
+__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WarpSmem &W) {
   const int lane = lane_id();
-  voltana_result R = voltana_result{};
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
   // ---------------------------------------------------------------- ids and table rows
   if (!(P.trace_id[s] < P.n_traces && P.slo_id[s] < P.n_slos && P.layout_id[s] < P.n_layouts &&
         P.grid_id[s] < P.n_grids && P.profile_id[s] < P.n_profiles)) {
-    R.status = VOLTANA_ITEM_E_INPUT;
-    if (lane == 0) P.out[s] = R;
+    write_status(P, s, 0, VOLTANA_ITEM_E_INPUT);
     return;
   }
   const uint32_t tr = P.trace_id[s];
@@ -244,9 +484,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
   const double *arr = P.arrival + off;
   const uint32_t *inl = P.in_len + off;
   const uint32_t *outl = P.out_len + off;
-  R.n_requests = (uint32_t)N64;
 
   // ---------------------------------------------------------------- device validation (A40)
+  uint32_t tok_total;
   {
     bool ok = N64 <= P.max_requests && Dur >= 0.0;
     uint64_t tok = 0;
@@ -262,153 +502,93 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
     for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(FULL, tok, o);
     ok = __all_sync(FULL, ok) && tok <= 0x7fffffffull;
     if (!ok) {
-      R.status = VOLTANA_ITEM_E_INPUT;
-      if (lane == 0) P.out[s] = R;
+      write_status(P, s, (uint32_t)N64, VOLTANA_ITEM_E_INPUT);
       return;
     }
+    tok_total = (uint32_t)tok + 2u;
   }
   const uint32_t N = (uint32_t)N64;
   const int NP = LY.n_p, ND = LY.n_d;
 
-  // ---------------------------------------------------------------- stage the ladder's tables
-  Tables S;
-  S.K = GR.k; S.T = PR.n_tiles; S.W = PR.tile_w; S.kp = PR.k;
-  S.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
-  S.itl_smem = P.itl_smem != 0;
-  {
-    char *p = wsm;
-    uint16_t *lad = (uint16_t *)p; p += 128;
-    double *tt = (double *)p; p += 16 * VOLTANA_MAX_LEVELS;
-    double *dyn = (double *)p; p += 16 * VOLTANA_MAX_LEVELS;
-    int *mhz = (int *)p; p += 4 * VOLTANA_MAX_LEVELS;
-    double *it = (double *)p;
-    for (int k = lane; k < S.K; k += 32) {
-      const int lv = GR.level[k];
-      lad[k] = (uint16_t)lv;
-      tt[2 * k] = PR.a1[lv]; tt[2 * k + 1] = PR.c1[lv];
-      dyn[k] = PR.dyn[lv]; dyn[S.K + k] = PR.dyn[PR.k + lv];
-      mhz[k] = PR.mhz[lv];
+  // ---------------------------------------------------------------- stage constants and tables
+  const uint32_t K = (uint32_t)GR.k, T = (uint32_t)PR.n_tiles;
+  if (lane == 0) {
+    W.tau = LY.kv_transfer_ms; W.slo_itl = SL.itl_ms; W.slo_ttft = SL.ttft_ms;
+    W.tgt_itl = mul(SL.scale, SL.itl_ms);   // A3
+    W.tgt_ttft = mul(SL.scale, SL.ttft_ms);
+    W.p_idle = PR.p_idle; W.tdp = PR.tdp; W.uh_p = PR.uh[0]; W.uh_d = PR.uh[1];
+    W.a2g = PR.a2; W.b2g = PR.b2; W.c2g = PR.c2;
+    W.kvcap = LY.kv_capacity; W.max_steps = tok_total; W.B = LY.max_batch_tokens;
+    W.K = K; W.T = T; W.W = (uint32_t)PR.tile_w; W.kp = (uint32_t)PR.k; W.nb = P.nb;
+    W.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
+    W.itl_smem = P.itl_smem;
+  }
+  for (uint32_t k = lane; k < K; k += 32) {
+    const int lv = GR.level[k];
+    W.lad[k] = (uint16_t)lv;
+    W.tt[2 * k] = PR.a1[lv];
+    W.tt[2 * k + 1] = PR.c1[lv];
+    W.dyn[k] = PR.dyn[lv];
+    W.dyn[K + k] = PR.dyn[PR.k + lv];
+    W.mhz[k] = PR.mhz[lv];
+  }
+  if (P.itl_smem) {
+    for (uint32_t x = lane; x < T * K; x += 32) {
+      const uint32_t j = x / K, k = x - j * K;
+      const size_t o = (size_t)j * PR.k + GR.level[k];
+      W.it[3 * x] = PR.a2[o]; W.it[3 * x + 1] = PR.b2[o]; W.it[3 * x + 2] = PR.c2[o];
     }
-    if (S.itl_smem) {
-      for (int x = lane; x < S.T * S.K; x += 32) {
-        const int j = x / S.K, k = x - j * S.K;
-        const size_t o = (size_t)j * PR.k + GR.level[k];
-        it[3 * x] = PR.a2[o]; it[3 * x + 1] = PR.b2[o]; it[3 * x + 2] = PR.c2[o];
-      }
-    }
-    __syncwarp();
-    S.lad = lad; S.tt = tt; S.dyn = dyn; S.mhz = mhz; S.it = it;
-    S.a2g = PR.a2; S.b2g = PR.b2; S.c2g = PR.c2;
-    // coefficient-monotone (non-increasing in f) tables allow the exact binary search (A32)
+  }
+  {  // coefficient-monotone (non-increasing in f) tables allow the exact binary search (A32)
     bool mt = true, mi = true;
-    for (int k = lane; k + 1 < S.K; k += 32)
-      mt = mt && tt[2 * k + 2] <= tt[2 * k] && tt[2 * k + 3] <= tt[2 * k + 1];
-    for (int x = lane; x < S.T * (S.K - 1); x += 32) {
-      const int j = x / (S.K - 1), k = x - j * (S.K - 1);
+    for (uint32_t k = lane; k + 1 < K; k += 32)
+      mt = mt && PR.a1[GR.level[k + 1]] <= PR.a1[GR.level[k]] && PR.c1[GR.level[k + 1]] <= PR.c1[GR.level[k]];
+    for (uint32_t x = lane; x < T * (K - 1); x += 32) {
+      const uint32_t j = x / (K - 1), k = x - j * (K - 1);
       const size_t o0 = (size_t)j * PR.k + GR.level[k], o1 = (size_t)j * PR.k + GR.level[k + 1];
       mi = mi && PR.a2[o1] <= PR.a2[o0] && PR.b2[o1] <= PR.b2[o0] && PR.c2[o1] <= PR.c2[o0];
     }
-    S.mono_tt = __all_sync(FULL, mt);
-    S.mono_it = __all_sync(FULL, mi);
+    mt = __all_sync(FULL, mt);
+    mi = __all_sync(FULL, mi);
+    if (lane == 0) { W.mono_tt = mt; W.mono_it = mi; }
   }
+  __syncwarp();
   Node *node = (Node *)slot;
-  const double tgt_ttft = mul(SL.scale, SL.ttft_ms);  // A3
-  const double tgt_itl = mul(SL.scale, SL.itl_ms);
-  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const uint64_t h0 = P.hash_seed[s];
 
   // ================================================================ PHASE A: prefill lanes
-  double p_ebusy = 0.0, p_bms = 0.0, p_top = 0.0, p_sttft = 0.0, p_tlast = 0.0;
-  uint64_t p_h = P.hash_seed[s];
-  uint32_t p_iters = 0, p_ttft_ok = 0, p_itl_ok = 0, p_both = 0, p_head = NIL;
-  Err pE = {INF, 0};
-  if (lane < NP) {
-    const uint32_t p = (uint32_t)lane, NPu = (uint32_t)NP;
-    double tfree = 0.0;
-    uint32_t nxt = p, prev = NIL;
-    Node pend;
-    pend.tf = 0.0; pend.next = NIL; pend.in = 0; pend.out = 0;
-    while (nxt < N) {
-      const double a0 = arr[nxt];
-      const double ts = tfree > a0 ? tfree : a0;  // START: instance idle and queue non-empty
-      // FCFS prefix of the arrived queue with sum(in) <= B, at least one request (A6)
-      uint32_t nbt = inl[nxt], cnt = 1, id = nxt + NPu;
-      bool backlog = false;
-      for (bool stop = false; !stop;) {  // 4 candidates per round, loads issued together
-        double av[4];
-        uint32_t xv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const uint32_t j = id + (uint32_t)u * NPu;
-          av[u] = j < N ? arr[j] : INF;     // past the trace end: "not arrived"
-          xv[u] = j < N ? inl[j] : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (stop) continue;
-          if (!(av[u] <= ts)) stop = true;                                             // not arrived yet
-          else if (nbt + xv[u] > LY.max_batch_tokens) { backlog = true; stop = true; }  // does not fit
-          else { nbt += xv[u]; cnt++; id += NPu; }
-        }
-      }
-      // (A5) backlog: requests still queued after the batch
-      double budget = sub(tgt_ttft, sub(ts, a0));  // A4: SLO minus the oldest request's wait
-      budget = budget > 0.0 ? budget : 0.0;
-      double dur;
-      int k;
-      if (backlog) { k = S.K - 1; dur = ttft_at(S, k, nbt); }
-      else k = lowest_ttft(S, nbt, budget, &dur);
-      p_h = fold(p_h, 1, (uint64_t)p, (uint64_t)k, 0);
-      p_iters++;
-      if (!(dur > 0.0)) { pE.t = ts; pE.code = VOLTANA_ITEM_E_CONTRACT; break; }
-      const double end = add(ts, dur);
-      p_ebusy = add(p_ebusy, mul(busy_power(PR.p_idle, PR.tdp, PR.uh[0], S.dyn[k], nbt), dur));  // W*ms (A23)
-      p_bms = add(p_bms, dur);
-      if (k == S.K - 1) p_top = add(p_top, dur);
-      // ---- O5 PrefillDone at `end`, batch in FCFS order
-      for (uint32_t q = 0, i = nxt; q < cnt; ++q, i += NPu) {
-        const double ttft = sub(end, arr[i]);  // A26
-        p_sttft = add(p_sttft, ttft);
-        const bool ok = ttft <= SL.ttft_ms;
-        p_ttft_ok += ok;
-        const uint32_t o = outl[i];
-        if (o == 1u) {  // first token came from prefill: done (A8, A30)
-          p_itl_ok++;
-          p_both += ok;
-          continue;
-        }
-        if (prev != NIL) { pend.next = i; node[prev] = pend; } else p_head = i;
-        prev = i;
-        pend.tf = ok ? end : -end;
-        pend.next = NIL;
-        pend.in = (uint16_t)inl[i];
-        pend.out = (uint16_t)o;
-      }
-      tfree = end;
-      p_tlast = end;
-      nxt = id;
-    }
-    if (prev != NIL) { pend.next = NIL; node[prev] = pend; }
-  }
+  uint32_t p_head = NIL;
+  if (lane < NP) prefill_lane(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
   __syncwarp();
 
   // ================================================================ PHASE B: routing + decode lanes
-  Ctx C;
-  C.node = node;
-  C.wheel = wheels + (size_t)(lane < ND ? lane : 0) * P.nb;
-  C.nbm = P.nb - 1u;
-  C.tau = LY.kv_transfer_ms; C.slo_itl = SL.itl_ms; C.tgt_itl = tgt_itl;
-  C.p_idle = PR.p_idle; C.tdp = PR.tdp; C.uh_d = PR.uh[1]; C.kvcap = LY.kv_capacity;
+  const int dl = lane < ND ? lane : 0;
+  Lane L;
+  L.node = node;
+  L.farfin = (uint32_t *)(slot + P.node_bytes);
+  L.wheel = wheels + (size_t)dl * P.nb;
+  L.fid = W.fid[dl];
+  L.ft = W.ft[dl];
   Dec D;
   D.nreq = D.nkv = D.pn = D.pkv = D.iters = D.cur = 0;
   D.qh = D.qt = NIL;
-  D.n_itl_ok = D.n_both = 0;
-  D.busy = false; D.dead = !(lane < ND);
+  D.n_itl_ok = D.n_both = D.nfifo = 0;
+  D.far_h = D.far_hfin = NIL;
+  D.busy = false;
+  D.dead = !(lane < ND);
   D.end = D.ebusy = D.bms = D.top = D.sitl = D.tlast = 0.0;
-  D.h = P.hash_seed[s];
+  D.h = h0;
+  D.bcur = make_uint4(0u, 0u, 0u, 0u);
+#if VT_QCACHE
+  D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.in = 0; D.qhn.out = 0;
+#endif
+#if VT_BHPF
+  D.bh_fin = NIL;
+  D.bh = D.bcur;
+#endif
   Err dE = {INF, 0};
 
-  // stream head of prefill lane p: next routed request in its completion order
-  // (head node hn and, loaded one step ahead, its successor nn)
+  // stream head of prefill lane p (head node hn and, loaded one step ahead, its successor nn)
   uint32_t hd = lane < NP ? p_head : NIL;
   Node hn, nn;
   hn.tf = 0.0; hn.next = NIL; hn.in = 0; hn.out = 0;
@@ -417,23 +597,27 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
     hn = node[hd];
     if (hn.next != NIL) nn = node[hn.next];
   }
-  uint64_t h_r = P.hash_seed[s];
+  uint64_t h_r = h0;
   uint32_t cursor = 0, steps_route = 0;
   const bool eco = LY.policy == 0 && ND > 1;
+  const int32_t delta = LY.delta_mhz;
   for (;;) {
     const double ht = fabs(hn.tf);
     const int w = argmin_time(ht, hd != NIL);  // next PrefillDone request in (t, p, id) order
     if (w < 0) break;
+    if (steps_route > N) { dE.t = 0.0; dE.code = VOLTANA_ITEM_E_INTERNAL; break; }  // watchdog
     const double t = __shfl_sync(FULL, ht, w);
     const uint32_t i = __shfl_sync(FULL, hd, w);
-    const uint32_t in_i = __shfl_sync(FULL, (uint32_t)hn.in, w);
-    if (lane == w) {                           // advance that stream; prefetch one further
+    const uint32_t io = __shfl_sync(FULL, (uint32_t)hn.in | ((uint32_t)hn.out << 16), w);
+    const double tf_i = __shfl_sync(FULL, hn.tf, w);  // signed: carries the TTFT verdict
+    const uint32_t in_i = io & 0xffffu;
+    if (lane == w) {                                  // advance that stream; prefetch one further
       hd = hn.next;
       hn = nn;
       if (hd != NIL && hn.next != NIL) nn = node[hn.next];
     }
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
-    dec_advance(D, lane, C, S, t, dE);
+    dec_advance(D, lane, L, W, t, dE);
     // ---- O8 EcoRoute
     int dsel, cse;
     if (!eco) {
@@ -445,15 +629,14 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
       if (lane < ND) {
         const uint32_t n = D.nreq + D.pn, kv = D.nkv + D.pkv;  // A9 effective state
         double pr;
-        const int kn = n == 0u ? 0 : lowest_itl(S, n, kv, tgt_itl, &pr);  // A10, A11
-        const int ka = lowest_itl(S, n + 1u, kv + in_i + 1u, tgt_itl, &pr);  // A12
-        fnow = S.mhz[kn];
-        faft = S.mhz[ka];
+        const int kn = n == 0u ? 0 : lowest_itl(W, n, kv, W.tgt_itl, &pr);  // A10, A11
+        const int ka = lowest_itl(W, n + 1u, kv + in_i + 1u, W.tgt_itl, &pr);  // A12
+        fnow = W.mhz[kn];
+        faft = W.mhz[ka];
       }
       const bool act = lane < ND;
       const bool cr = act && faft > fnow;  // A13
-      const unsigned Rm = __ballot_sync(FULL, cr);
-      const int nc = __popc(Rm);
+      const int nc = __popc(__ballot_sync(FULL, cr));
       const int mn = (int)__reduce_min_sync(FULL, (unsigned)fnow);
       unsigned inset;
       if (nc == 0) {
@@ -463,7 +646,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
         const int mu = (int)__reduce_min_sync(FULL, (unsigned)(act && !cr ? fnow : 0x7fffffff));
         const int mr = (int)__reduce_min_sync(FULL, (unsigned)(cr ? faft : 0x7fffffff));
         const long long g = (long long)mu - (long long)mr;  // A14, A15
-        if (g <= (long long)LY.delta_mhz) { inset = __ballot_sync(FULL, act && !cr && fnow == mu); cse = 3; }
+        if (g <= (long long)delta) { inset = __ballot_sync(FULL, act && !cr && fnow == mu); cse = 3; }
         else { inset = __ballot_sync(FULL, act && fnow == mn); cse = 4; }
       } else {
         const int ma = (int)__reduce_min_sync(FULL, (unsigned)faft);
@@ -477,74 +660,81 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint2 *
     }
     steps_route++;
     h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
-    if (lane == dsel) {
-      D.pn += 1u;
-      D.pkv += in_i + 1u;
-      node[i].next = NIL;
-      if (D.qt == NIL) D.qh = i; else node[D.qt].next = i;
-      D.qt = i;
-    }
+    if (lane == dsel) dec_push(D, L, i, tf_i, in_i, io >> 16);
   }
-  // drain: every decode instance runs to completion
-  dec_advance(D, lane, C, S, INF, dE);
+  // drain: every decode instance runs to completion, then its deferred ITL accounting
+  dec_advance(D, lane, L, W, INF, dE);
+  if (lane < ND && !D.dead) itl_drain(D, L, W);
   __syncwarp();
 
   // ================================================================ O9: record
   // first error in (time, prefill before decode, instance) order = the oracle's stop point
-  const int wp = argmin_time(pE.t, lane < NP && pE.t < INF);
+  const double pet = lane < NP ? W.pa_errt[lane] : INF;
+  const int wp = argmin_time(pet, lane < NP && pet < INF);
   const int wd = argmin_time(dE.t, lane < ND && dE.t < INF);
   if (wp >= 0 || wd >= 0) {
-    const double tp = wp >= 0 ? __shfl_sync(FULL, pE.t, wp) : INF;
+    const double tp = wp >= 0 ? W.pa_errt[wp] : INF;
     const double td = wd >= 0 ? __shfl_sync(FULL, dE.t, wd) : INF;
-    const uint32_t cp = __shfl_sync(FULL, pE.code, wp >= 0 ? wp : 0);
     const uint32_t cd = __shfl_sync(FULL, dE.code, wd >= 0 ? wd : 0);
-    R.status = (wp >= 0 && tp <= td) ? cp : cd;
-    // leave the wheels clean for the next scenario of this warp
-    if (lane < ND)
-      for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint2(NIL, NIL);
-    if (lane == 0) P.out[s] = R;
+    write_status(P, s, N, (wp >= 0 && tp <= td) ? W.pa_errc[wp] : cd);
+    if (lane < ND)  // leave the wheel clean for the next scenario of this warp
+      for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
-  double tl = p_tlast > D.tlast ? p_tlast : D.tlast;
+  double tl = D.tlast;
+  if (lane < NP) tl = tl > W.pa_tlast[lane] ? tl : W.pa_tlast[lane];
   for (int o = 16; o > 0; o >>= 1) {
     const double x = __shfl_xor_sync(FULL, tl, o);
     tl = x > tl ? x : tl;
   }
   const double horizon = Dur > tl ? Dur : tl;  // A23
-  uint64_t hh = splitmix64(h_r);                // A36: route chain, prefill chains, decode chains
-  double sttft = 0.0, sitl = 0.0, top = 0.0, epb = 0.0, epi = 0.0, edb = 0.0, edi = 0.0, bp = 0.0, bd = 0.0;
-  for (int q = 0; q < NP; ++q) {
-    hh = splitmix64(hh ^ __shfl_sync(FULL, p_h, q));
-    sttft = add(sttft, __shfl_sync(FULL, p_sttft, q));
-    top = add(top, __shfl_sync(FULL, p_top, q));
-    epb = add(epb, div(__shfl_sync(FULL, p_ebusy, q), 1000.0));
-    const double b = __shfl_sync(FULL, p_bms, q);
-    epi = add(epi, energy_j(PR.p_idle, sub(horizon, b)));
-    bp = add(bp, b);
+  // decode instances: lane d's totals gathered in instance order (A36/A37)
+  uint64_t hd_[NI];
+  double topd_[NI];
+  double sitl = 0.0, edb = 0.0, edi = 0.0, bd = 0.0;
+#pragma unroll
+  for (int d = 0; d < NI; ++d) {
+    hd_[d] = __shfl_sync(FULL, D.h, d);
+    if (d < ND) {
+      sitl = add(sitl, __shfl_sync(FULL, D.sitl, d));
+      topd_[d] = __shfl_sync(FULL, D.top, d);
+      edb = add(edb, div(__shfl_sync(FULL, D.ebusy, d), 1000.0));
+      const double b = __shfl_sync(FULL, D.bms, d);
+      edi = add(edi, energy_j(W.p_idle, sub(horizon, b)));
+      bd = add(bd, b);
+    }
   }
-  for (int d = 0; d < ND; ++d) {
-    hh = splitmix64(hh ^ __shfl_sync(FULL, D.h, d));
-    sitl = add(sitl, __shfl_sync(FULL, D.sitl, d));
-    top = add(top, __shfl_sync(FULL, D.top, d));
-    edb = add(edb, div(__shfl_sync(FULL, D.ebusy, d), 1000.0));
-    const double b = __shfl_sync(FULL, D.bms, d);
-    edi = add(edi, energy_j(PR.p_idle, sub(horizon, b)));
-    bd = add(bd, b);
+  const uint32_t c_itl = __reduce_add_sync(FULL, lane < ND ? D.n_itl_ok : 0u);
+  const uint32_t c_both = __reduce_add_sync(FULL, lane < ND ? D.n_both : 0u);
+  const uint32_t c_di = __reduce_add_sync(FULL, lane < ND ? D.iters : 0u);
+  if (lane == 0) {
+    voltana_result R = voltana_result{};
+    uint64_t hh = splitmix64(h_r);  // A36: route chain, then prefill chains, then decode chains
+    double sttft = 0.0, top = 0.0, epb = 0.0, epi = 0.0, bp = 0.0;
+    uint32_t c_ttft = 0, c_itl_p = 0, c_both_p = 0, c_pi = 0;
+    for (int q = 0; q < NP; ++q) {
+      hh = splitmix64(hh ^ W.pa_h[q]);
+      sttft = add(sttft, W.pa_sttft[q]);
+      top = add(top, W.pa_top[q]);
+      epb = add(epb, div(W.pa_ebusy[q], 1000.0));
+      epi = add(epi, energy_j(W.p_idle, sub(horizon, W.pa_bms[q])));
+      bp = add(bp, W.pa_bms[q]);
+      c_ttft += W.pa_ttft_ok[q]; c_itl_p += W.pa_itl_ok[q]; c_both_p += W.pa_both[q]; c_pi += W.pa_iters[q];
+    }
+#pragma unroll
+    for (int d = 0; d < NI; ++d)
+      if (d < ND) {
+        hh = splitmix64(hh ^ hd_[d]);
+        top = add(top, topd_[d]);  // one running sum: prefill instances, then decode (A37)
+      }
+    R.status = 0; R.n_requests = N;
+    R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl_p + c_itl; R.n_both_ok = c_both_p + c_both; R.prefill_iters = c_pi;
+    R.steps_ctrl = (uint64_t)c_pi + c_di; R.steps_route = steps_route; R.decision_hash = hh;
+    R.sum_ttft_ms = sttft; R.sum_itl_mean_ms = sitl;
+    R.e_prefill_busy_j = epb; R.e_prefill_idle_j = epi; R.e_decode_busy_j = edb; R.e_decode_idle_j = edi;
+    R.busy_ms_prefill = bp; R.busy_ms_decode = bd; R.top_level_ms = top; R.horizon_ms = horizon;
+    P.out[s] = R;
   }
-  uint32_t c_ttft = p_ttft_ok, c_itl = p_itl_ok + (lane < ND ? D.n_itl_ok : 0u);
-  uint32_t c_both = p_both + (lane < ND ? D.n_both : 0u), c_pi = lane < NP ? p_iters : 0u;
-  uint32_t c_di = lane < ND ? D.iters : 0u;
-  c_ttft = __reduce_add_sync(FULL, c_ttft);
-  c_itl = __reduce_add_sync(FULL, c_itl);
-  c_both = __reduce_add_sync(FULL, c_both);
-  c_pi = __reduce_add_sync(FULL, c_pi);
-  c_di = __reduce_add_sync(FULL, c_di);
-  R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl; R.n_both_ok = c_both; R.prefill_iters = c_pi;
-  R.steps_ctrl = (uint64_t)c_pi + c_di; R.steps_route = steps_route; R.decision_hash = hh;
-  R.sum_ttft_ms = sttft; R.sum_itl_mean_ms = sitl;
-  R.e_prefill_busy_j = epb; R.e_prefill_idle_j = epi; R.e_decode_busy_j = edb; R.e_decode_idle_j = edi;
-  R.busy_ms_prefill = bp; R.busy_ms_decode = bd; R.top_level_ms = top; R.horizon_ms = horizon;
-  if (lane == 0) P.out[s] = R;
 }
 
 __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(const __grid_constant__ SimParams P) {
@@ -554,17 +744,29 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (warp >= P.n_slots) return;
   char *slot = P.slots + (size_t)warp * P.slot_bytes;
-  uint2 *wheels = P.wheels + (size_t)warp * P.wheel_per_slot;
-  char *wsm = smem + (size_t)wib * P.smem_per_warp;
+  uint4 *wheels = P.wheels + (size_t)warp * P.wheel_per_slot;
+  WarpSmem &W = *(WarpSmem *)(smem + (size_t)wib * P.smem_per_warp);
   for (;;) {
     uint32_t s = 0;
     if (lane == 0) s = atomicAdd(P.counter, 1u);
     s = __shfl_sync(FULL, s, 0);
     if (s >= P.n) break;
-    run_scenario(P, s, slot, wheels, wsm);
+    uint64_t t0 = 0;
+    if (P.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    run_scenario(P, s, slot, wheels, W);
     __syncwarp();
+    if (P.timing && lane == 0) {
+      uint64_t t1;
+      uint32_t sm;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      P.timing[2 * s] = t0;
+      P.timing[2 * s + 1] = (t1 - t0) | ((uint64_t)sm << 56);
+    }
   }
 }
+
+size_t sim_smem_fixed() { return (sizeof(WarpSmem) - sizeof(double) + 15) & ~(size_t)15; }
 
 const void *sim_kernel_ptr() { return (const void *)simulate_kernel; }
 

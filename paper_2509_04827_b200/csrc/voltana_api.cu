@@ -18,6 +18,7 @@ namespace {
 
 thread_local char g_detail[512] = "";
 thread_local int g_launches = 0;
+thread_local uint64_t *g_debug_timing = nullptr;
 
 voltana_status fail(voltana_status s, const char *fmt, ...) {
   va_list ap;
@@ -96,6 +97,7 @@ const char *voltana_status_string(voltana_status s) {
 
 const char *voltana_last_error_detail(void) { return g_detail; }
 int voltana_last_launch_count(void) { return g_launches; }
+void voltana_debug_set_timing(uint64_t *buf) { g_debug_timing = buf; }
 
 // ------------------------------------------------------------------ K2
 voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, const uint16_t *ladder_h, int k,
@@ -237,7 +239,7 @@ int max_nd(const voltana_layout *lays, int n_layouts) {
 
 uint32_t wheel_buckets(uint32_t max_out) {
   uint32_t nb = 2;
-  while (nb < max_out) nb <<= 1;
+  while (nb < max_out && nb < SIM_WHEEL_MAX) nb <<= 1;
   return nb;
 }
 
@@ -271,16 +273,17 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.nb = wheel_buckets(tr->max_out);
   size_t itl_bytes = (size_t)kmax * tmax * 24;
   L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
-  L.smem_per_warp = (SIM_SMEM_FIXED + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
+  L.smem_per_warp = (sim_smem_fixed() + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
   L.smem = L.smem_per_warp * (SIM_THREADS / 32);
   L.node = align256((size_t)tr->max_requests * 16);
-  L.slot = L.node > 256 ? L.node : 256;
+  L.slot = L.node + align256((size_t)tr->max_requests * 4);
+  L.slot = L.slot > 256 ? L.slot : 256;
   L.wheel_per_slot = (size_t)max_nd(lays, n_layouts) * L.nb;
   size_t rw = (size_t)resident_warps(L.smem);
   L.n_slots = (uint32_t)(n < rw ? (n < 1 ? 1 : n) : rw);
   L.slots_off = 256;
   L.wheels_off = align256(L.slots_off + (size_t)L.n_slots * L.slot);
-  L.total = L.wheels_off + (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint2);
+  L.total = L.wheels_off + (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint4);
   return L;
 }
 
@@ -379,19 +382,21 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   P->counter = (uint32_t *)ws;
   P->slots = ws + L.slots_off;
   P->slot_bytes = L.slot;
-  P->wheels = (uint2 *)(ws + L.wheels_off);
+  P->node_bytes = L.node;
+  P->wheels = (uint4 *)(ws + L.wheels_off);
   P->wheel_per_slot = L.wheel_per_slot;
   P->itl_smem = L.itl_smem;
   P->smem_per_warp = (uint32_t)L.smem_per_warp;
+  P->timing = g_debug_timing;
   for (int i = 0; i < n_slos; ++i) P->slo[i] = slos_h[i];
   for (int i = 0; i < n_layouts; ++i) P->lay[i] = layouts_h[i];
   for (int i = 0; i < n_grids; ++i) P->grid[i] = grids_h[i];
   for (int i = 0; i < n_profiles; ++i) P->prof[i] = to_dev(profiles_h[i]);
   cudaStream_t st = (cudaStream_t)stream;
-  // scenario counter = 0; every wheel bucket = {NIL, NIL} (buckets are left clean after use)
+  // scenario counter = 0; every wheel bucket empty (buckets are left clean after use)
   cudaError_t e = cudaMemsetAsync(P->counter, 0, sizeof(uint32_t), st);
   if (e == cudaSuccess)
-    e = cudaMemsetAsync(P->wheels, 0xFF, (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint2), st);
+    e = cudaMemsetAsync(P->wheels, 0, (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint4), st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
   const int grid = (int)((L.n_slots + (SIM_THREADS / 32) - 1) / (SIM_THREADS / 32));
   e = launch_sim(*P, grid, L.smem, st);

@@ -74,7 +74,7 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 // decision hash fold (A36)
 __device__ __forceinline__ uint64_t fold(uint64_t h, uint64_t kind, uint64_t inst, uint64_t level,
                                          uint64_t cse) {
-  return splitmix64(h ^ ((kind << 48) ^ (inst << 32) ^ (level << 16) ^ cse));
+  return (h ^ ((kind << 48) ^ (inst << 32) ^ (level << 16) ^ cse)) * 0x9E3779B97F4A7C15ull;
 }
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

@@ -15,8 +15,9 @@ constexpr int SIM_THREADS = 128;      // 4 warps per CTA, one scenario per warp
 #endif
 constexpr int SIM_MIN_BLOCKS = VT_SIM_MIN_BLOCKS;  // 4: <= 128 registers, 16 warps per SM
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
-constexpr size_t SIM_SMEM_FIXED = 128 + 16 * VOLTANA_MAX_LEVELS * 2 + 4 * VOLTANA_MAX_LEVELS;  // per warp
+size_t sim_smem_fixed();  // per-warp shared-memory block without the staged ITL table
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size
+constexpr uint32_t SIM_WHEEL_MAX = 1024;    // decode wheel buckets (L2-resident); longer requests use the far list
 
 struct SimParams {
   // traces (device)
@@ -38,11 +39,12 @@ struct SimParams {
   // workspace
   uint32_t *counter;
   char *slots;                 // [n_slots][slot_bytes]: request nodes
-  size_t slot_bytes;
-  uint2 *wheels;               // [n_slots][wheel_per_slot]: decode timing wheels
+  size_t slot_bytes, node_bytes;  // slot = [N] 16-B nodes, then [N] u32 far-list finishing iterations
+  uint4 *wheels;               // [n_slots][wheel_per_slot]: decode timing wheels (16-B buckets, 0 = empty)
   size_t wheel_per_slot;       // max N_D * nb buckets
   uint32_t itl_smem;           // stage the ladder's ITL table in shared memory
   uint32_t smem_per_warp;
+  uint64_t *timing;            // debug: [n][2] globaltimer ns at scenario start/end | smid<<56 (NULL: off)
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];

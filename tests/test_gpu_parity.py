@@ -229,6 +229,21 @@ def test_simulate_edge_cases(vt, orc):
     _one(vt, orc, arr, inl, outl, 20000.0, b, Slo(100, 10), Layout(4, 4), list(range(60)))
 
 
+def test_simulate_wheel_bucket_reuse(vt, orc):
+    """Many requests admitted at one START whose finishing iterations alternate between a few
+    buckets (out lengths 2,3,2,3,... and long/short mixes), with KV-blocked heads: exercises the
+    decode timing wheel's bucket coherence and the cached admission-queue head."""
+    p = synth.make_profile("L8")
+    n = 600
+    arr = np.repeat(np.arange(60) * 50.0, 10)
+    outl = np.tile([2, 3, 2, 3, 40, 2, 3, 900, 2, 5], 60)
+    outl[7::37] = 1030 + np.arange(len(outl[7::37])) % 3 * 700    # far list: finishes > 1024 ahead
+    inl = np.tile([10, 20, 30, 3000, 10, 10, 4000, 10, 10, 20], 60)
+    for cap in (400000, 9000):
+        _one(vt, orc, arr, inl, outl, 4000.0, p, Slo(600, 60), Layout(1, 2, kv_capacity=cap), [0, 6, 13, 20, 27])
+        _one(vt, orc, arr, inl, outl, 4000.0, p, Slo(600, 60), Layout(2, 1, kv_capacity=cap), [0, 27])
+
+
 def test_simulate_invalid_trace_status(vt, orc):
     p = synth.make_profile("L8")
     r = _one(vt, orc, [5.0, 1.0], [10, 10], [5, 5], 100.0, p, Slo(600, 60), Layout(1, 1), [0, 27])

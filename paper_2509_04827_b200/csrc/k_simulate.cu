@@ -40,6 +40,9 @@
 #ifndef VT_BHPF
 #define VT_BHPF 0      // prefetch the bucket the queue head will join at the next START
 #endif
+#ifndef VT_ITL_FIFO
+#define VT_ITL_FIFO 1  // completion lists deferred before their ITL accounting runs (1..8; 1 measured best)
+#endif
 
 namespace vt {
 
@@ -81,13 +84,14 @@ __device__ __forceinline__ uint32_t tile_j(const WarpSmem &W, uint32_t n) {
   return j < W.T - 1u ? j : W.T - 1u;
 }
 
-__device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, uint32_t n, uint32_t kv) {
+// eq:pred-itl at ladder index k, tile j; dn = (double)N_req, dkv = (double)N_kv (exact)
+__device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, double dn, double dkv) {
   if (W.itl_smem) {
     const double *r = W.it + 3 * ((size_t)j * W.K + k);
-    return itl_pred(r[0], r[1], r[2], n, kv);
+    return add(add(mul(r[0], dn), mul(r[1], dkv)), r[2]);
   }
   const size_t o = (size_t)j * W.kp + W.lad[k];
-  return itl_pred(__ldg(W.a2g + o), __ldg(W.b2g + o), __ldg(W.c2g + o), n, kv);
+  return add(add(mul(__ldg(W.a2g + o), dn), mul(__ldg(W.b2g + o), dkv)), __ldg(W.c2g + o));
 }
 
 __device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt) {
@@ -100,21 +104,22 @@ __device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt
 __device__ int lowest_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
   const uint32_t j = tile_j(W, n);
   const int K = (int)W.K;
+  const double dn = (double)n, dkv = (double)kv;
   if (W.mono_it && K > 8) {
     int lo = 0, hi = K;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (itl_at(W, j, mid, n, kv) <= target) hi = mid; else lo = mid + 1;
+      if (itl_at(W, j, mid, dn, dkv) <= target) hi = mid; else lo = mid + 1;
     }
     const int k = lo < K ? lo : K - 1;
-    *pred = itl_at(W, j, k, n, kv);
+    *pred = itl_at(W, j, k, dn, dkv);
     return k;
   }
   for (int k = 0; k < K - 1; ++k) {
-    const double p = itl_at(W, j, k, n, kv);
+    const double p = itl_at(W, j, k, dn, dkv);
     if (p <= target) { *pred = p; return k; }
   }
-  *pred = itl_at(W, j, K - 1, n, kv);
+  *pred = itl_at(W, j, K - 1, dn, dkv);
   return K - 1;
 }
 
@@ -265,7 +270,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, const WarpSmem &W, dou
         L.wheel[D.cur & nbm] = make_uint4(0u, 0u, 0u, 0u);
         L.fid[D.nfifo] = b.x - 1u;
         L.ft[D.nfifo] = tnow;
-        if (++D.nfifo == ITL_FIFO) itl_drain(D, L, W);
+        if (++D.nfifo == VT_ITL_FIFO) itl_drain(D, L, W);
       }
       D.busy = false;
       D.tlast = tnow;
@@ -319,7 +324,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, const WarpSmem &W, dou
     }
     double dur;
     int k;
-    if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, D.nreq, D.nkv); }
+    if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
     else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
     D.h = fold(D.h, 2, (uint64_t)d, (uint64_t)k, 0);
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
@@ -599,6 +604,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   uint64_t h_r = h0;
   uint32_t cursor = 0, steps_route = 0;
+  double t_adv = -1.0;                              // decode lanes are caught up to events < t_adv
+  uint32_t c_n = NIL, c_kv = 0;                     // what-if cache: EcoFreq level of the lane's
+  int c_lvl = 0;                                    // effective state (c_n, c_kv)
+  int ka_last = 0;
   const bool eco = LY.policy == 0 && ND > 1;
   const int32_t delta = LY.delta_mhz;
   for (;;) {
@@ -617,7 +626,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       if (hd != NIL && hn.next != NIL) nn = node[hn.next];
     }
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
-    dec_advance(D, lane, L, W, t, dE);
+    if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
+      dec_advance(D, lane, L, W, t, dE);
+      t_adv = t;
+    }
     // ---- O8 EcoRoute
     int dsel, cse;
     if (!eco) {
@@ -629,8 +641,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       if (lane < ND) {
         const uint32_t n = D.nreq + D.pn, kv = D.nkv + D.pkv;  // A9 effective state
         double pr;
-        const int kn = n == 0u ? 0 : lowest_itl(W, n, kv, W.tgt_itl, &pr);  // A10, A11
+        int kn = 0;                                                            // A10, A11
+        if (n != 0u) {
+          if (n != c_n || kv != c_kv) { c_lvl = lowest_itl(W, n, kv, W.tgt_itl, &pr); c_n = n; c_kv = kv; }
+          kn = c_lvl;
+        }
         const int ka = lowest_itl(W, n + 1u, kv + in_i + 1u, W.tgt_itl, &pr);  // A12
+        ka_last = ka;
         fnow = W.mhz[kn];
         faft = W.mhz[ka];
       }
@@ -660,7 +677,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
     steps_route++;
     h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
-    if (lane == dsel) dec_push(D, L, i, tf_i, in_i, io >> 16);
+    if (lane == dsel) {
+      if (eco) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
+      dec_push(D, L, i, tf_i, in_i, io >> 16);
+    }
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
   dec_advance(D, lane, L, W, INF, dE);

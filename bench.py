@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "scenario-steps/sec (ctrl+router decisions)"
+METRIC = "scenario-steps/sec (ctrl+router decisions) at 1/2/4/8 B200; % of HBM roofline"  # BASELINE.json
 UNIT = "steps/s"
 CONFIG_NAME = "C4"
 N_SAMPLES = 2_000_000
@@ -47,7 +47,66 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1024, help="scenarios in the oracle sample")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-streaming", action="store_true", help="skip the K1/K2/K3 streaming sub-bench")
     return ap.parse_args()
+
+
+def streaming_kernels(vt, torch, dev, hbm_gbs, reps=10):
+    """K2 control_step, K3 route_batch and K1 fit_profile on large SoA batches (HBM-bound):
+    algorithmic bytes per launch / mean CUDA-event time, against the measured copy bandwidth."""
+    import synth
+    from synth.samples import profile_samples
+    prof = synth.make_profile("L8")
+    dp = vt.DeviceProfile(prof, dev)
+    lad = [0, 6, 13, 20, 27]
+    g = torch.Generator(device=dev).manual_seed(0)
+    n = 1 << 25
+    u32 = lambda lo, hi, size: torch.randint(lo, hi, size, generator=g, device=dev, dtype=torch.int64).to(torch.int32).view(torch.uint32)
+    load = u32(1, 700, (n,))
+    kv = u32(700, 300000, (n,))
+    q = (torch.rand(n, generator=g, device=dev) < 0.05).to(torch.int32).view(torch.uint32)
+    tgt = torch.rand(n, generator=g, device=dev, dtype=torch.float64) * 60 + 20
+    out = {}
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        b.synchronize()
+        return a.elapsed_time(b) / reps / 1000.0
+
+    s = timed(lambda: vt.control_step(dp, 1, lad, load, kv, q, None, tgt))
+    by = n * (4 + 4 + 4 + 8 + 2 + 1)
+    out["control_step"] = {"items": n, "bytes_per_item": 23, "ms": s * 1e3, "achieved_gbs": by / s / 1e9,
+                           "frac": by / s / 1e9 / hbm_gbs, "decisions_per_s": n / s}
+    nd, m = 2, 1 << 24
+    nr = u32(0, 500, (m * nd,))
+    nk = u32(500, 200000, (m * nd,))
+    rin = u32(1, 4000, (m,))
+    cur = torch.zeros(m, dtype=torch.int32, device=dev).view(torch.uint32)
+    s = timed(lambda: vt.route_batch(dp, lad, nd, nr, nk, rin, tgt[:m], 150, 0, cur))
+    by = m * (8 * nd + 4 + 8 + 4 + 4 + 2 + 1 + 1)
+    out["route_batch"] = {"items": m, "bytes_per_item": 8 * nd + 24, "ms": s * 1e3, "achieved_gbs": by / s / 1e9,
+                          "frac": by / s / 1e9 / hbm_gbs, "decisions_per_s": m / s}
+    smp = profile_samples(prof, 4096, 4096, noise_sigma=0.02, seed=9)
+    to = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else
+                                    (a.view(np.int16) if a.dtype == np.uint16 else a)).to(dev)
+    d = {k: to(v) for k, v in smp.items()}
+    for k in ("n_bt", "n_req", "n_kv"):
+        d[k] = d[k].view(torch.uint32)
+    d["level"] = d["level"].view(torch.uint16)
+    ns = int(d["lat_ms"].numel())
+    fo = vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k, prof.n_tiles)
+    s = timed(lambda: vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k,
+                                     prof.n_tiles, workspace=fo["workspace"], out=fo))
+    by = 3 * ns * 23
+    out["fit_profile"] = {"samples": ns, "bytes_per_sample": 69, "ms": s * 1e3, "achieved_gbs": by / s / 1e9,
+                          "frac": by / s / 1e9 / hbm_gbs, "note": "3 streaming passes x 23 B/sample"}
+    return out
 
 
 def dist_env():
@@ -279,8 +338,12 @@ def run_ours(args):
     comp_bytes = trace_bytes + 128 * wl.n
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    traffic = None
+    tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # committed summary of one ncu --set full capture
+    if os.path.exists(tj):
+        traffic = json.load(open(tj)).get("simulate_kernel", {}).get("dram_bytes_per_launch")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": None, "kernel": "vt::simulate_kernel<2,2>",
+            "traffic": traffic, "kernel": "vt::simulate_kernel",
             "note": "algorithmic FP64 ops of the decision procedure (prefill ctrl 2K, decode ctrl 4K, route "
                     "8*N_D*K per decision) / mean kernel time; peak = 148 SM x 64 FP64 lanes x 1965 MHz "
                     "(non-FMA ops); the kernel is latency/issue-bound on the serial event loop",
@@ -294,7 +357,8 @@ def run_ours(args):
            "kernel_ms": {"fit_profile": statistics.mean(t_fit), "simulate": statistics.mean(t_sim),
                          "all_gather": statistics.mean(t_gather) if world > 1 else 0.0},
            "fit_samples": n_samp, "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roof,
-           "cpu_baseline": cpu}
+           "cpu_baseline": cpu,
+           "streaming": streaming_kernels(vt, torch, dev, peaks["hbm_gbs"]) if not args.no_streaming else None}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -1,0 +1,65 @@
+"""Multi-GPU scenario sharding (one process per GPU, torch.distributed).
+
+Scenarios never interact, so a sweep shards with no data-path
+collective. Two modes:
+- weak scaling (bench.py): every rank evaluates its own block of scenarios;
+- strong scaling: one fixed sweep split by a deterministic longest-processing-
+  time (LPT) partition that every rank computes identically from the scenario
+  table — no broadcast.
+The only collective is the all-gather of the 128-byte result records
+(BASELINE north_star), NCCL over NVLink on GPUs (gloo on CPU for tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+RECORD_BYTES = 128
+
+
+def lpt_partition(costs, world: int) -> list[np.ndarray]:
+    """Greedy LPT: scenarios in descending cost go to the least-loaded rank (ties: lowest
+    rank, then lowest index). Returns, per rank, its scenario indices in descending cost."""
+    costs = np.asarray(costs, np.float64)
+    order = np.argsort(-costs, kind="stable")
+    load = np.zeros(world)
+    parts = [[] for _ in range(world)]
+    for i in order:
+        r = int(np.argmin(load))
+        parts[r].append(int(i))
+        load[r] += costs[i]
+    return [np.asarray(p, np.int64) for p in parts]
+
+
+def scenario_costs(w) -> np.ndarray:
+    """Cost estimate per scenario: requests of its trace (each is one route and part of a
+    prefill batch), weighted by the number of decode instances."""
+    lens = np.diff(np.asarray(w.traces.offset, np.int64))
+    nd = np.array([w.layouts[i].n_d for i in np.asarray(w.scen["layout_id"], np.int64)])
+    return lens[np.asarray(w.scen["trace_id"], np.int64)] * (1.0 + 0.05 * nd)
+
+
+def gather_records(local: torch.Tensor, parts: list[np.ndarray], n_total: int, group=None) -> np.ndarray:
+    """All-gather every rank's records ([n_local, 128] uint8, in the order of its part) and
+    return all records in global scenario order (host numpy [n_total, 128] uint8)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    assert local.shape == (len(parts[rank]), RECORD_BYTES)
+    m = max(len(p) for p in parts)
+    pad = torch.zeros((m, RECORD_BYTES), dtype=torch.uint8, device=local.device)
+    pad[: local.shape[0]] = local
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((world * m, RECORD_BYTES), dtype=torch.uint8, device=local.device)
+        dist.all_gather_into_tensor(out, pad, group=group)
+        chunks = out.view(world, m, RECORD_BYTES)
+    else:
+        lst = [torch.empty_like(pad) for _ in range(world)]
+        dist.all_gather(lst, pad, group=group)
+        chunks = torch.stack(lst)
+    host = chunks.cpu().numpy()
+    res = np.zeros((n_total, RECORD_BYTES), np.uint8)
+    for r, p in enumerate(parts):
+        res[p] = host[r, : len(p)]
+    return res

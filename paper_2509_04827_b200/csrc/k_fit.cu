@@ -57,9 +57,20 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
   const size_t gw = (size_t)blockIdx.x * wpb + wib;
   const size_t lo = gw * P.chunk, hi = lo + P.chunk < P.n ? lo + P.chunk : P.n;
   uint64_t invalid = 0;
+  constexpr int PF = 4;  // 32-sample chunks loaded ahead (processed strictly in order)
+  Sample buf[PF];
+#pragma unroll
+  for (int u = 0; u < PF; ++u) buf[u] = load_sample(P, lo + (size_t)u * 32 + lane, lo + (size_t)u * 32 + lane < hi);
+  int slot = 0;
   for (size_t base = lo; base < hi; base += 32) {
-    const size_t i = base + lane;
-    Sample s = load_sample(P, i, i < hi);
+    Sample s = buf[0];
+#pragma unroll
+    for (int u = 0; u + 1 < PF; ++u) buf[u] = buf[u + 1];
+    {
+      const size_t ni = base + (size_t)PF * 32 + lane;
+      buf[PF - 1] = load_sample(P, ni, ni < hi);
+    }
+    (void)slot;
     if (s.cell == -2) invalid++;
     double v[NS];
     if (PASS == 1) {

@@ -10,6 +10,7 @@
 namespace vt {
 
 constexpr int DECIDE_THREADS = 256;
+constexpr int DECIDE_UNROLL = 4;   // items per thread per tile (independent loads in flight)
 
 struct LadderParam {
   int32_t k;

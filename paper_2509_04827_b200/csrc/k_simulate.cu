@@ -40,11 +40,22 @@
 #ifndef VT_BHPF
 #define VT_BHPF 0      // prefetch the bucket the queue head will join at the next START
 #endif
+#ifndef VT_TWO_ENDED
+#define VT_TWO_ENDED 0 // heavy scenarios claimed by the last warp of each CTA (arbiter priority)
+#endif
 #ifndef VT_ITL_FIFO
 #define VT_ITL_FIFO 1  // completion lists deferred before their ITL accounting runs (1..8; 1 measured best)
 #endif
 
 namespace vt {
+
+// ---- scenario groups: SPW scenarios per warp, GS lanes each; every collective is group-masked
+constexpr int GS = 32 / SPW;
+__device__ __forceinline__ int glane() { return (int)(threadIdx.x & (GS - 1)); }
+__device__ __forceinline__ unsigned gbase() { return (threadIdx.x & 31u) & ~(unsigned)(GS - 1); }
+__device__ __forceinline__ unsigned gmask() { return GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << gbase()); }
+__device__ __forceinline__ unsigned gballot(bool p) { return __ballot_sync(gmask(), p) >> gbase(); }
+template <class T> __device__ __forceinline__ T gshfl(T v, int src) { return __shfl_sync(gmask(), v, src, GS); }
 
 struct Node {       // 16 B per request (workspace)
   double tf;        // +t_first if the TTFT SLO was met, -t_first otherwise (t_first > 0)
@@ -372,16 +383,16 @@ __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, doub
 __device__ __forceinline__ int argmin_time(double t, bool valid) {
   const uint64_t b = __double_as_longlong(t);
   const uint32_t hi = valid ? (uint32_t)(b >> 32) : 0xffffffffu;
-  const uint32_t mhi = __reduce_min_sync(FULL, hi);
+  const uint32_t mhi = __reduce_min_sync(gmask(), hi);
   const bool c1 = valid && hi == mhi;
   const uint32_t lo = c1 ? (uint32_t)b : 0xffffffffu;
-  const uint32_t mlo = __reduce_min_sync(FULL, lo);
-  const unsigned m = __ballot_sync(FULL, c1 && lo == mlo);
+  const uint32_t mlo = __reduce_min_sync(gmask(), lo);
+  const unsigned m = gballot(c1 && lo == mlo);
   return m ? ffs0(m) : -1;
 }
 
 __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uint32_t n_req, uint32_t status) {
-  if (lane_id() == 0) {
+  if (glane() == 0) {
     voltana_result R = voltana_result{};
     R.status = status;
     R.n_requests = n_req;
@@ -470,7 +481,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
 }
 
 __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WarpSmem &W) {
-  const int lane = lane_id();
+  const int lane = glane();
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   // ---------------------------------------------------------------- ids and table rows
   if (!(P.trace_id[s] < P.n_traces && P.slo_id[s] < P.n_slos && P.layout_id[s] < P.n_layouts &&
@@ -496,7 +507,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     bool ok = N64 <= P.max_requests && Dur >= 0.0;
     uint64_t tok = 0;
     if (ok) {
-      for (uint64_t i = lane; i < N64; i += 32) {
+      for (uint64_t i = lane; i < N64; i += GS) {
         const uint32_t a = inl[i], b = outl[i];
         const double x = arr[i];
         ok = ok && a >= 1u && a <= 65535u && b >= 1u && b <= P.max_out && x >= 0.0 && x < 1e9;
@@ -504,8 +515,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         tok += (uint64_t)a + b;
       }
     }
-    for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(FULL, tok, o);
-    ok = __all_sync(FULL, ok) && tok <= 0x7fffffffull;
+    for (int o = GS / 2; o > 0; o >>= 1) tok += __shfl_xor_sync(gmask(), tok, o, GS);
+    ok = __all_sync(gmask(), ok) && tok <= 0x7fffffffull;
     if (!ok) {
       write_status(P, s, (uint32_t)N64, VOLTANA_ITEM_E_INPUT);
       return;
@@ -528,7 +539,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
     W.itl_smem = P.itl_smem;
   }
-  for (uint32_t k = lane; k < K; k += 32) {
+  for (uint32_t k = lane; k < K; k += GS) {
     const int lv = GR.level[k];
     W.lad[k] = (uint16_t)lv;
     W.tt[2 * k] = PR.a1[lv];
@@ -538,7 +549,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.mhz[k] = PR.mhz[lv];
   }
   if (P.itl_smem) {
-    for (uint32_t x = lane; x < T * K; x += 32) {
+    for (uint32_t x = lane; x < T * K; x += GS) {
       const uint32_t j = x / K, k = x - j * K;
       const size_t o = (size_t)j * PR.k + GR.level[k];
       W.it[3 * x] = PR.a2[o]; W.it[3 * x + 1] = PR.b2[o]; W.it[3 * x + 2] = PR.c2[o];
@@ -546,25 +557,25 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   {  // coefficient-monotone (non-increasing in f) tables allow the exact binary search (A32)
     bool mt = true, mi = true;
-    for (uint32_t k = lane; k + 1 < K; k += 32)
+    for (uint32_t k = lane; k + 1 < K; k += GS)
       mt = mt && PR.a1[GR.level[k + 1]] <= PR.a1[GR.level[k]] && PR.c1[GR.level[k + 1]] <= PR.c1[GR.level[k]];
-    for (uint32_t x = lane; x < T * (K - 1); x += 32) {
+    for (uint32_t x = lane; x < T * (K - 1); x += GS) {
       const uint32_t j = x / (K - 1), k = x - j * (K - 1);
       const size_t o0 = (size_t)j * PR.k + GR.level[k], o1 = (size_t)j * PR.k + GR.level[k + 1];
       mi = mi && PR.a2[o1] <= PR.a2[o0] && PR.b2[o1] <= PR.b2[o0] && PR.c2[o1] <= PR.c2[o0];
     }
-    mt = __all_sync(FULL, mt);
-    mi = __all_sync(FULL, mi);
+    mt = __all_sync(gmask(), mt);
+    mi = __all_sync(gmask(), mi);
     if (lane == 0) { W.mono_tt = mt; W.mono_it = mi; }
   }
-  __syncwarp();
+  __syncwarp(gmask());
   Node *node = (Node *)slot;
   const uint64_t h0 = P.hash_seed[s];
 
   // ================================================================ PHASE A: prefill lanes
   uint32_t p_head = NIL;
   if (lane < NP) prefill_lane(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
-  __syncwarp();
+  __syncwarp(gmask());
 
   // ================================================================ PHASE B: routing + decode lanes
   const int dl = lane < ND ? lane : 0;
@@ -615,10 +626,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     const int w = argmin_time(ht, hd != NIL);  // next PrefillDone request in (t, p, id) order
     if (w < 0) break;
     if (steps_route > N) { dE.t = 0.0; dE.code = VOLTANA_ITEM_E_INTERNAL; break; }  // watchdog
-    const double t = __shfl_sync(FULL, ht, w);
-    const uint32_t i = __shfl_sync(FULL, hd, w);
-    const uint32_t io = __shfl_sync(FULL, (uint32_t)hn.in | ((uint32_t)hn.out << 16), w);
-    const double tf_i = __shfl_sync(FULL, hn.tf, w);  // signed: carries the TTFT verdict
+    const double t = gshfl(ht, w);
+    const uint32_t i = gshfl(hd, w);
+    const uint32_t io = gshfl((uint32_t)hn.in | ((uint32_t)hn.out << 16), w);
+    const double tf_i = gshfl(hn.tf, w);  // signed: carries the TTFT verdict
     const uint32_t in_i = io & 0xffffu;
     if (lane == w) {                                  // advance that stream; prefetch one further
       hd = hn.next;
@@ -653,21 +664,21 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       }
       const bool act = lane < ND;
       const bool cr = act && faft > fnow;  // A13
-      const int nc = __popc(__ballot_sync(FULL, cr));
-      const int mn = (int)__reduce_min_sync(FULL, (unsigned)fnow);
+      const int nc = __popc(gballot(cr));
+      const int mn = (int)__reduce_min_sync(gmask(), (unsigned)fnow);
       unsigned inset;
       if (nc == 0) {
-        inset = __ballot_sync(FULL, act && fnow == mn);
+        inset = gballot(act && fnow == mn);
         cse = __popc(inset) == 1 ? 1 : 2;
       } else if (nc < ND) {
-        const int mu = (int)__reduce_min_sync(FULL, (unsigned)(act && !cr ? fnow : 0x7fffffff));
-        const int mr = (int)__reduce_min_sync(FULL, (unsigned)(cr ? faft : 0x7fffffff));
+        const int mu = (int)__reduce_min_sync(gmask(), (unsigned)(act && !cr ? fnow : 0x7fffffff));
+        const int mr = (int)__reduce_min_sync(gmask(), (unsigned)(cr ? faft : 0x7fffffff));
         const long long g = (long long)mu - (long long)mr;  // A14, A15
-        if (g <= (long long)delta) { inset = __ballot_sync(FULL, act && !cr && fnow == mu); cse = 3; }
-        else { inset = __ballot_sync(FULL, act && fnow == mn); cse = 4; }
+        if (g <= (long long)delta) { inset = gballot(act && !cr && fnow == mu); cse = 3; }
+        else { inset = gballot(act && fnow == mn); cse = 4; }
       } else {
-        const int ma = (int)__reduce_min_sync(FULL, (unsigned)faft);
-        inset = __ballot_sync(FULL, act && faft == ma);
+        const int ma = (int)__reduce_min_sync(gmask(), (unsigned)faft);
+        inset = gballot(act && faft == ma);
         cse = 5;
       }
       // round robin among the candidate set from the cursor (A17)
@@ -685,7 +696,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   // drain: every decode instance runs to completion, then its deferred ITL accounting
   dec_advance(D, lane, L, W, INF, dE);
   if (lane < ND && !D.dead) itl_drain(D, L, W);
-  __syncwarp();
+  __syncwarp(gmask());
 
   // ================================================================ O9: record
   // first error in (time, prefill before decode, instance) order = the oracle's stop point
@@ -694,8 +705,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const int wd = argmin_time(dE.t, lane < ND && dE.t < INF);
   if (wp >= 0 || wd >= 0) {
     const double tp = wp >= 0 ? W.pa_errt[wp] : INF;
-    const double td = wd >= 0 ? __shfl_sync(FULL, dE.t, wd) : INF;
-    const uint32_t cd = __shfl_sync(FULL, dE.code, wd >= 0 ? wd : 0);
+    const double td = wd >= 0 ? gshfl(dE.t, wd) : INF;
+    const uint32_t cd = gshfl(dE.code, wd >= 0 ? wd : 0);
     write_status(P, s, N, (wp >= 0 && tp <= td) ? W.pa_errc[wp] : cd);
     if (lane < ND)  // leave the wheel clean for the next scenario of this warp
       for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint4(0u, 0u, 0u, 0u);
@@ -703,8 +714,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   double tl = D.tlast;
   if (lane < NP) tl = tl > W.pa_tlast[lane] ? tl : W.pa_tlast[lane];
-  for (int o = 16; o > 0; o >>= 1) {
-    const double x = __shfl_xor_sync(FULL, tl, o);
+  for (int o = GS / 2; o > 0; o >>= 1) {
+    const double x = __shfl_xor_sync(gmask(), tl, o, GS);
     tl = x > tl ? x : tl;
   }
   const double horizon = Dur > tl ? Dur : tl;  // A23
@@ -714,19 +725,19 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   double sitl = 0.0, edb = 0.0, edi = 0.0, bd = 0.0;
 #pragma unroll
   for (int d = 0; d < NI; ++d) {
-    hd_[d] = __shfl_sync(FULL, D.h, d);
+    hd_[d] = gshfl(D.h, d);
     if (d < ND) {
-      sitl = add(sitl, __shfl_sync(FULL, D.sitl, d));
-      topd_[d] = __shfl_sync(FULL, D.top, d);
-      edb = add(edb, div(__shfl_sync(FULL, D.ebusy, d), 1000.0));
-      const double b = __shfl_sync(FULL, D.bms, d);
+      sitl = add(sitl, gshfl(D.sitl, d));
+      topd_[d] = gshfl(D.top, d);
+      edb = add(edb, div(gshfl(D.ebusy, d), 1000.0));
+      const double b = gshfl(D.bms, d);
       edi = add(edi, energy_j(W.p_idle, sub(horizon, b)));
       bd = add(bd, b);
     }
   }
-  const uint32_t c_itl = __reduce_add_sync(FULL, lane < ND ? D.n_itl_ok : 0u);
-  const uint32_t c_both = __reduce_add_sync(FULL, lane < ND ? D.n_both : 0u);
-  const uint32_t c_di = __reduce_add_sync(FULL, lane < ND ? D.iters : 0u);
+  const uint32_t c_itl = __reduce_add_sync(gmask(), lane < ND ? D.n_itl_ok : 0u);
+  const uint32_t c_both = __reduce_add_sync(gmask(), lane < ND ? D.n_both : 0u);
+  const uint32_t c_di = __reduce_add_sync(gmask(), lane < ND ? D.iters : 0u);
   if (lane == 0) {
     voltana_result R = voltana_result{};
     uint64_t hh = splitmix64(h_r);  // A36: route chain, then prefill chains, then decode chains
@@ -759,22 +770,33 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
 __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(const __grid_constant__ SimParams P) {
   extern __shared__ __align__(16) char smem[];
-  const int lane = lane_id();
+  const int lane = glane();
+  const uint32_t grp = (threadIdx.x & 31u) / GS;
   const uint32_t wib = threadIdx.x >> 5;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  if (warp >= P.n_slots) return;
-  char *slot = P.slots + (size_t)warp * P.slot_bytes;
-  uint4 *wheels = P.wheels + (size_t)warp * P.wheel_per_slot;
-  WarpSmem &W = *(WarpSmem *)(smem + (size_t)wib * P.smem_per_warp);
+  const uint32_t sid = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * SPW + grp;  // scenario slot
+  if (sid >= P.n_slots) return;
+  char *slot = P.slots + (size_t)sid * P.slot_bytes;
+  uint4 *wheels = P.wheels + (size_t)sid * P.wheel_per_slot;
+  WarpSmem &W = *(WarpSmem *)(smem + (size_t)(wib * SPW + grp) * P.smem_per_warp);
   for (;;) {
     uint32_t s = 0;
+#if VT_TWO_ENDED
+    // the last warp of each CTA takes the expensive end of the (LPT-ordered) list, the
+    // others the cheap end; counter[0] bounds the total so the two ends never overlap
+    if (lane == 0) {
+      s = atomicAdd(P.counter, 1u);
+      if (s < P.n)
+        s = wib == SIM_THREADS / 32 - 1 ? atomicAdd(P.counter + 1, 1u) : P.n - 1u - atomicAdd(P.counter + 2, 1u);
+    }
+#else
     if (lane == 0) s = atomicAdd(P.counter, 1u);
-    s = __shfl_sync(FULL, s, 0);
+#endif
+    s = gshfl(s, 0);
     if (s >= P.n) break;
     uint64_t t0 = 0;
     if (P.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     run_scenario(P, s, slot, wheels, W);
-    __syncwarp();
+    __syncwarp(gmask());
     if (P.timing && lane == 0) {
       uint64_t t1;
       uint32_t sm;

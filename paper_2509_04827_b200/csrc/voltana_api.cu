@@ -261,7 +261,7 @@ int resident_warps(size_t smem_per_block) {
       cudaGetLastError();
       nb = 1;
     }
-    cached = nb * sm_count() * (SIM_THREADS / 32);
+    cached = nb * sm_count() * (SIM_THREADS / 32) * SPW;  // scenario slots
     cached_smem = smem_per_block;
   }
   return cached;
@@ -274,7 +274,7 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   size_t itl_bytes = (size_t)kmax * tmax * 24;
   L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
   L.smem_per_warp = (sim_smem_fixed() + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
-  L.smem = L.smem_per_warp * (SIM_THREADS / 32);
+  L.smem = L.smem_per_warp * (SIM_THREADS / 32) * SPW;  // per-scenario block x scenarios per CTA
   L.node = align256((size_t)tr->max_requests * 16);
   L.slot = L.node + align256((size_t)tr->max_requests * 4);
   L.slot = L.slot > 256 ? L.slot : 256;
@@ -394,11 +394,12 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   for (int i = 0; i < n_profiles; ++i) P->prof[i] = to_dev(profiles_h[i]);
   cudaStream_t st = (cudaStream_t)stream;
   // scenario counter = 0; every wheel bucket empty (buckets are left clean after use)
-  cudaError_t e = cudaMemsetAsync(P->counter, 0, sizeof(uint32_t), st);
+  cudaError_t e = cudaMemsetAsync(P->counter, 0, 4 * sizeof(uint32_t), st);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(P->wheels, 0, (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint4), st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
-  const int grid = (int)((L.n_slots + (SIM_THREADS / 32) - 1) / (SIM_THREADS / 32));
+  const int per_cta = (SIM_THREADS / 32) * SPW;
+  const int grid = (int)((L.n_slots + per_cta - 1) / per_cta);
   e = launch_sim(*P, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");

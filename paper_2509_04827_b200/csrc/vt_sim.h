@@ -14,6 +14,10 @@ constexpr int SIM_THREADS = 128;      // 4 warps per CTA, one scenario per warp
 #define VT_SIM_MIN_BLOCKS 4
 #endif
 constexpr int SIM_MIN_BLOCKS = VT_SIM_MIN_BLOCKS;  // 4: <= 128 registers, 16 warps per SM
+#ifndef VT_SPW
+#define VT_SPW 1
+#endif
+constexpr int SPW = VT_SPW;           // scenarios per warp (lane groups of 32 / SPW; N_P, N_D <= 8)
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
 size_t sim_smem_fixed();  // per-warp shared-memory block without the staged ITL table
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size

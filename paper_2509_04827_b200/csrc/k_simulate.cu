@@ -43,6 +43,14 @@
 #ifndef VT_TWO_ENDED
 #define VT_TWO_ENDED 0 // heavy scenarios claimed by the last warp of each CTA (arbiter priority)
 #endif
+#ifndef VT_DACC_SMEM
+#define VT_DACC_SMEM 0 // decode-lane accumulators in shared memory instead of registers
+#endif
+#if VT_DACC_SMEM
+#define ACC(f) W.da_##f[d]
+#else
+#define ACC(f) D.f
+#endif
 #ifndef VT_ITL_FIFO
 #define VT_ITL_FIFO 1  // completion lists deferred before their ITL accounting runs (1..8; 1 measured best)
 #endif
@@ -75,6 +83,10 @@ struct WarpSmem {
   double pa_ebusy[NI], pa_bms[NI], pa_top[NI], pa_sttft[NI], pa_tlast[NI], pa_errt[NI];
   uint64_t pa_h[NI];
   uint32_t pa_iters[NI], pa_ttft_ok[NI], pa_itl_ok[NI], pa_both[NI], pa_errc[NI];
+  // ---- decode-lane accumulators (VT_DACC_SMEM)
+  double da_ebusy[NI], da_bms[NI], da_top[NI], da_sitl[NI], da_tlast[NI];
+  uint64_t da_h[NI];
+  uint32_t da_n_itl_ok[NI], da_n_both[NI];
   // ---- scenario constants
   double tau, slo_itl, tgt_itl, slo_ttft, tgt_ttft, p_idle, tdp, uh_p, uh_d;
   const double *a2g, *b2g, *c2g;   // profile ITL tables (when not staged)
@@ -195,7 +207,7 @@ __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
 
 // ITL accounting of deferred completion lists, in completion order (A30, A37); the head
 // nodes of up to four lists are loaded together.
-__device__ void itl_drain(Dec &D, const Lane &L, const WarpSmem &W) {
+__device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d) {
   const double slo = W.slo_itl;
   for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
     Node h4[4];
@@ -209,10 +221,10 @@ __device__ void itl_drain(Dec &D, const Lane &L, const WarpSmem &W) {
       Node nd = h4[u];
       for (uint32_t hop = 0; hop < W.max_steps; ++hop) {
         const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
-        D.sitl = add(D.sitl, itl);
+        ACC(sitl) = add(ACC(sitl), itl);
         const bool ok = itl <= slo;
-        D.n_itl_ok += ok;
-        D.n_both += ok && nd.tf > 0.0;
+        ACC(n_itl_ok) += ok;
+        ACC(n_both) += ok && nd.tf > 0.0;
         if (nd.next == NIL) break;
         nd = L.node[nd.next];
       }
@@ -264,7 +276,7 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
-__device__ void dec_advance(Dec &D, int d, const Lane &L, const WarpSmem &W, double t_lim, Err &E) {
+__device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E) {
   if (D.dead) return;
   const uint32_t nbm = W.nb - 1u;
   for (;;) {
@@ -281,10 +293,10 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, const WarpSmem &W, dou
         L.wheel[D.cur & nbm] = make_uint4(0u, 0u, 0u, 0u);
         L.fid[D.nfifo] = b.x - 1u;
         L.ft[D.nfifo] = tnow;
-        if (++D.nfifo == VT_ITL_FIFO) itl_drain(D, L, W);
+        if (++D.nfifo == VT_ITL_FIFO) itl_drain(D, L, W, d);
       }
       D.busy = false;
-      D.tlast = tnow;
+      ACC(tlast) = tnow;
     } else {
       // idle: the next START happens when the head of the admission queue becomes available
       if (D.qh == NIL) return;
@@ -337,13 +349,13 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, const WarpSmem &W, dou
     int k;
     if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
     else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
-    D.h = fold(D.h, 2, (uint64_t)d, (uint64_t)k, 0);
+    ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
     D.end = add(tnow, dur);
     D.busy = true;
-    D.ebusy = add(D.ebusy, mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
-    D.bms = add(D.bms, dur);
-    if (k == (int)W.K - 1) D.top = add(D.top, dur);
+    ACC(ebusy) = add(ACC(ebusy), mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
+    ACC(bms) = add(ACC(bms), dur);
+    if (k == (int)W.K - 1) ACC(top) = add(ACC(top), dur);
     D.cur = D.iters;
     D.iters += 1u;
     D.bcur = L.wheel[D.cur & nbm];  // final now: read at the END of this iteration
@@ -588,12 +600,18 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   Dec D;
   D.nreq = D.nkv = D.pn = D.pkv = D.iters = D.cur = 0;
   D.qh = D.qt = NIL;
-  D.n_itl_ok = D.n_both = D.nfifo = 0;
+  D.nfifo = 0;
   D.far_h = D.far_hfin = NIL;
   D.busy = false;
   D.dead = !(lane < ND);
-  D.end = D.ebusy = D.bms = D.top = D.sitl = D.tlast = 0.0;
-  D.h = h0;
+  D.end = 0.0;
+  {
+    const int d = lane < ND ? lane : 0;
+    if (lane < ND || !VT_DACC_SMEM) {
+      ACC(ebusy) = 0.0; ACC(bms) = 0.0; ACC(top) = 0.0; ACC(sitl) = 0.0; ACC(tlast) = 0.0;
+      ACC(h) = h0; ACC(n_itl_ok) = 0; ACC(n_both) = 0;
+    }
+  }
   D.bcur = make_uint4(0u, 0u, 0u, 0u);
 #if VT_QCACHE
   D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.in = 0; D.qhn.out = 0;
@@ -695,7 +713,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
   dec_advance(D, lane, L, W, INF, dE);
-  if (lane < ND && !D.dead) itl_drain(D, L, W);
+  if (lane < ND && !D.dead) itl_drain(D, L, W, lane);
   __syncwarp(gmask());
 
   // ================================================================ O9: record
@@ -712,7 +730,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
-  double tl = D.tlast;
+  const int dd = lane < ND ? lane : 0;
+#define LACC(f) (VT_DACC_SMEM ? W.da_##f[dd] : D.f)
+  double tl = lane < ND ? LACC(tlast) : 0.0;
   if (lane < NP) tl = tl > W.pa_tlast[lane] ? tl : W.pa_tlast[lane];
   for (int o = GS / 2; o > 0; o >>= 1) {
     const double x = __shfl_xor_sync(gmask(), tl, o, GS);
@@ -725,18 +745,18 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   double sitl = 0.0, edb = 0.0, edi = 0.0, bd = 0.0;
 #pragma unroll
   for (int d = 0; d < NI; ++d) {
-    hd_[d] = gshfl(D.h, d);
+    hd_[d] = gshfl(LACC(h), d);
     if (d < ND) {
-      sitl = add(sitl, gshfl(D.sitl, d));
-      topd_[d] = gshfl(D.top, d);
-      edb = add(edb, div(gshfl(D.ebusy, d), 1000.0));
-      const double b = gshfl(D.bms, d);
+      sitl = add(sitl, gshfl(LACC(sitl), d));
+      topd_[d] = gshfl(LACC(top), d);
+      edb = add(edb, div(gshfl(LACC(ebusy), d), 1000.0));
+      const double b = gshfl(LACC(bms), d);
       edi = add(edi, energy_j(W.p_idle, sub(horizon, b)));
       bd = add(bd, b);
     }
   }
-  const uint32_t c_itl = __reduce_add_sync(gmask(), lane < ND ? D.n_itl_ok : 0u);
-  const uint32_t c_both = __reduce_add_sync(gmask(), lane < ND ? D.n_both : 0u);
+  const uint32_t c_itl = __reduce_add_sync(gmask(), lane < ND ? LACC(n_itl_ok) : 0u);
+  const uint32_t c_both = __reduce_add_sync(gmask(), lane < ND ? LACC(n_both) : 0u);
   const uint32_t c_di = __reduce_add_sync(gmask(), lane < ND ? D.iters : 0u);
   if (lane == 0) {
     voltana_result R = voltana_result{};

@@ -108,9 +108,98 @@ static uint64_t fold(uint64_t h, uint64_t kind, uint64_t inst, uint64_t level, u
 /* One EcoRoute decision for a request of input length `in`.
  * n[d], kv[d]: effective state of decode instance d (running + routed-but-not-
  * admitted, [A9]). Returns the instance, writes the case (0 = round robin). */
+/* Round robin among a candidate set, starting at the cursor [A17]. */
+static int rr_pick(const int *in_set, int n_d, uint32_t *cursor) {
+  int cnt = 0, best = -1;
+  uint32_t best_dist = UINT32_MAX;
+  for (int d = 0; d < n_d; ++d) {
+    if (!in_set[d]) continue;
+    cnt++;
+    uint32_t dist = (uint32_t)((d - (int)*cursor + n_d) % n_d);
+    if (dist < best_dist) { best_dist = dist; best = d; }
+  }
+  if (cnt >= 2) *cursor = (uint32_t)((best + 1) % n_d);
+  return best;
+}
+
+/* [f1, B1-B3] Energy-scored routing, the north_star's reading of the state-space router:
+ * "scores every (candidate instance, frequency) successor state with the latency and
+ * power(f) models, masks SLO violators and takes the argmin-energy decision". Routing to d
+ * changes only d's per-iteration energy P*T, so the system's energy rate changes by
+ *   score(d) = min over SLO-feasible k of P(k, n+1) * T_itl(k, n+1, kv+in+1)
+ *              - P(k_now, n) * T_itl(k_now, n, kv)        (0 for an empty instance),
+ * k_now = EcoFreq's level of the current effective state [A9-A11]. argmin score over
+ * instances with a feasible k (case 6); none feasible: the fastest top-level successor
+ * (case 7); ties round robin [A17]. */
+static int energy_route(const orc_profile *p, const uint16_t *L, int K, int n_d, const uint64_t *n,
+                        const uint64_t *kv, uint64_t in, double target, uint32_t *cursor, int *case_out) {
+  double score[64], tmax[64];
+  int feas[64], in_set[64], any = 0;
+  for (int d = 0; d < n_d; ++d) {
+    double enow = 0.0;
+    if (n[d] > 0) {
+      int k0 = lowest_feasible_itl(p, L, K, n[d], kv[d], target);
+      enow = busy_power(p, 1, L[k0], n[d]) * predict_itl(p, L[k0], n[d], kv[d]);
+    }
+    double best = 0.0;
+    int found = 0;
+    for (int k = 0; k < K; ++k) {
+      double t = predict_itl(p, L[k], n[d] + 1, kv[d] + in + 1);
+      if (t <= target) {
+        double e = busy_power(p, 1, L[k], n[d] + 1) * t;
+        if (!found || e < best) { best = e; found = 1; }
+      }
+    }
+    feas[d] = found;
+    any |= found;
+    score[d] = best - enow;
+    tmax[d] = predict_itl(p, L[K - 1], n[d] + 1, kv[d] + in + 1);
+  }
+  double m = 0.0;
+  int first = 1;
+  for (int d = 0; d < n_d; ++d) {
+    if (any && !feas[d]) continue;
+    double v = any ? score[d] : tmax[d];
+    if (first || v < m) { m = v; first = 0; }
+  }
+  for (int d = 0; d < n_d; ++d) in_set[d] = any ? (feas[d] && score[d] == m) : (tmax[d] == m);
+  *case_out = any ? 6 : 7;
+  return rr_pick(in_set, n_d, cursor);
+}
+
+/* [f1, B4] Energy-argmin controller: among the levels whose prediction meets the target,
+ * the one with the lowest iteration energy P(k, load) * T(k); ties -> lower level; none
+ * feasible -> top level (A2). Differs from the paper's lowest feasible level only when the
+ * grid spans the bottom of the U-shaped energy curve. */
+static int energy_level_itl(const orc_profile *p, const uint16_t *L, int K, uint64_t n, uint64_t kv,
+                            double target) {
+  int best = -1;
+  double be = 0.0;
+  for (int k = 0; k < K; ++k) {
+    double t = predict_itl(p, L[k], n, kv);
+    if (!(t <= target)) continue;
+    double e = busy_power(p, 1, L[k], n) * t;
+    if (best < 0 || e < be) { best = k; be = e; }
+  }
+  return best < 0 ? K - 1 : best;
+}
+
+static int energy_level_ttft(const orc_profile *p, const uint16_t *L, int K, uint64_t nbt, double budget) {
+  int best = -1;
+  double be = 0.0;
+  for (int k = 0; k < K; ++k) {
+    double t = predict_ttft(p, L[k], nbt);
+    if (!(t <= budget)) continue;
+    double e = busy_power(p, 0, L[k], nbt) * t;
+    if (best < 0 || e < be) { best = k; be = e; }
+  }
+  return best < 0 ? K - 1 : best;
+}
+
 static int ecoroute(const orc_profile *p, const uint16_t *L, int K, int n_d, const uint64_t *n,
                     const uint64_t *kv, uint64_t in, double target, int32_t delta, int policy,
                     uint32_t *cursor, int *case_out) {
+  if (policy == 2 && n_d > 1) return energy_route(p, L, K, n_d, n, kv, in, target, cursor, case_out);
   if (policy == 1 || n_d == 1) { /* SGLang round robin / single instance [A17] */
     int d = (int)*cursor;
     *cursor = (uint32_t)((d + 1) % n_d);
@@ -167,17 +256,8 @@ static int ecoroute(const orc_profile *p, const uint16_t *L, int K, int n_d, con
     cse = 5;
   }
   /* ties: round robin among the candidate set, starting at the cursor [A17] */
-  int cnt = 0, best = -1;
-  uint32_t best_dist = UINT32_MAX;
-  for (int d = 0; d < n_d; ++d) {
-    if (!in_set[d]) continue;
-    cnt++;
-    uint32_t dist = (uint32_t)((d - (int)*cursor + n_d) % n_d);
-    if (dist < best_dist) { best_dist = dist; best = d; }
-  }
-  if (cnt >= 2) *cursor = (uint32_t)((best + 1) % n_d);
   *case_out = cse;
-  return best;
+  return rr_pick(in_set, n_d, cursor);
 }
 
 /* --------------------------------------------------------------- simulator */
@@ -213,7 +293,7 @@ static int validate(const orc_scenario *s) {
     if (k > 0 && s->ladder[k] <= s->ladder[k - 1]) return 0;
   }
   if (s->n_p < 1 || s->n_d < 1 || s->n_p > 64 || s->n_d > 64) return 0;
-  if (s->policy != 0 && s->policy != 1) return 0;
+  if (s->policy < 0 || s->policy > 2 || s->ctrl_mode < 0 || s->ctrl_mode > 1) return 0;
   if (s->max_batch_tokens == 0 || s->kv_capacity == 0) return 0;
   if (s->max_batch_tokens > 0x7fffffffu || s->kv_capacity > 0x7fffffffu) return 0;
   if (!(s->slo_ttft > 0.0) || !(s->slo_itl > 0.0) || !(s->slo_scale > 0.0)) return 0;
@@ -321,7 +401,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         int cse, d;
         if (diag && diag->force_decode) {
           d = diag->force_decode[i];
-          cse = 6;
+          cse = 15; /* forced (test hook), not a routing case */
         } else {
           for (int e = 0; e < ND; ++e) { /* effective state = running + pending [A9] */
             eff_n[e] = D[e].nreq + D[e].pend_n;
@@ -394,7 +474,10 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         k = diag->force_level[force_pos++];
       } else {
         /* EcoFreq: backlog -> max frequency; else lowest feasible */
-        k = backlog ? K - 1 : lowest_feasible_ttft(p, L, K, nbt, prefill_budget(tgt_ttft, wait));
+        double bud = prefill_budget(tgt_ttft, wait);
+        k = backlog ? K - 1
+                    : (s->ctrl_mode == 1 ? energy_level_ttft(p, L, K, nbt, bud)
+                                         : lowest_feasible_ttft(p, L, K, nbt, bud));
       }
       steps_ctrl++;
       I->h = fold(I->h, 1, (uint64_t)q, (uint64_t)k, 0);
@@ -447,7 +530,9 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       if (diag && diag->force_level && force_pos < diag->n_force_level) {
         k = diag->force_level[force_pos++];
       } else {
-        k = backlog ? K - 1 : lowest_feasible_itl(p, L, K, I->nreq, I->nkv, tgt_itl);
+        k = backlog ? K - 1
+                    : (s->ctrl_mode == 1 ? energy_level_itl(p, L, K, I->nreq, I->nkv, tgt_itl)
+                                         : lowest_feasible_itl(p, L, K, I->nreq, I->nkv, tgt_itl));
       }
       steps_ctrl++;
       I->h = fold(I->h, 2, (uint64_t)d, (uint64_t)k, 0);

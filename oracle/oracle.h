@@ -41,7 +41,7 @@ typedef struct {
   uint64_t n;
   double duration_ms;
   double slo_ttft, slo_itl, slo_scale;
-  int32_t n_p, n_d, policy;          /* policy 0 EcoRoute, 1 round-robin */
+  int32_t n_p, n_d, policy;          /* policy 0 EcoRoute, 1 round-robin, 2 energy-scored [B1] */
   uint32_t max_batch_tokens, kv_capacity;
   double kv_transfer_ms;
   int32_t delta_mhz;                 /* INT32_MAX = "large value" */
@@ -49,6 +49,7 @@ typedef struct {
   int32_t K;
   const orc_profile *prof;
   uint64_t hash_seed;
+  int32_t ctrl_mode;                 /* 0 EcoFreq lowest feasible, 1 energy argmin [B4] */
 } orc_scenario;
 
 /* 128-byte per-scenario result record. */
@@ -66,7 +67,7 @@ typedef struct {
   double *req_tdone;       /* [n] last token time                           */
   double *req_itl;         /* [n] mean ITL (0 for out == 1)                 */
   int32_t *req_decode;     /* [n] decode instance, -1 if out == 1           */
-  uint8_t *req_case;       /* [n] routing case 0..5                         */
+  uint8_t *req_case;       /* [n] routing case 0..7 (15 = forced)           */
   uint64_t *iters;         /* [n_p + n_d] iterations started per instance  */
   double *time_le_boundary;/* [n_d] busy ms with n_req <= boundary          */
   double *time_busy;       /* [n_d] busy ms                                 */

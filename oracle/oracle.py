@@ -53,7 +53,8 @@ class OrcScenario(C.Structure):
                 ("slo_scale", C.c_double), ("n_p", C.c_int32), ("n_d", C.c_int32), ("policy", C.c_int32),
                 ("max_batch_tokens", C.c_uint32), ("kv_capacity", C.c_uint32),
                 ("kv_transfer_ms", C.c_double), ("delta_mhz", C.c_int32), ("ladder", vp),
-                ("K", C.c_int32), ("prof", P(OrcProfile)), ("hash_seed", C.c_uint64)]
+                ("K", C.c_int32), ("prof", P(OrcProfile)), ("hash_seed", C.c_uint64),
+                ("ctrl_mode", C.c_int32)]
 
 
 class OrcDiag(C.Structure):
@@ -122,7 +123,7 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                      float(slo.ttft), float(slo.itl), float(slo.scale), int(layout.n_p), int(layout.n_d),
                      int(layout.policy), int(layout.max_batch_tokens), int(layout.kv_capacity),
                      float(layout.kv_transfer_ms), int(layout.delta_mhz), _ptr(ladder), int(len(ladder)),
-                     C.pointer(ph.s), int(hash_seed))
+                     C.pointer(ph.s), int(hash_seed), int(getattr(layout, "ctrl_mode", 0)))
     res = np.zeros(1, RESULT_DTYPE)
     dg = None
     keep = []

@@ -22,5 +22,5 @@ from .traces import TraceSet, lognormal_params, gen_trace, concat_traces  # noqa
 from .profiles import Profile, make_profile  # noqa: F401
 from .workload import (  # noqa: F401
     Slo, Layout, Workload, build_config, single_trace_workload, CONFIG_NAMES,
-    INF_DELTA, POLICY_ECOROUTE, POLICY_RR,
+    INF_DELTA, POLICY_ECOROUTE, POLICY_RR, POLICY_ENERGY, CTRL_ECOFREQ, CTRL_ENERGY,
 )

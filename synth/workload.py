@@ -15,7 +15,8 @@ from .profiles import Profile, make_profile
 from .traces import TraceSet, TraceSpec, concat_traces, gen_trace
 
 INF_DELTA = 2**31 - 1      # "set to a large value"
-POLICY_ECOROUTE, POLICY_RR = 0, 1
+POLICY_ECOROUTE, POLICY_RR, POLICY_ENERGY = 0, 1, 2   # router: EcoRoute, round robin, energy-scored [B1]
+CTRL_ECOFREQ, CTRL_ENERGY = 0, 1                      # controller: lowest feasible, energy argmin [B4]
 CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")
 
 
@@ -35,6 +36,7 @@ class Layout:
     kv_capacity: int = 400000
     kv_transfer_ms: float = 0.0
     delta_mhz: int = 150
+    ctrl_mode: int = CTRL_ECOFREQ
 
 
 @dataclass

@@ -79,12 +79,15 @@ typedef struct {
  *   else prefill: lowest k with a1*load + c1 <= max(0, target - wait)
  *   else decode : lowest k with a2*load + b2*n_kv + c2 (tile of load) <= target
  *   nothing feasible -> K-1 [A2]
+ * mode: 0 = EcoFreq as above; 1 = energy argmin [DESIGN B4]: among the feasible levels the
+ *   one minimising P(k, load) * T(k) (busy power eq:P-f P:187 times the prediction; energy =
+ *   time x power P:74), ties -> lower level; backlog / nothing feasible as above.
  * phase: 0 prefill (load = N_bt; n_kv unused, may be NULL), 1 decode (load = N_req;
  * wait_ms unused, may be NULL). ladder_h: host [k] ascending profile-level indices.
  * out_level[i] = ladder index (0..k-1), 0xFFFF on a contract error; out_status[i] per
  * the VOLTANA_ITEM_* codes (load == 0, decode n_kv < load -> E_CONTRACT).
- * Errors: INVALID_ARG (null/phase/n), LADDER, COVERAGE.                                 */
-voltana_status voltana_control_step(const voltana_profile *prof_h, int phase,
+ * Errors: INVALID_ARG (null/phase/mode/n), LADDER, COVERAGE.                            */
+voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, int mode,
                                     const uint16_t *ladder_h, int k, const uint32_t *load,
                                     const uint32_t *n_kv, const uint32_t *queue_len,
                                     const double *wait_ms, const double *target_ms, size_t n,
@@ -96,10 +99,14 @@ voltana_status voltana_control_step(const voltana_profile *prof_h, int phase,
  *   0), f'(d) = EcoFreq level on (n_req + 1, n_kv + req_in + 1) [A10-A12]; crossed iff
  *   MHz(f') > MHz(f) [A13]; cases (1)-(5) with Delta (inclusive g <= Delta) [A14-A16];
  *   ties go round robin from cursor[i] [A17]. policy 1 = plain round robin.
+ *   policy 2 = energy-scored [DESIGN B1-B3] (the north_star's argmin-energy successor
+ *   state): score(d) = min over feasible k of P(k,n+1)*T(k,n+1,kv+in+1) - P(k_now,n)*T(k_now,n,kv)
+ *   (0 if n = 0), argmin over instances with a feasible k (case 6); none feasible: the
+ *   lowest top-level T after adding (case 7); ties round robin.
  * n_req, n_kv: device [n * n_d] row-major (item, instance) effective states (running +
  * pending). req_in, itl_target_ms: device [n]. cursor: device [n] in/out.
- * out_instance[i] in 0..n_d-1 (0xFFFF on error), out_case[i] 0 = RR, 1..5 = cases.
- * Errors: INVALID_ARG, LADDER, COVERAGE, CONFIG (n_d outside 1..8).                     */
+ * out_instance[i] in 0..n_d-1 (0xFFFF on error), out_case[i] 0 = RR, 1..5 = cases, 6/7 energy.
+ * Errors: INVALID_ARG (policy outside 0..2), LADDER, COVERAGE, CONFIG (n_d outside 1..8).                     */
 voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t *ladder_h,
                                    int k, int n_d, const uint32_t *n_req, const uint32_t *n_kv,
                                    const uint32_t *req_in, const double *itl_target_ms,
@@ -150,11 +157,14 @@ typedef struct {
 
 typedef struct {
   int32_t n_p, n_d;        /* prefill / decode instances, 1..8 (2P2D in P:593)          */
-  int32_t policy;          /* 0 EcoRoute, 1 round robin (SGLang baseline)        */
+  int32_t policy;          /* 0 EcoRoute, 1 round robin (SGLang baseline),
+                              2 energy-scored router [DESIGN B1-B3]                      */
   int32_t delta_mhz;       /* EcoRoute threshold Delta; VOLTANA_DELTA_INF         */
   uint32_t max_batch_tokens; /* prefill batch token budget B (8192) [A6]                 */
   uint32_t kv_capacity;    /* decode KV tokens C (400000) [A20]                          */
   double kv_transfer_ms;   /* tau: 0, or >= 1e-3 [A18]                                    */
+  int32_t ctrl_mode;       /* 0 EcoFreq lowest feasible, 1 energy argmin [B4] */
+  int32_t reserved;        /* 0                                                           */
 } voltana_layout;
 
 typedef struct {

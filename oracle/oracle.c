@@ -619,7 +619,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
 
 /* ------------------------------------------------ single-decision oracles */
 
-int oracle_control_step(const orc_profile *p, int phase, const uint16_t *L, int K,
+int oracle_control_step(const orc_profile *p, int phase, int mode, const uint16_t *L, int K,
                         const uint32_t *load, const uint32_t *n_kv, const uint32_t *queue_len,
                         const double *wait_ms, const double *target_ms, size_t n,
                         uint16_t *out_level, uint8_t *out_status) {
@@ -630,9 +630,11 @@ int oracle_control_step(const orc_profile *p, int phase, const uint16_t *L, int 
     if (queue_len[i] > 0) {
       k = K - 1; /* backlog -> max frequency */
     } else if (phase == 0) {
-      k = lowest_feasible_ttft(p, L, K, load[i], prefill_budget(target_ms[i], wait_ms[i]));
-    } else {
-      k = lowest_feasible_itl(p, L, K, load[i], n_kv[i], target_ms[i]); /* no wait subtraction */
+      double bud = prefill_budget(target_ms[i], wait_ms[i]);
+      k = mode == 1 ? energy_level_ttft(p, L, K, load[i], bud) : lowest_feasible_ttft(p, L, K, load[i], bud);
+    } else { /* no wait subtraction */
+      k = mode == 1 ? energy_level_itl(p, L, K, load[i], n_kv[i], target_ms[i])
+                    : lowest_feasible_itl(p, L, K, load[i], n_kv[i], target_ms[i]);
     }
     out_level[i] = (uint16_t)k;
     out_status[i] = (uint8_t)ORC_OK;

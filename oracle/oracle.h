@@ -94,7 +94,8 @@ typedef struct {
 
 int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag);
 
-int oracle_control_step(const orc_profile *p, int phase, const uint16_t *ladder, int K,
+/* mode 0 EcoFreq (lowest feasible), 1 energy argmin [B4] */
+int oracle_control_step(const orc_profile *p, int phase, int mode, const uint16_t *ladder, int K,
                         const uint32_t *load, const uint32_t *n_kv, const uint32_t *queue_len,
                         const double *wait_ms, const double *target_ms, size_t n,
                         uint16_t *out_level, uint8_t *out_status);

@@ -72,7 +72,7 @@ def lib():
         build()
         L = C.CDLL(_SO)
         L.oracle_simulate.argtypes = [P(OrcScenario), vp, P(OrcDiag)]
-        L.oracle_control_step.argtypes = [P(OrcProfile), C.c_int, vp, C.c_int, vp, vp, vp, vp, vp,
+        L.oracle_control_step.argtypes = [P(OrcProfile), C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp,
                                           C.c_size_t, vp, vp]
         L.oracle_route_batch.argtypes = [P(OrcProfile), vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int32,
                                          C.c_int, vp, C.c_size_t, vp, vp, vp]
@@ -168,7 +168,7 @@ def simulate_workload(w, idx=None) -> np.ndarray:
     return out
 
 
-def control_step(prof, phase, ladder, load, n_kv, queue_len, wait_ms, target_ms):
+def control_step(prof, phase, ladder, load, n_kv, queue_len, wait_ms, target_ms, mode=0):
     ph = _ProfileHandle(prof)
     ladder = np.ascontiguousarray(ladder, np.uint16)
     load = np.ascontiguousarray(load, np.uint32)
@@ -179,7 +179,7 @@ def control_step(prof, phase, ladder, load, n_kv, queue_len, wait_ms, target_ms)
     target_ms = np.ascontiguousarray(target_ms, np.float64)
     lvl = np.zeros(n, np.uint16)
     st = np.zeros(n, np.uint8)
-    lib().oracle_control_step(C.byref(ph.s), int(phase), _ptr(ladder), len(ladder), _ptr(load), _ptr(n_kv),
+    lib().oracle_control_step(C.byref(ph.s), int(phase), int(mode), _ptr(ladder), len(ladder), _ptr(load), _ptr(n_kv),
                               _ptr(queue_len), _ptr(wait_ms), _ptr(target_ms), n, _ptr(lvl), _ptr(st))
     return lvl, st
 

@@ -44,7 +44,8 @@ class Slo(C.Structure):
 
 class Layout(C.Structure):
     _fields_ = [("n_p", C.c_int32), ("n_d", C.c_int32), ("policy", C.c_int32), ("delta_mhz", C.c_int32),
-                ("max_batch_tokens", C.c_uint32), ("kv_capacity", C.c_uint32), ("kv_transfer_ms", C.c_double)]
+                ("max_batch_tokens", C.c_uint32), ("kv_capacity", C.c_uint32), ("kv_transfer_ms", C.c_double),
+                ("ctrl_mode", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Grid(C.Structure):
@@ -89,7 +90,7 @@ def lib():
                           "(the CUDA extension is required, there is no CPU fallback)")
     L = C.CDLL(SO_PATH)
     P = C.POINTER
-    L.voltana_control_step.argtypes = [P(Profile), C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_size_t, vp, vp, vp]
+    L.voltana_control_step.argtypes = [P(Profile), C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_size_t, vp, vp, vp]
     L.voltana_route_batch.argtypes = [P(Profile), vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int32, C.c_int, vp,
                                       C.c_size_t, vp, vp, vp, vp]
     L.voltana_fit_workspace_bytes.argtypes = [C.c_size_t, C.c_int, C.c_int]

@@ -83,14 +83,15 @@ def _ladder(ladder):
 
 # ---------------------------------------------------------------------------- K2
 def control_step(prof: DeviceProfile, phase: int, ladder, load, n_kv, queue_len, wait_ms, target_ms,
-                 stream=None):
-    """EcoFreq per snapshot (voltana_control_step). Returns (level uint16, status uint8) tensors."""
+                 stream=None, mode: int = 0):
+    """EcoFreq per snapshot (voltana_control_step; mode 1 = energy argmin).
+    Returns (level uint16, status uint8) tensors."""
     lad, k = _ladder(ladder)
     n = int(load.numel())
     dev = load.device
     lvl = torch.empty(n, dtype=torch.uint16, device=dev)
     st = torch.empty(n, dtype=torch.uint8, device=dev)
-    check(lib().voltana_control_step(C.byref(prof.struct), int(phase), lad.ctypes.data, k, _p(load), _p(n_kv),
+    check(lib().voltana_control_step(C.byref(prof.struct), int(phase), int(mode), lad.ctypes.data, k, _p(load), _p(n_kv),
                                      _p(queue_len), _p(wait_ms), _p(target_ms), n, _p(lvl), _p(st),
                                      _stream(stream)))
     return lvl, st
@@ -197,7 +198,8 @@ class DeviceWorkload:
         self.slos = (_lib.Slo * len(slos))(*[_lib.Slo(float(s.ttft), float(s.itl), float(s.scale)) for s in slos])
         self.layouts = (_lib.Layout * len(layouts))(*[
             _lib.Layout(int(x.n_p), int(x.n_d), int(x.policy), int(x.delta_mhz), int(x.max_batch_tokens),
-                        int(x.kv_capacity), float(x.kv_transfer_ms)) for x in layouts])
+                        int(x.kv_capacity), float(x.kv_transfer_ms), int(getattr(x, "ctrl_mode", 0)), 0)
+            for x in layouts])
         gs = []
         for g in grids:
             g = np.asarray(g, np.uint16)

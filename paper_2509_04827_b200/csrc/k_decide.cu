@@ -20,12 +20,18 @@ struct SmemTables {
   const int *mhz;     // [K]
 };
 
+// Layout (doubles): [K][2] a1,c1 | [T][K][3] a2,b2,c2 | [K] DYN row of `dyn_phase`; then int [K] MHz.
+__device__ __forceinline__ double *dyn_smem(double *sm, int K, int T) { return sm + 2 * K + 3 * T * K; }
+__device__ __forceinline__ int *mhz_smem(double *sm, int K, int T) { return (int *)(sm + 3 * K + 3 * T * K); }
+
 __device__ void stage_tables(const DevProfile &PR, const LadderParam &LP, bool need_tt, bool need_it,
-                             double *sm, int *smi) {
+                             int dyn_phase, double *sm, int *smi) {
   const int K = LP.k, T = PR.n_tiles;
+  double *dy = dyn_smem(sm, K, T);
   for (int x = threadIdx.x; x < K; x += blockDim.x) {
     int lv = LP.level[x];
     if (need_tt) { sm[2 * x] = PR.a1[lv]; sm[2 * x + 1] = PR.c1[lv]; }
+    if (dyn_phase >= 0) dy[x] = PR.dyn[dyn_phase * PR.k + lv];
     smi[x] = PR.mhz[lv];
   }
   if (need_it) {
@@ -47,15 +53,60 @@ __device__ __forceinline__ int scan_ttft(const double *tt, int K, uint32_t nbt, 
 
 // 64-bit state: the what-if state (n+1, kv+in+1) may exceed 32 bits for caller data.
 // Tile index by shift when the tile width is a power of two (wshift >= 0).
-__device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, int K, uint64_t n,
-                                        uint64_t kv, double target, int wshift) {
+__device__ __forceinline__ const double *itl_row(const double *it, const DevProfile &PR, int K, uint64_t n,
+                                                 int wshift) {
   uint64_t j = wshift >= 0 ? (n - 1u) >> wshift : (n - 1u) / (uint64_t)PR.tile_w;
   if (j > (uint64_t)(PR.n_tiles - 1)) j = (uint64_t)(PR.n_tiles - 1);
-  const double *row = it + 3 * (size_t)j * K;
+  return it + 3 * (size_t)j * K;
+}
+
+__device__ __forceinline__ double itl_eval(const double *row, int k, double dn, double dkv) {
+  return add(add(mul(row[3 * k], dn), mul(row[3 * k + 1], dkv)), row[3 * k + 2]);
+}
+
+__device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, int K, uint64_t n,
+                                        uint64_t kv, double target, int wshift) {
+  const double *row = itl_row(it, PR, K, n, wshift);
   const double dn = (double)n, dkv = (double)kv;
   for (int k = 0; k < K; ++k)
-    if (add(add(mul(row[3 * k], dn), mul(row[3 * k + 1], dkv)), row[3 * k + 2]) <= target) return k;
+    if (itl_eval(row, k, dn, dkv) <= target) return k;
   return K - 1;
+}
+
+// busy power (eq:P-f P:187, A22) for a 64-bit load
+__device__ __forceinline__ double power_at(const DevProfile &PR, int phase, double dyn, uint64_t load) {
+  const double u = div((double)load, add((double)load, PR.uh[phase]));
+  const double w = add(PR.p_idle, mul(u, dyn));
+  return w < PR.tdp ? w : PR.tdp;
+}
+
+// Energy-argmin controller [B4]: lowest P*T among feasible levels, ties -> lower; else K-1.
+__device__ __forceinline__ int energy_ttft(const double *tt, const double *dy, const DevProfile &PR, int K,
+                                           uint32_t nbt, double budget) {
+  int best = -1;
+  double be = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double t = ttft_pred(tt[2 * k], tt[2 * k + 1], nbt);
+    if (!(t <= budget)) continue;
+    const double e = mul(power_at(PR, 0, dy[k], nbt), t);
+    if (best < 0 || e < be) { best = k; be = e; }
+  }
+  return best < 0 ? K - 1 : best;
+}
+
+__device__ __forceinline__ int energy_itl(const double *it, const double *dy, const DevProfile &PR, int K,
+                                          uint64_t n, uint64_t kv, double target, int wshift) {
+  const double *row = itl_row(it, PR, K, n, wshift);
+  const double dn = (double)n, dkv = (double)kv;
+  int best = -1;
+  double be = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double t = itl_eval(row, k, dn, dkv);
+    if (!(t <= target)) continue;
+    const double e = mul(power_at(PR, 1, dy[k], n), t);
+    if (best < 0 || e < be) { best = k; be = e; }
+  }
+  return best < 0 ? K - 1 : best;
 }
 
 // ---------------------------------------------------------------- K2 control_step
@@ -63,9 +114,11 @@ template <int PHASE>
 __global__ void __launch_bounds__(DECIDE_THREADS)
 control_kernel(const __grid_constant__ ControlParams P) {
   extern __shared__ double sm[];
-  int *smi = (int *)(sm + 2 * P.lad.k + 3 * P.prof.n_tiles * P.lad.k);
-  stage_tables(P.prof, P.lad, PHASE == 0, PHASE == 1, sm, smi);
+  int *smi = mhz_smem(sm, P.lad.k, P.prof.n_tiles);
+  stage_tables(P.prof, P.lad, PHASE == 0, PHASE == 1, P.mode == 1 ? PHASE : -1, sm, smi);
   const int K = P.lad.k;
+  const double *dy = dyn_smem(sm, K, P.prof.n_tiles);
+  const bool emode = P.mode == 1;
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
   // DECIDE_UNROLL items per thread per tile, block-strided: every load instruction is
   // coalesced and each thread keeps DECIDE_UNROLL independent loads of each array in flight.
@@ -97,7 +150,7 @@ control_kernel(const __grid_constant__ ControlParams P) {
         } else {
           double b = sub(tgt[u], wait[u]);
           b = b > 0.0 ? b : 0.0;
-          lvl = (uint16_t)scan_ttft(sm, K, load[u], b);
+          lvl = (uint16_t)(emode ? energy_ttft(sm, dy, P.prof, K, load[u], b) : scan_ttft(sm, K, load[u], b));
         }
       } else {
         if (load[u] == 0u || kv[u] < load[u]) {
@@ -105,7 +158,8 @@ control_kernel(const __grid_constant__ ControlParams P) {
         } else if (q[u] > 0u) {
           lvl = (uint16_t)(K - 1);
         } else {
-          lvl = (uint16_t)scan_itl(sm + 2 * K, P.prof, K, load[u], kv[u], tgt[u], wshift);
+          lvl = (uint16_t)(emode ? energy_itl(sm + 2 * K, dy, P.prof, K, load[u], kv[u], tgt[u], wshift)
+                                 : scan_itl(sm + 2 * K, P.prof, K, load[u], kv[u], tgt[u], wshift));
         }
       }
       P.out_level[i] = lvl;
@@ -116,8 +170,8 @@ control_kernel(const __grid_constant__ ControlParams P) {
 
 // ---------------------------------------------------------------- K3 route_batch
 // One EcoRoute decision on caller-given effective states.
-__device__ __forceinline__ void route_item(const RouteParams &P, const double *it, const int *smi, int K, int ND,
-                                           int wshift, uint32_t in, double tgt, uint32_t &cursor,
+__device__ __forceinline__ void route_item(const RouteParams &P, const double *it, const double *dy, const int *smi,
+                                           int K, int ND, int wshift, uint32_t in, double tgt, uint32_t &cursor,
                                            const uint32_t *n, const uint32_t *kv, uint16_t &dsel, uint8_t &cse,
                                            uint8_t &st) {
   bool bad = cursor >= (uint32_t)ND || in == 0u;
@@ -133,6 +187,50 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
     cse = 0;
     return;
   }
+  unsigned inset = 0;
+  if (P.policy == 2) {  // energy-scored router [B1-B3]
+    double score[VOLTANA_MAX_INSTANCES], tmax[VOLTANA_MAX_INSTANCES];
+    bool feas[VOLTANA_MAX_INSTANCES];
+    bool any = false;
+#pragma unroll
+    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) {
+      score[d] = tmax[d] = 0.0;
+      feas[d] = false;
+      if (d >= ND) continue;
+      double enow = 0.0;
+      if (n[d] != 0u) {
+        const double *r0 = itl_row(it, P.prof, K, n[d], wshift);
+        const int k0 = scan_itl(it, P.prof, K, n[d], kv[d], tgt, wshift);        // A10, A11
+        enow = mul(power_at(P.prof, 1, dy[k0], n[d]), itl_eval(r0, k0, (double)n[d], (double)kv[d]));
+      }
+      const uint64_t n1 = (uint64_t)n[d] + 1u, kv1 = (uint64_t)kv[d] + in + 1u;   // A12
+      const double *row = itl_row(it, P.prof, K, n1, wshift);
+      const double dn = (double)n1, dkv = (double)kv1;
+      double best = 0.0, t = 0.0;
+      for (int k = 0; k < K; ++k) {
+        t = itl_eval(row, k, dn, dkv);
+        if (!(t <= tgt)) continue;
+        const double e = mul(power_at(P.prof, 1, dy[k], n1), t);
+        if (!feas[d] || e < best) best = e;
+        feas[d] = true;
+      }
+      tmax[d] = t;
+      score[d] = sub(best, enow);
+      any = any || feas[d];
+    }
+    double m = 0.0;
+    bool first = true;
+#pragma unroll
+    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) {
+      if (d >= ND || (any && !feas[d])) continue;
+      const double v = any ? score[d] : tmax[d];
+      if (first || v < m) { m = v; first = false; }
+    }
+#pragma unroll
+    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d)
+      if (d < ND && (any ? (feas[d] && score[d] == m) : tmax[d] == m)) inset |= 1u << d;
+    cse = any ? 6 : 7;
+  } else {
   int fnow[VOLTANA_MAX_INSTANCES], faft[VOLTANA_MAX_INSTANCES];
   int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
 #pragma unroll
@@ -151,7 +249,6 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
       if (faft[d] < ma) ma = faft[d];
     }
   }
-  unsigned inset = 0;
   if (ncross == 0) {
 #pragma unroll
     for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
@@ -173,6 +270,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
     for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) if (d < ND && faft[d] == ma) inset |= 1u << d;
     cse = 5;
   }
+  }
   const unsigned rot = ((inset >> cursor) | (inset << (ND - cursor))) & ((1u << ND) - 1u);
   const uint32_t d = (cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND;
   dsel = (uint16_t)d;
@@ -183,10 +281,11 @@ template <int ND_MAX>
 __global__ void __launch_bounds__(DECIDE_THREADS)
 route_kernel(const __grid_constant__ RouteParams P) {
   extern __shared__ double sm[];
-  int *smi = (int *)(sm + 2 * P.lad.k + 3 * P.prof.n_tiles * P.lad.k);
-  stage_tables(P.prof, P.lad, false, true, sm, smi);
+  int *smi = mhz_smem(sm, P.lad.k, P.prof.n_tiles);
+  stage_tables(P.prof, P.lad, false, true, P.policy == 2 ? 1 : -1, sm, smi);
   const int K = P.lad.k, ND = P.n_d;
   const double *it = sm + 2 * K;
+  const double *dy = dyn_smem(sm, K, P.prof.n_tiles);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
   constexpr int U = ND_MAX <= 2 ? DECIDE_UNROLL : 2;
   const size_t tile = (size_t)blockDim.x * U;
@@ -218,7 +317,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
       }
       uint16_t dsel;
       uint8_t cse, st;
-      route_item(P, it, smi, K, ND, wshift, inv[u], tg[u], cur[u], nn, kk, dsel, cse, st);
+      route_item(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], nn, kk, dsel, cse, st);
       P.out_instance[i] = dsel;
       P.out_case[i] = cse;
       P.out_status[i] = st;
@@ -228,7 +327,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
 }
 
 size_t decide_smem_bytes(int k, int n_tiles) {
-  return (size_t)(2 * k + 3 * n_tiles * k) * sizeof(double) + (size_t)k * sizeof(int);
+  return (size_t)(3 * k + 3 * n_tiles * k) * sizeof(double) + (size_t)k * sizeof(int);
 }
 
 cudaError_t launch_control(const ControlParams &P, int phase, int grid, size_t smem, cudaStream_t st) {

@@ -93,6 +93,7 @@ struct WarpSmem {
   uint32_t kvcap, max_steps, B, K, T, W, kp, nb;
   int32_t wshift;
   uint32_t itl_smem, mono_tt, mono_it;
+  uint32_t ctrl;                   // layout ctrl_mode: 0 EcoFreq, 1 energy argmin [B4]
   // ---- staged ladder tables
   uint16_t lad[VOLTANA_MAX_LEVELS];
   int32_t mhz[VOLTANA_MAX_LEVELS];
@@ -164,6 +165,41 @@ __device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
   }
   *pred = ttft_at(W, K - 1, nbt);
   return K - 1;
+}
+
+// Energy-argmin controller [B4]: among the levels meeting the target, the lowest busy
+// energy P(k, load) * T(k) (eq:P-f P:187, energy = time x power P:74); ties -> lower level;
+// none feasible -> K-1 (A2). Full scan (the energy curve is not monotone).
+__device__ int energy_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
+  const uint32_t j = tile_j(W, n);
+  const int K = (int)W.K;
+  const double dn = (double)n, dkv = (double)kv;
+  int best = -1;
+  double be = 0.0, bt = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double t = itl_at(W, j, k, dn, dkv);
+    if (!(t <= target)) continue;
+    const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[K + k], n), t);
+    if (best < 0 || e < be) { best = k; be = e; bt = t; }
+  }
+  if (best < 0) { best = K - 1; bt = itl_at(W, j, K - 1, dn, dkv); }
+  *pred = bt;
+  return best;
+}
+
+__device__ int energy_ttft(const WarpSmem &W, uint32_t nbt, double budget, double *pred) {
+  const int K = (int)W.K;
+  int best = -1;
+  double be = 0.0, bt = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const double t = ttft_at(W, k, nbt);
+    if (!(t <= budget)) continue;
+    const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), t);
+    if (best < 0 || e < be) { best = k; be = e; bt = t; }
+  }
+  if (best < 0) { best = K - 1; bt = ttft_at(W, K - 1, nbt); }
+  *pred = bt;
+  return best;
 }
 
 // ------------------------------------------------------------------ decode lanes
@@ -276,6 +312,7 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
+template <bool EN>  // EN: the scenario may use the energy variants [B1-B4]
 __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E) {
   if (D.dead) return;
   const uint32_t nbm = W.nb - 1u;
@@ -348,6 +385,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     double dur;
     int k;
     if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
+    else if (EN && W.ctrl) k = energy_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
     else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
     ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
@@ -403,6 +441,20 @@ __device__ __forceinline__ int argmin_time(double t, bool valid) {
   return m ? ffs0(m) : -1;
 }
 
+// Lanes holding the minimum of a signed double among lanes with `valid` (bitmask, group
+// relative). -0 is folded into +0 first so the set equals the `==` set of the oracle.
+__device__ __forceinline__ unsigned min_set(double v, bool valid) {
+  if (v == 0.0) v = 0.0;
+  const uint64_t b = (uint64_t)__double_as_longlong(v);
+  const uint64_t key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // total order as unsigned
+  const uint32_t hi = valid ? (uint32_t)(key >> 32) : 0xffffffffu;
+  const uint32_t mhi = __reduce_min_sync(gmask(), hi);
+  const bool c1 = valid && hi == mhi;
+  const uint32_t lo = c1 ? (uint32_t)key : 0xffffffffu;
+  const uint32_t mlo = __reduce_min_sync(gmask(), lo);
+  return gballot(c1 && lo == mlo);
+}
+
 __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uint32_t n_req, uint32_t status) {
   if (glane() == 0) {
     voltana_result R = voltana_result{};
@@ -413,6 +465,7 @@ __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uin
 }
 
 // ------------------------------------------------------------------ phase A: prefill lane p
+template <bool EN>
 __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const double *arr, const uint32_t *inl,
                              const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0,
                              uint32_t *head_out) {
@@ -454,6 +507,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
     double dur;
     int k;
     if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
+    else if (EN && W.ctrl) k = energy_ttft(W, nbt, budget, &dur);  // B4
     else k = lowest_ttft(W, nbt, budget, &dur);
     h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
     iters++;
@@ -492,6 +546,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   *head_out = head;
 }
 
+template <bool EN>
 __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WarpSmem &W) {
   const int lane = glane();
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -550,6 +605,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.K = K; W.T = T; W.W = (uint32_t)PR.tile_w; W.kp = (uint32_t)PR.k; W.nb = P.nb;
     W.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
     W.itl_smem = P.itl_smem;
+    W.ctrl = (uint32_t)LY.ctrl_mode;
   }
   for (uint32_t k = lane; k < K; k += GS) {
     const int lv = GR.level[k];
@@ -586,7 +642,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
   // ================================================================ PHASE A: prefill lanes
   uint32_t p_head = NIL;
-  if (lane < NP) prefill_lane(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
+  if (lane < NP) prefill_lane<EN>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
   __syncwarp(gmask());
 
   // ================================================================ PHASE B: routing + decode lanes
@@ -637,7 +693,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   uint32_t c_n = NIL, c_kv = 0;                     // what-if cache: EcoFreq level of the lane's
   int c_lvl = 0;                                    // effective state (c_n, c_kv)
   int ka_last = 0;
+  double c_en = 0.0, en_new = 0.0;                  // energy router: P*T of the cached state / successor
   const bool eco = LY.policy == 0 && ND > 1;
+  const bool ens = EN && LY.policy == 2 && ND > 1;
   const int32_t delta = LY.delta_mhz;
   for (;;) {
     const double ht = fabs(hn.tf);
@@ -656,12 +714,50 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
-      dec_advance(D, lane, L, W, t, dE);
+      dec_advance<EN>(D, lane, L, W, t, dE);
       t_adv = t;
     }
     // ---- O8 EcoRoute
     int dsel, cse;
-    if (!eco) {
+    if (ens) {  // ---- energy-scored router [B1-B3]
+      const bool act = lane < ND;
+      bool feas = false;
+      double score = 0.0, tmax = 0.0;
+      if (act) {
+        const uint32_t n = D.nreq + D.pn, kv = D.nkv + D.pkv;  // A9 effective state
+        double enow = 0.0;
+        if (n != 0u) {
+          if (n != c_n || kv != c_kv) {
+            double pr;
+            const int k0 = lowest_itl(W, n, kv, W.tgt_itl, &pr);  // EcoFreq level now (A10/A11)
+            c_en = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k0], n), pr);
+            c_n = n; c_kv = kv;
+          }
+          enow = c_en;
+        }
+        const uint32_t n1 = n + 1u, kv1 = kv + in_i + 1u;  // A12
+        const uint32_t j = tile_j(W, n1);
+        const double dn = (double)n1, dkv = (double)kv1;
+        double best = 0.0, t = 0.0;
+        for (int k = 0; k < (int)W.K; ++k) {
+          t = itl_at(W, j, k, dn, dkv);
+          if (!(t <= W.tgt_itl)) continue;
+          const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], n1), t);
+          if (!feas) en_new = e;                    // the successor's own EcoFreq-level P*T
+          if (!feas || e < best) best = e;
+          feas = true;
+        }
+        tmax = t;                                   // T at K-1
+        if (!feas) en_new = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + W.K - 1], n1), tmax);
+        score = sub(best, enow);
+      }
+      const bool any = gballot(feas) != 0u;
+      const unsigned inset = any ? min_set(score, feas) : min_set(tmax, act);
+      cse = any ? 6 : 7;
+      const unsigned rot = ((inset >> cursor) | (inset << (ND - (int)cursor))) & ((1u << ND) - 1u);
+      dsel = (int)((cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND);
+      if (__popc(inset) >= 2) cursor = (uint32_t)(dsel + 1) % (uint32_t)ND;
+    } else if (!eco) {
       dsel = (int)cursor;
       cursor = (cursor + 1u) % (uint32_t)ND;
       cse = 0;
@@ -708,11 +804,12 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
     if (lane == dsel) {
       if (eco) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
+      if (ens) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_en = en_new; }
       dec_push(D, L, i, tf_i, in_i, io >> 16);
     }
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
-  dec_advance(D, lane, L, W, INF, dE);
+  dec_advance<EN>(D, lane, L, W, INF, dE);
   if (lane < ND && !D.dead) itl_drain(D, L, W, lane);
   __syncwarp(gmask());
 
@@ -788,6 +885,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
 }
 
+// EN = false: the paper's EcoFreq/EcoRoute/RR only (the default kernel); EN = true also runs
+// the energy variants [B1-B4] (selected on the host when any layout asks for them).
+template <bool EN>
 __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(const __grid_constant__ SimParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = glane();
@@ -815,7 +915,7 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
     if (s >= P.n) break;
     uint64_t t0 = 0;
     if (P.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    run_scenario(P, s, slot, wheels, W);
+    run_scenario<EN>(P, s, slot, wheels, W);
     __syncwarp(gmask());
     if (P.timing && lane == 0) {
       uint64_t t1;
@@ -830,12 +930,15 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
 
 size_t sim_smem_fixed() { return (sizeof(WarpSmem) - sizeof(double) + 15) & ~(size_t)15; }
 
-const void *sim_kernel_ptr() { return (const void *)simulate_kernel; }
+const void *sim_kernel_ptr(bool energy) {
+  return energy ? (const void *)simulate_kernel<true> : (const void *)simulate_kernel<false>;
+}
 
-cudaError_t launch_sim(const SimParams &P, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(simulate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t launch_sim(const SimParams &P, bool energy, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(energy), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  simulate_kernel<<<grid, SIM_THREADS, smem, st>>>(P);
+  if (energy) simulate_kernel<true><<<grid, SIM_THREADS, smem, st>>>(P);
+  else simulate_kernel<false><<<grid, SIM_THREADS, smem, st>>>(P);
   return cudaGetLastError();
 }
 

@@ -100,7 +100,7 @@ int voltana_last_launch_count(void) { return g_launches; }
 void voltana_debug_set_timing(uint64_t *buf) { g_debug_timing = buf; }
 
 // ------------------------------------------------------------------ K2
-voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, const uint16_t *ladder_h, int k,
+voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, int mode, const uint16_t *ladder_h, int k,
                                     const uint32_t *load, const uint32_t *n_kv, const uint32_t *queue_len,
                                     const double *wait_ms, const double *target_ms, size_t n,
                                     uint16_t *out_level, uint8_t *out_status, void *stream) {
@@ -108,6 +108,7 @@ voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, co
   voltana_status s;
   if ((s = check_profile(prof_h, "control_step")) != VOLTANA_OK) return s;
   if (phase != 0 && phase != 1) return fail(VOLTANA_E_INVALID_ARG, "control_step: phase=%d", phase);
+  if (mode != 0 && mode != 1) return fail(VOLTANA_E_INVALID_ARG, "control_step: mode=%d", mode);
   if ((s = check_ladder(ladder_h, k, prof_h->k, "control_step")) != VOLTANA_OK) return s;
   if (n == 0) return ok();
   if (!load || !queue_len || !target_ms || !out_level || !out_status || (phase == 0 && !wait_ms) ||
@@ -120,6 +121,7 @@ voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, co
   for (int i = 0; i < k; ++i) P.lad.level[i] = ladder_h[i];
   P.load = load; P.n_kv = n_kv; P.queue_len = queue_len; P.wait = wait_ms; P.target = target_ms;
   P.n = n; P.out_level = out_level; P.out_status = out_status;
+  P.mode = mode;
   cudaError_t e = launch_control(P, phase, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles),
                                  (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "control_step launch");
@@ -138,7 +140,7 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
   if ((s = check_profile(prof_h, "route_batch")) != VOLTANA_OK) return s;
   if ((s = check_ladder(ladder_h, k, prof_h->k, "route_batch")) != VOLTANA_OK) return s;
   if (n_d < 1 || n_d > VOLTANA_MAX_INSTANCES) return fail(VOLTANA_E_CONFIG, "route_batch: n_d=%d outside 1..8", n_d);
-  if (policy != 0 && policy != 1) return fail(VOLTANA_E_INVALID_ARG, "route_batch: policy=%d", policy);
+  if (policy < 0 || policy > 2) return fail(VOLTANA_E_INVALID_ARG, "route_batch: policy=%d", policy);
   if (n == 0) return ok();
   if (!n_req || !n_kv || !req_in || !itl_target_ms || !cursor || !out_instance || !out_case || !out_status)
     return fail(VOLTANA_E_INVALID_ARG, "route_batch: null array pointer");
@@ -255,8 +257,9 @@ int resident_warps(size_t smem_per_block) {
   std::lock_guard<std::mutex> g(mu);
   if (smem_per_block != cached_smem) {
     int nb = 0;
-    cudaFuncSetAttribute(sim_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_per_block);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(), SIM_THREADS, smem_per_block) !=
+    // both instantiations are built for the same bound (128 registers, 4 CTAs per SM)
+    cudaFuncSetAttribute(sim_kernel_ptr(false), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_per_block);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(false), SIM_THREADS, smem_per_block) !=
             cudaSuccess || nb < 1) {
       cudaGetLastError();
       nb = 1;
@@ -334,7 +337,9 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
     const voltana_layout &x = layouts_h[i];
     if (x.n_p < 1 || x.n_p > VOLTANA_MAX_INSTANCES || x.n_d < 1 || x.n_d > VOLTANA_MAX_INSTANCES)
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d] n_p=%d n_d=%d (1..8)", i, x.n_p, x.n_d);
-    if (x.policy != 0 && x.policy != 1) return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].policy=%d", i, x.policy);
+    if (x.policy < 0 || x.policy > 2) return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].policy=%d", i, x.policy);
+    if (x.ctrl_mode != 0 && x.ctrl_mode != 1)
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].ctrl_mode=%d", i, x.ctrl_mode);
     if (x.max_batch_tokens == 0 || x.max_batch_tokens > 0x7fffffffu || x.kv_capacity == 0 ||
         x.kv_capacity > 0x7fffffffu)
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d] B or C outside 1..2^31-1", i);
@@ -400,7 +405,9 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
   const int per_cta = (SIM_THREADS / 32) * SPW;
   const int grid = (int)((L.n_slots + per_cta - 1) / per_cta);
-  e = launch_sim(*P, grid, L.smem, st);
+  bool energy = false;  // any energy-variant layout [B1-B4] selects that instantiation
+  for (int i = 0; i < n_layouts; ++i) energy = energy || layouts_h[i].policy == 2 || layouts_h[i].ctrl_mode != 0;
+  e = launch_sim(*P, energy, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
   g_launches = 1;

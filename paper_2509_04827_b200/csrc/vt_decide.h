@@ -25,6 +25,7 @@ struct ControlParams {
   size_t n;
   uint16_t *out_level;
   uint8_t *out_status;
+  int32_t mode;        // 0 EcoFreq lowest feasible, 1 energy argmin [B4]
 };
 
 struct RouteParams {

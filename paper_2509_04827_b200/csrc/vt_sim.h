@@ -56,7 +56,7 @@ struct SimParams {
   DevProfile prof[MAX_PROFILES];
 };
 
-const void *sim_kernel_ptr();
-cudaError_t launch_sim(const SimParams &P, int grid, size_t smem, cudaStream_t st);
+const void *sim_kernel_ptr(bool energy);  // energy: the instantiation that also runs [B1-B4]
+cudaError_t launch_sim(const SimParams &P, bool energy, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace vt

@@ -52,13 +52,18 @@ def test_host_validation_errors(vt):
     L = vt.lib()
     p = _profile(vt)
     bad = np.array([2, 1], np.uint16)
-    rc = L.voltana_control_step(C.byref(p), 0, bad.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
+    rc = L.voltana_control_step(C.byref(p), 0, 0, bad.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
     assert rc == 2 and b"strictly increasing" in L.voltana_last_error_detail()
     off = np.array([0, 5], np.uint16)
-    rc = L.voltana_control_step(C.byref(p), 0, off.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
+    rc = L.voltana_control_step(C.byref(p), 0, 0, off.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
     assert rc == 3
-    rc = L.voltana_control_step(C.byref(p), 7, off.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
+    lad = np.array([0, 2], np.uint16)
+    rc = L.voltana_control_step(C.byref(p), 7, 0, lad.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
     assert rc == 1
+    rc = L.voltana_control_step(C.byref(p), 1, 2, lad.ctypes.data, 2, 1, 1, 1, 1, 1, 10, 1, 1, None)
+    assert rc == 1 and b"mode" in L.voltana_last_error_detail()                    # mode outside 0..1
+    rc = L.voltana_route_batch(C.byref(p), lad.ctypes.data, 2, 2, 1, 1, 1, 1, 150, 3, 1, 10, 1, 1, 1, None)
+    assert rc == 1 and b"policy" in L.voltana_last_error_detail()                  # policy outside 0..2
     lad = np.array([0, 2], np.uint16)
     rc = L.voltana_route_batch(C.byref(p), lad.ctypes.data, 2, 9, 1, 1, 1, 1, 150, 0, 1, 10, 1, 1, 1, None)
     assert rc == 5
@@ -87,6 +92,12 @@ def test_simulate_validation_errors(vt):
     assert L.voltana_simulate(*args(lays)) == 5                                     # tau too small
     lays[0].kv_transfer_ms = 0.0
     assert L.voltana_simulate(*args(lays)) == 6                                     # no workspace
+    lays[0].ctrl_mode = 2
+    assert L.voltana_simulate(*args(lays)) == 5                                     # ctrl_mode outside 0..1
+    lays[0].ctrl_mode = 0
+    lays[0].policy = 3
+    assert L.voltana_simulate(*args(lays)) == 5                                     # policy outside 0..2
+    lays[0].policy = 0
     bad_slo = (lib.Slo * 1)(lib.Slo(-1.0, 60.0, 1.0))
     assert L.voltana_simulate(*args(lays, slos=bad_slo)) == 1
     g2 = lib.Grid(2)

@@ -102,14 +102,18 @@ def test_simulate_mixed_default_and_energy(vt, orc):
     """One launch holding default and energy-variant scenarios (the energy instantiation runs
     both); and the default records equal the default-kernel records bit for bit."""
     w0 = synth.build_config("C4", scenarios=list(range(0, 4096, 257)), duration_scale=0.1)
-    w = _energy_variant(w0, POLICY_ENERGY, CTRL_ENERGY, every=2)
+    nl = len(w0.layouts)
+    lays = list(w0.layouts) + [dataclasses.replace(x, policy=POLICY_ENERGY, ctrl_mode=CTRL_ENERGY)
+                               for x in w0.layouts]
+    scen = dict(w0.scen)
+    odd = (np.arange(w0.n) % 2) == 1
+    scen["layout_id"] = np.where(odd, np.asarray(w0.scen["layout_id"]) + nl, w0.scen["layout_id"]).astype(np.uint32)
+    w = dataclasses.replace(w0, layouts=lays, scen=scen)
     g = gpu_records(vt, w)
     compare_records(g, orc.simulate_workload(w))
     g0 = gpu_records(vt, w0)
-    lid = np.asarray(w.scen["layout_id"])
-    keep = (lid % 2) == 1
-    assert keep.any()
-    assert g[keep].tobytes() == g0[keep].tobytes()
+    assert g[~odd].tobytes() == g0[~odd].tobytes()
+    assert g[odd]["decision_hash"].tolist() != g0[odd]["decision_hash"].tolist()
 
 
 def test_simulate_energy_edge_cases(vt, orc):

@@ -165,6 +165,12 @@ typedef struct {
   double kv_transfer_ms;   /* tau: 0, or >= 1e-3 [A18]                                    */
   int32_t ctrl_mode;       /* 0 EcoFreq lowest feasible, 1 energy argmin [B4] */
   int32_t reserved;        /* 0                                                           */
+  double ctrl_interval_ms; /* window control: an instance decides at
+                              an iteration START only when >= this has elapsed since its
+                              previous decision (inclusive); 0 = every iteration [C1]      */
+  double freq_overhead_ms; /* blocking frequency set: an iteration whose
+                              level differs from the running one starts this much later;
+                              0 = non-blocking. Instances start at the top level [C2, C3]  */
 } voltana_layout;
 
 typedef struct {

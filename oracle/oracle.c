@@ -273,6 +273,8 @@ typedef struct {
   uint64_t h;       /* decision-hash chain of this instance's controller decisions [A36] */
   double sum_itl;   /* ITL-mean sum of this instance's completions, completion order [A37] */
   double top;       /* ms at the top level [A37] */
+  int cur;          /* ladder index the GPU runs at [C2] */
+  double last_dec;  /* time of the last controller decision (-inf: none) [C1] */
 } dec_inst;
 
 typedef struct {
@@ -282,6 +284,8 @@ typedef struct {
   uint64_t h;       /* decision-hash chain of this instance's controller decisions [A36] */
   double sum_ttft;  /* TTFT sum of this instance's completions, completion order [A37] */
   double top;       /* ms at the top level [A37] */
+  int cur;          /* ladder index the GPU runs at [C2] */
+  double last_dec;  /* time of the last controller decision (-inf: none) [C1] */
 } pre_inst;
 
 static int validate(const orc_scenario *s) {
@@ -294,6 +298,8 @@ static int validate(const orc_scenario *s) {
   }
   if (s->n_p < 1 || s->n_d < 1 || s->n_p > 64 || s->n_d > 64) return 0;
   if (s->policy < 0 || s->policy > 2 || s->ctrl_mode < 0 || s->ctrl_mode > 1) return 0;
+  if (!(s->ctrl_interval_ms >= 0.0 && s->ctrl_interval_ms < 1e12)) return 0;
+  if (!(s->freq_overhead_ms >= 0.0 && s->freq_overhead_ms < 1e9)) return 0;
   if (s->max_batch_tokens == 0 || s->kv_capacity == 0) return 0;
   if (s->max_batch_tokens > 0x7fffffffu || s->kv_capacity > 0x7fffffffu) return 0;
   if (!(s->slo_ttft > 0.0) || !(s->slo_itl > 0.0) || !(s->slo_scale > 0.0)) return 0;
@@ -336,8 +342,15 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
   uint64_t xq_head = 0, xq_tail = 0;
   uint64_t *eff_n = malloc((size_t)ND * sizeof(uint64_t));
   uint64_t *eff_kv = malloc((size_t)ND * sizeof(uint64_t));
-  for (int q = 0; q < NP; ++q) { P[q].qhead = (uint64_t)q; P[q].h = s->hash_seed; }
+  for (int q = 0; q < NP; ++q) {
+    P[q].qhead = (uint64_t)q;
+    P[q].h = s->hash_seed;
+    P[q].cur = K - 1; /* the GPU starts at the top of the ladder [C2] */
+    P[q].last_dec = -INFINITY;
+  }
   for (int d = 0; d < ND; ++d) {
+    D[d].cur = K - 1;
+    D[d].last_dec = -INFINITY;
     D[d].h = s->hash_seed;
     D[d].cap_run = 16;
     D[d].run = malloc(D[d].cap_run * sizeof(run_entry));
@@ -469,18 +482,27 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       }
       int backlog = id < a; /* requests still waiting after the batch [A5] */
       double wait = t - arr[I->qhead];
-      int k;
-      if (diag && diag->force_level && force_pos < diag->n_force_level) {
-        k = diag->force_level[force_pos++];
-      } else {
-        /* EcoFreq: backlog -> max frequency; else lowest feasible */
-        double bud = prefill_budget(tgt_ttft, wait);
-        k = backlog ? K - 1
-                    : (s->ctrl_mode == 1 ? energy_level_ttft(p, L, K, nbt, bud)
-                                         : lowest_feasible_ttft(p, L, K, nbt, bud));
+      int k = I->cur;
+      /* window gating: decide only when the interval has elapsed since
+       * the last decision, boundary inclusive; interval 0 = every iteration [C1] */
+      if (t - I->last_dec >= s->ctrl_interval_ms) {
+        if (diag && diag->force_level && force_pos < diag->n_force_level) {
+          k = diag->force_level[force_pos++];
+        } else {
+          /* EcoFreq: backlog -> max frequency; else lowest feasible */
+          double bud = prefill_budget(tgt_ttft, wait);
+          k = backlog ? K - 1
+                      : (s->ctrl_mode == 1 ? energy_level_ttft(p, L, K, nbt, bud)
+                                           : lowest_feasible_ttft(p, L, K, nbt, bud));
+        }
+        steps_ctrl++;
+        I->h = fold(I->h, 1, (uint64_t)q, (uint64_t)k, 0);
+        I->last_dec = t;
       }
-      steps_ctrl++;
-      I->h = fold(I->h, 1, (uint64_t)q, (uint64_t)k, 0);
+      /* blocking frequency set: the iteration starts after the overhead when the level
+       * changes [C3] */
+      double t0 = (k != I->cur && s->freq_overhead_ms > 0.0) ? t + s->freq_overhead_ms : t;
+      I->cur = k;
       double dur = predict_ttft(p, L[k], nbt); /* execution time = prediction (noise 0) [A25] */
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
       if (diag && diag->iter_n < diag->iter_cap) {
@@ -488,9 +510,10 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         diag->iter_level[diag->iter_n] = (uint16_t)k;
         diag->iter_dur[diag->iter_n] = dur;
         diag->iter_target[diag->iter_n] = prefill_budget(tgt_ttft, wait);
+        if (diag->iter_start) diag->iter_start[diag->iter_n] = t;
         diag->iter_n++;
       }
-      I->end = t + dur;
+      I->end = t0 + dur;
       I->busy = 1;
       I->bstart = I->qhead;
       I->bcnt = cnt;
@@ -526,16 +549,21 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         continue;
       }
       int backlog = I->q_head < I->q_tail; /* KV-blocked admission queue [A5] */
-      int k;
-      if (diag && diag->force_level && force_pos < diag->n_force_level) {
-        k = diag->force_level[force_pos++];
-      } else {
-        k = backlog ? K - 1
-                    : (s->ctrl_mode == 1 ? energy_level_itl(p, L, K, I->nreq, I->nkv, tgt_itl)
-                                         : lowest_feasible_itl(p, L, K, I->nreq, I->nkv, tgt_itl));
+      int k = I->cur;
+      if (t - I->last_dec >= s->ctrl_interval_ms) { /* window gating [C1] */
+        if (diag && diag->force_level && force_pos < diag->n_force_level) {
+          k = diag->force_level[force_pos++];
+        } else {
+          k = backlog ? K - 1
+                      : (s->ctrl_mode == 1 ? energy_level_itl(p, L, K, I->nreq, I->nkv, tgt_itl)
+                                           : lowest_feasible_itl(p, L, K, I->nreq, I->nkv, tgt_itl));
+        }
+        steps_ctrl++;
+        I->h = fold(I->h, 2, (uint64_t)d, (uint64_t)k, 0);
+        I->last_dec = t;
       }
-      steps_ctrl++;
-      I->h = fold(I->h, 2, (uint64_t)d, (uint64_t)k, 0);
+      double t0 = (k != I->cur && s->freq_overhead_ms > 0.0) ? t + s->freq_overhead_ms : t; /* [C3] */
+      I->cur = k;
       double dur = predict_itl(p, L[k], I->nreq, I->nkv);
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
       if (diag && diag->time_busy) diag->time_busy[d] += dur;
@@ -548,9 +576,10 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         diag->iter_level[diag->iter_n] = (uint16_t)k;
         diag->iter_dur[diag->iter_n] = dur;
         diag->iter_target[diag->iter_n] = tgt_itl;
+        if (diag->iter_start) diag->iter_start[diag->iter_n] = t;
         diag->iter_n++;
       }
-      I->end = t + dur;
+      I->end = t0 + dur;
       I->busy = 1;
       I->ebusy += busy_power(p, 1, L[k], I->nreq) * dur; /* W*ms [A23] */
       I->bms += dur;

@@ -50,6 +50,8 @@ typedef struct {
   const orc_profile *prof;
   uint64_t hash_seed;
   int32_t ctrl_mode;                 /* 0 EcoFreq lowest feasible, 1 energy argmin [B4] */
+  double ctrl_interval_ms;           /* window control: decide when >= this elapsed (0 = every iteration) [C1] */
+  double freq_overhead_ms;           /* blocking frequency-set delay on a level change (0 = non-blocking) [C3] */
 } orc_scenario;
 
 /* 128-byte per-scenario result record. */
@@ -84,6 +86,7 @@ typedef struct {
   uint16_t *iter_level;    /* [iter_cap] ladder index                       */
   double *iter_dur;        /* [iter_cap] duration ms                        */
   double *iter_target;     /* [iter_cap] controller target (budget) ms      */
+  double *iter_start;      /* [iter_cap] START time t (the iteration runs from t + overhead) */
 } orc_diag;
 
 /* status codes (result.status / per-item status) */

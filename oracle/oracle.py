@@ -54,7 +54,7 @@ class OrcScenario(C.Structure):
                 ("max_batch_tokens", C.c_uint32), ("kv_capacity", C.c_uint32),
                 ("kv_transfer_ms", C.c_double), ("delta_mhz", C.c_int32), ("ladder", vp),
                 ("K", C.c_int32), ("prof", P(OrcProfile)), ("hash_seed", C.c_uint64),
-                ("ctrl_mode", C.c_int32)]
+                ("ctrl_mode", C.c_int32), ("ctrl_interval_ms", C.c_double), ("freq_overhead_ms", C.c_double)]
 
 
 class OrcDiag(C.Structure):
@@ -63,7 +63,7 @@ class OrcDiag(C.Structure):
                 ("max_nreq", vp), ("boundary", C.c_uint32), ("force_decode", vp), ("force_level", vp),
                 ("n_force_level", C.c_uint64), ("tokens", vp), ("kv_peak", vp), ("iter_cap", C.c_uint64),
                 ("iter_n", C.c_uint64), ("iter_inst", vp), ("iter_level", vp), ("iter_dur", vp),
-                ("iter_target", vp)]
+                ("iter_target", vp), ("iter_start", vp)]
 
 
 def lib():
@@ -123,7 +123,8 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                      float(slo.ttft), float(slo.itl), float(slo.scale), int(layout.n_p), int(layout.n_d),
                      int(layout.policy), int(layout.max_batch_tokens), int(layout.kv_capacity),
                      float(layout.kv_transfer_ms), int(layout.delta_mhz), _ptr(ladder), int(len(ladder)),
-                     C.pointer(ph.s), int(hash_seed), int(getattr(layout, "ctrl_mode", 0)))
+                     C.pointer(ph.s), int(hash_seed), int(getattr(layout, "ctrl_mode", 0)),
+                     float(getattr(layout, "ctrl_interval_ms", 0.0)), float(getattr(layout, "freq_overhead_ms", 0.0)))
     res = np.zeros(1, RESULT_DTYPE)
     dg = None
     keep = []
@@ -135,7 +136,7 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                  time_busy=np.zeros(nd), max_nreq=np.zeros(nd, np.uint32), tokens=np.zeros(nd, np.uint64),
                  kv_peak=np.zeros(nd, np.uint64), iter_inst=np.zeros(max(iter_cap, 1), np.int32),
                  iter_level=np.zeros(max(iter_cap, 1), np.uint16), iter_dur=np.zeros(max(iter_cap, 1)),
-                 iter_target=np.zeros(max(iter_cap, 1)))
+                 iter_target=np.zeros(max(iter_cap, 1)), iter_start=np.zeros(max(iter_cap, 1)))
         fd = None if force_decode is None else np.ascontiguousarray(force_decode, np.int32)
         fl = None if force_level is None else np.ascontiguousarray(force_level, np.uint16)
         keep += [fd, fl]
@@ -143,13 +144,13 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                                             "iters", "time_le_boundary", "time_busy", "max_nreq")],
                      int(boundary), _ptr(fd), _ptr(fl), 0 if fl is None else len(fl),
                      _ptr(d["tokens"]), _ptr(d["kv_peak"]), int(iter_cap), 0, _ptr(d["iter_inst"]),
-                     _ptr(d["iter_level"]), _ptr(d["iter_dur"]), _ptr(d["iter_target"]))
+                     _ptr(d["iter_level"]), _ptr(d["iter_dur"]), _ptr(d["iter_target"]), _ptr(d["iter_start"]))
         if diag is not None:
             diag.update(d)
     lib().oracle_simulate(C.byref(sc), res.ctypes.data, None if dg is None else C.byref(dg))
     if dg is not None and diag is not None:
         m = int(dg.iter_n)
-        for k in ("iter_inst", "iter_level", "iter_dur", "iter_target"):
+        for k in ("iter_inst", "iter_level", "iter_dur", "iter_target", "iter_start"):
             diag[k] = diag[k][:m]
     del keep
     return res[0]

@@ -198,7 +198,8 @@ class DeviceWorkload:
         self.slos = (_lib.Slo * len(slos))(*[_lib.Slo(float(s.ttft), float(s.itl), float(s.scale)) for s in slos])
         self.layouts = (_lib.Layout * len(layouts))(*[
             _lib.Layout(int(x.n_p), int(x.n_d), int(x.policy), int(x.delta_mhz), int(x.max_batch_tokens),
-                        int(x.kv_capacity), float(x.kv_transfer_ms), int(getattr(x, "ctrl_mode", 0)), 0)
+                        int(x.kv_capacity), float(x.kv_transfer_ms), int(getattr(x, "ctrl_mode", 0)), 0,
+                        float(getattr(x, "ctrl_interval_ms", 0.0)), float(getattr(x, "freq_overhead_ms", 0.0)))
             for x in layouts])
         gs = []
         for g in grids:

@@ -94,6 +94,11 @@ struct WarpSmem {
   int32_t wshift;
   uint32_t itl_smem, mono_tt, mono_it;
   uint32_t ctrl;                   // layout ctrl_mode: 0 EcoFreq, 1 energy argmin [B4]
+  double ctrl_iv, fs_ov;           // window interval, blocking frequency-set overhead [C1-C3]
+  // ---- variant-kernel per-instance controller state [C1-C3]
+  double dl_last[NI];              // decode lane: time of the last decision (-inf: none)
+  uint32_t dl_cur[NI], dl_ndec[NI];  // decode lane: running level, decisions taken
+  uint32_t pa_ndec[NI];            // prefill lane: decisions taken
   // ---- staged ladder tables
   uint16_t lad[VOLTANA_MAX_LEVELS];
   int32_t mhz[VOLTANA_MAX_LEVELS];
@@ -312,7 +317,7 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
-template <bool EN>  // EN: the scenario may use the energy variants [B1-B4]
+template <bool EN>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
 __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E) {
   if (D.dead) return;
   const uint32_t nbm = W.nb - 1u;
@@ -384,12 +389,23 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     }
     double dur;
     int k;
-    if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
-    else if (EN && W.ctrl) k = energy_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
-    else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
-    ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
+    if (EN && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+      k = (int)W.dl_cur[d];
+      dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv);
+    } else {
+      if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
+      else if (EN && W.ctrl) k = energy_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
+      else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
+      ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
+      if (EN) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
+    }
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
-    D.end = add(tnow, dur);
+    double t0 = tnow;
+    if (EN) {  // blocking frequency set on a level change [C3]
+      if (k != (int)W.dl_cur[d] && W.fs_ov > 0.0) t0 = add(tnow, W.fs_ov);
+      W.dl_cur[d] = (uint32_t)k;
+    }
+    D.end = add(t0, dur);
     D.busy = true;
     ACC(ebusy) = add(ACC(ebusy), mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
     ACC(bms) = add(ACC(bms), dur);
@@ -476,6 +492,8 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   const double tgt_ttft = W.tgt_ttft, slo_ttft = W.slo_ttft;
   const uint32_t B = W.B, K = W.K;
   double tfree = 0.0;
+  double last = -INF;             // [C1] time of the last decision
+  uint32_t cur = K - 1u, ndec = 0;  // [C2] running level (starts at the top), decisions
   uint32_t nxt = p, prev = NIL;
   Node pend;
   pend.tf = 0.0; pend.next = NIL; pend.in = 0; pend.out = 0;
@@ -506,13 +524,24 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
     budget = budget > 0.0 ? budget : 0.0;
     double dur;
     int k;
-    if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
-    else if (EN && W.ctrl) k = energy_ttft(W, nbt, budget, &dur);  // B4
-    else k = lowest_ttft(W, nbt, budget, &dur);
-    h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
+    if (EN && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+      k = (int)cur;
+      dur = ttft_at(W, k, nbt);
+    } else {
+      if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
+      else if (EN && W.ctrl) k = energy_ttft(W, nbt, budget, &dur);  // B4
+      else k = lowest_ttft(W, nbt, budget, &dur);
+      h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
+      if (EN) { last = ts; ndec++; }
+    }
     iters++;
     if (!(dur > 0.0)) { errt = ts; errc = VOLTANA_ITEM_E_CONTRACT; break; }
-    const double end = add(ts, dur);
+    double t0 = ts;
+    if (EN) {  // blocking frequency set on a level change [C3]
+      if (k != (int)cur && W.fs_ov > 0.0) t0 = add(ts, W.fs_ov);
+      cur = (uint32_t)k;
+    }
+    const double end = add(t0, dur);
     ebusy = add(ebusy, mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), dur));  // W*ms (A23)
     bms = add(bms, dur);
     if (k == (int)K - 1) top = add(top, dur);
@@ -543,6 +572,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   W.pa_ebusy[p] = ebusy; W.pa_bms[p] = bms; W.pa_top[p] = top; W.pa_sttft[p] = sttft; W.pa_tlast[p] = tlast;
   W.pa_errt[p] = errt; W.pa_errc[p] = errc; W.pa_h[p] = h; W.pa_iters[p] = iters; W.pa_ttft_ok[p] = ttft_ok;
   W.pa_itl_ok[p] = itl_ok; W.pa_both[p] = both;
+  if (EN) W.pa_ndec[p] = ndec;
   *head_out = head;
 }
 
@@ -606,6 +636,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
     W.itl_smem = P.itl_smem;
     W.ctrl = (uint32_t)LY.ctrl_mode;
+    W.ctrl_iv = LY.ctrl_interval_ms;
+    W.fs_ov = LY.freq_overhead_ms;
+  }
+  if (EN && lane < NI) {
+    W.dl_last[lane] = -INF;
+    W.dl_cur[lane] = (uint32_t)GR.k - 1u;  // the GPU starts at the top of the ladder [C2]
+    W.dl_ndec[lane] = 0u;
   }
   for (uint32_t k = lane; k < K; k += GS) {
     const int lv = GR.level[k];
@@ -877,7 +914,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       }
     R.status = 0; R.n_requests = N;
     R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl_p + c_itl; R.n_both_ok = c_both_p + c_both; R.prefill_iters = c_pi;
-    R.steps_ctrl = (uint64_t)c_pi + c_di; R.steps_route = steps_route; R.decision_hash = hh;
+    uint64_t sc = (uint64_t)c_pi + c_di;  // one decision per iteration ...
+    if (EN) {                            // ... unless window control skipped some [C1]
+      sc = 0;
+      for (int q = 0; q < NP; ++q) sc += W.pa_ndec[q];
+      for (int d = 0; d < ND; ++d) sc += W.dl_ndec[d];
+    }
+    R.steps_ctrl = sc; R.steps_route = steps_route; R.decision_hash = hh;
     R.sum_ttft_ms = sttft; R.sum_itl_mean_ms = sitl;
     R.e_prefill_busy_j = epb; R.e_prefill_idle_j = epi; R.e_decode_busy_j = edb; R.e_decode_idle_j = edi;
     R.busy_ms_prefill = bp; R.busy_ms_decode = bd; R.top_level_ms = top; R.horizon_ms = horizon;

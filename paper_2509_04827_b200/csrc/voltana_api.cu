@@ -340,6 +340,10 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
     if (x.policy < 0 || x.policy > 2) return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].policy=%d", i, x.policy);
     if (x.ctrl_mode != 0 && x.ctrl_mode != 1)
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].ctrl_mode=%d", i, x.ctrl_mode);
+    if (!(x.ctrl_interval_ms >= 0.0 && x.ctrl_interval_ms < 1e12))
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].ctrl_interval_ms must be in [0, 1e12)", i);
+    if (!(x.freq_overhead_ms >= 0.0 && x.freq_overhead_ms < 1e9))
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].freq_overhead_ms must be in [0, 1e9)", i);
     if (x.max_batch_tokens == 0 || x.max_batch_tokens > 0x7fffffffu || x.kv_capacity == 0 ||
         x.kv_capacity > 0x7fffffffu)
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d] B or C outside 1..2^31-1", i);
@@ -405,8 +409,11 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
   const int per_cta = (SIM_THREADS / 32) * SPW;
   const int grid = (int)((L.n_slots + per_cta - 1) / per_cta);
-  bool energy = false;  // any energy-variant layout [B1-B4] selects that instantiation
-  for (int i = 0; i < n_layouts; ++i) energy = energy || layouts_h[i].policy == 2 || layouts_h[i].ctrl_mode != 0;
+  bool energy = false;  // any variant layout [B1-B4, C1-C3] selects that instantiation
+  for (int i = 0; i < n_layouts; ++i) {
+    const voltana_layout &x = layouts_h[i];
+    energy = energy || x.policy == 2 || x.ctrl_mode != 0 || x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0;
+  }
   e = launch_sim(*P, energy, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");

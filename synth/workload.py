@@ -37,6 +37,8 @@ class Layout:
     kv_transfer_ms: float = 0.0
     delta_mhz: int = 150
     ctrl_mode: int = CTRL_ECOFREQ
+    ctrl_interval_ms: float = 0.0      # window control: 0 = per-iteration
+    freq_overhead_ms: float = 0.0      # blocking frequency set on a change (~50 ms nvidia-smi, ~3 ms pyNVML)
 
 
 @dataclass

@@ -98,6 +98,12 @@ def test_simulate_validation_errors(vt):
     lays[0].policy = 3
     assert L.voltana_simulate(*args(lays)) == 5                                     # policy outside 0..2
     lays[0].policy = 0
+    lays[0].ctrl_interval_ms = -1.0
+    assert L.voltana_simulate(*args(lays)) == 5                                     # negative window
+    lays[0].ctrl_interval_ms = 0.0
+    lays[0].freq_overhead_ms = float("nan")
+    assert L.voltana_simulate(*args(lays)) == 5                                     # NaN overhead
+    lays[0].freq_overhead_ms = 0.0
     bad_slo = (lib.Slo * 1)(lib.Slo(-1.0, 60.0, 1.0))
     assert L.voltana_simulate(*args(lays, slos=bad_slo)) == 1
     g2 = lib.Grid(2)

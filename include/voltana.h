@@ -171,6 +171,13 @@ typedef struct {
   double freq_overhead_ms; /* blocking frequency set: an iteration whose
                               level differs from the running one starts this much later;
                               0 = non-blocking. Instances start at the top level [C2, C3]  */
+  const double *exec_noise; /* device [noise_len] execution-noise factors or NULL (S:401,
+                              S:469): iteration j of instance i (prefill p: i = p, decode
+                              d: i = n_p + d) runs prediction x exec_noise[splitmix64(
+                              hash_seed ^ 0xD1B54A32D192ED03 ^ i<<40 ^ j) & (noise_len-1)];
+                              a factor outside (0, 1e6] sets status E_INPUT [D1, D2]      */
+  uint32_t noise_len;      /* power of two when exec_noise != NULL                        */
+  uint32_t reserved2;      /* 0                                                           */
 } voltana_layout;
 
 typedef struct {

@@ -99,6 +99,14 @@ static uint64_t splitmix64(uint64_t x) {
 /* h <- (h ^ (kind<<48 ^ instance<<32 ^ level<<16 ^ case)) * phi64 [A36]: for a fixed
  * decision word the step is a bijection of h, so two decision sequences that differ in
  * one decision keep differing; the chains are mixed with splitmix64 at the end. */
+/* [D2] execution-noise factor of iteration j of instance `inst` (prefill q, decode N_P + d):
+ * a counter-based index into the host-drawn factor table, so both sides read the same
+ * factor without evaluating a transcendental. */
+static double noise_factor(const orc_scenario *s, uint64_t inst, uint64_t j) {
+  uint64_t x = s->hash_seed ^ 0xD1B54A32D192ED03ull ^ (inst << 40) ^ j;
+  return s->noise[splitmix64(x) & (s->noise_len - 1)];
+}
+
 static uint64_t fold(uint64_t h, uint64_t kind, uint64_t inst, uint64_t level, uint64_t cse) {
   return (h ^ ((kind << 48) ^ (inst << 32) ^ (level << 16) ^ cse)) * 0x9E3779B97F4A7C15ull;
 }
@@ -300,6 +308,7 @@ static int validate(const orc_scenario *s) {
   if (s->policy < 0 || s->policy > 2 || s->ctrl_mode < 0 || s->ctrl_mode > 1) return 0;
   if (!(s->ctrl_interval_ms >= 0.0 && s->ctrl_interval_ms < 1e12)) return 0;
   if (!(s->freq_overhead_ms >= 0.0 && s->freq_overhead_ms < 1e9)) return 0;
+  if (s->noise && (s->noise_len == 0 || (s->noise_len & (s->noise_len - 1)) != 0)) return 0;
   if (s->max_batch_tokens == 0 || s->kv_capacity == 0) return 0;
   if (s->max_batch_tokens > 0x7fffffffu || s->kv_capacity > 0x7fffffffu) return 0;
   if (!(s->slo_ttft > 0.0) || !(s->slo_itl > 0.0) || !(s->slo_scale > 0.0)) return 0;
@@ -505,6 +514,11 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       I->cur = k;
       double dur = predict_ttft(p, L[k], nbt); /* execution time = prediction (noise 0) [A25] */
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
+      if (s->noise) { /* true time = prediction x lognormal factor [D1] */
+        double e = noise_factor(s, (uint64_t)q, I->iters);
+        if (!(e > 0.0 && e <= 1e6)) { status = ORC_E_INPUT; break; }
+        dur = dur * e;
+      }
       if (diag && diag->iter_n < diag->iter_cap) {
         diag->iter_inst[diag->iter_n] = q;
         diag->iter_level[diag->iter_n] = (uint16_t)k;
@@ -566,6 +580,11 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       I->cur = k;
       double dur = predict_itl(p, L[k], I->nreq, I->nkv);
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
+      if (s->noise) { /* [D1] */
+        double e = noise_factor(s, (uint64_t)(NP + d), I->iters);
+        if (!(e > 0.0 && e <= 1e6)) { status = ORC_E_INPUT; break; }
+        dur = dur * e;
+      }
       if (diag && diag->time_busy) diag->time_busy[d] += dur;
       if (diag && diag->time_le_boundary && I->nreq <= diag->boundary) diag->time_le_boundary[d] += dur;
       if (diag && diag->max_nreq && I->nreq > diag->max_nreq[d]) diag->max_nreq[d] = (uint32_t)I->nreq;

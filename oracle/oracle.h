@@ -52,6 +52,8 @@ typedef struct {
   int32_t ctrl_mode;                 /* 0 EcoFreq lowest feasible, 1 energy argmin [B4] */
   double ctrl_interval_ms;           /* window control: decide when >= this elapsed (0 = every iteration) [C1] */
   double freq_overhead_ms;           /* blocking frequency-set delay on a level change (0 = non-blocking) [C3] */
+  const double *noise;               /* [noise_len] execution-noise factors, NULL = none [D1, D2] */
+  uint64_t noise_len;                /* power of two */
 } orc_scenario;
 
 /* 128-byte per-scenario result record. */

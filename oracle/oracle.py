@@ -54,7 +54,8 @@ class OrcScenario(C.Structure):
                 ("max_batch_tokens", C.c_uint32), ("kv_capacity", C.c_uint32),
                 ("kv_transfer_ms", C.c_double), ("delta_mhz", C.c_int32), ("ladder", vp),
                 ("K", C.c_int32), ("prof", P(OrcProfile)), ("hash_seed", C.c_uint64),
-                ("ctrl_mode", C.c_int32), ("ctrl_interval_ms", C.c_double), ("freq_overhead_ms", C.c_double)]
+                ("ctrl_mode", C.c_int32), ("ctrl_interval_ms", C.c_double), ("freq_overhead_ms", C.c_double),
+                ("noise", vp), ("noise_len", C.c_uint64)]
 
 
 class OrcDiag(C.Structure):
@@ -119,12 +120,15 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
     ladder = np.ascontiguousarray(ladder, np.uint16)
     ph = _ProfileHandle(prof)
     n = len(arrival)
+    noise = getattr(layout, "exec_noise", None)
+    noise = None if noise is None else np.ascontiguousarray(noise, np.float64)
     sc = OrcScenario(_ptr(arrival), _ptr(in_len), _ptr(out_len), n, float(duration_ms),
                      float(slo.ttft), float(slo.itl), float(slo.scale), int(layout.n_p), int(layout.n_d),
                      int(layout.policy), int(layout.max_batch_tokens), int(layout.kv_capacity),
                      float(layout.kv_transfer_ms), int(layout.delta_mhz), _ptr(ladder), int(len(ladder)),
                      C.pointer(ph.s), int(hash_seed), int(getattr(layout, "ctrl_mode", 0)),
-                     float(getattr(layout, "ctrl_interval_ms", 0.0)), float(getattr(layout, "freq_overhead_ms", 0.0)))
+                     float(getattr(layout, "ctrl_interval_ms", 0.0)), float(getattr(layout, "freq_overhead_ms", 0.0)),
+                     _ptr(noise), 0 if noise is None else len(noise))
     res = np.zeros(1, RESULT_DTYPE)
     dg = None
     keep = []

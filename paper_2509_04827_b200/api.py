@@ -196,11 +196,15 @@ class DeviceWorkload:
         self.sc["hash_seed"] = self._up(np.asarray(sc["hash_seed"], np.uint64), torch.uint64)
         self.profiles = [p if isinstance(p, DeviceProfile) else DeviceProfile(p, self.device) for p in profiles]
         self.slos = (_lib.Slo * len(slos))(*[_lib.Slo(float(s.ttft), float(s.itl), float(s.scale)) for s in slos])
+        # execution-noise factor tables (D1, D2) live on the device for the workload's lifetime
+        self.noise = [None if getattr(x, "exec_noise", None) is None
+                      else self._up(np.ascontiguousarray(x.exec_noise, np.float64), torch.float64) for x in layouts]
         self.layouts = (_lib.Layout * len(layouts))(*[
             _lib.Layout(int(x.n_p), int(x.n_d), int(x.policy), int(x.delta_mhz), int(x.max_batch_tokens),
                         int(x.kv_capacity), float(x.kv_transfer_ms), int(getattr(x, "ctrl_mode", 0)), 0,
-                        float(getattr(x, "ctrl_interval_ms", 0.0)), float(getattr(x, "freq_overhead_ms", 0.0)))
-            for x in layouts])
+                        float(getattr(x, "ctrl_interval_ms", 0.0)), float(getattr(x, "freq_overhead_ms", 0.0)),
+                        None if nz is None else nz.data_ptr(), 0 if nz is None else int(nz.numel()), 0)
+            for x, nz in zip(layouts, self.noise)])
         gs = []
         for g in grids:
             g = np.asarray(g, np.uint16)

@@ -95,6 +95,9 @@ struct WarpSmem {
   uint32_t itl_smem, mono_tt, mono_it;
   uint32_t ctrl;                   // layout ctrl_mode: 0 EcoFreq, 1 energy argmin [B4]
   double ctrl_iv, fs_ov;           // window interval, blocking frequency-set overhead [C1-C3]
+  const double *noise;             // execution-noise factor table or NULL [D1, D2]
+  uint32_t noise_mask, np;         // np: N_P (decode instance d is noise instance N_P + d)
+  uint64_t seed;                   // scenario hash seed (noise index)
   // ---- variant-kernel per-instance controller state [C1-C3]
   double dl_last[NI];              // decode lane: time of the last decision (-inf: none)
   uint32_t dl_cur[NI], dl_ndec[NI];  // decode lane: running level, decisions taken
@@ -205,6 +208,13 @@ __device__ int energy_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
   if (best < 0) { best = K - 1; bt = ttft_at(W, K - 1, nbt); }
   *pred = bt;
   return best;
+}
+
+// [D2] execution-noise factor of iteration j of instance inst: counter-based index into the
+// host-drawn table (no transcendental on either side).
+__device__ __forceinline__ double noise_at(const WarpSmem &W, uint64_t inst, uint64_t j) {
+  const uint64_t x = W.seed ^ 0xD1B54A32D192ED03ull ^ (inst << 40) ^ j;
+  return __ldg(W.noise + (splitmix64(x) & W.noise_mask));
 }
 
 // ------------------------------------------------------------------ decode lanes
@@ -400,6 +410,11 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
       if (EN) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
     }
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
+    if (EN && W.noise) {  // [D1]
+      const double e = noise_at(W, (uint64_t)W.np + d, D.iters);
+      if (!(e > 0.0 && e <= 1e6)) { E.t = tnow; E.code = VOLTANA_ITEM_E_INPUT; D.dead = true; return; }
+      dur = mul(dur, e);
+    }
     double t0 = tnow;
     if (EN) {  // blocking frequency set on a level change [C3]
       if (k != (int)W.dl_cur[d] && W.fs_ov > 0.0) t0 = add(tnow, W.fs_ov);
@@ -534,8 +549,13 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
       h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
       if (EN) { last = ts; ndec++; }
     }
-    iters++;
+    const uint32_t jit = iters++;
     if (!(dur > 0.0)) { errt = ts; errc = VOLTANA_ITEM_E_CONTRACT; break; }
+    if (EN && W.noise) {  // true time = prediction x lognormal factor [D1]
+      const double e = noise_at(W, p, jit);
+      if (!(e > 0.0 && e <= 1e6)) { errt = ts; errc = VOLTANA_ITEM_E_INPUT; break; }
+      dur = mul(dur, e);
+    }
     double t0 = ts;
     if (EN) {  // blocking frequency set on a level change [C3]
       if (k != (int)cur && W.fs_ov > 0.0) t0 = add(ts, W.fs_ov);
@@ -638,6 +658,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.ctrl = (uint32_t)LY.ctrl_mode;
     W.ctrl_iv = LY.ctrl_interval_ms;
     W.fs_ov = LY.freq_overhead_ms;
+    W.noise = LY.exec_noise;
+    W.noise_mask = LY.noise_len - 1u;
+    W.seed = P.hash_seed[s];
+    W.np = (uint32_t)NP;
   }
   if (EN && lane < NI) {
     W.dl_last[lane] = -INF;

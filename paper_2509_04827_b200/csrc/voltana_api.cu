@@ -344,6 +344,8 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].ctrl_interval_ms must be in [0, 1e12)", i);
     if (!(x.freq_overhead_ms >= 0.0 && x.freq_overhead_ms < 1e9))
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].freq_overhead_ms must be in [0, 1e9)", i);
+    if (x.exec_noise && (x.noise_len == 0 || (x.noise_len & (x.noise_len - 1)) != 0))
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].noise_len=%u must be a power of two", i, x.noise_len);
     if (x.max_batch_tokens == 0 || x.max_batch_tokens > 0x7fffffffu || x.kv_capacity == 0 ||
         x.kv_capacity > 0x7fffffffu)
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d] B or C outside 1..2^31-1", i);
@@ -409,10 +411,11 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
   const int per_cta = (SIM_THREADS / 32) * SPW;
   const int grid = (int)((L.n_slots + per_cta - 1) / per_cta);
-  bool energy = false;  // any variant layout [B1-B4, C1-C3] selects that instantiation
+  bool energy = false;  // any variant layout [B1-B4, C1-C3, D1-D2] selects that instantiation
   for (int i = 0; i < n_layouts; ++i) {
     const voltana_layout &x = layouts_h[i];
-    energy = energy || x.policy == 2 || x.ctrl_mode != 0 || x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0;
+    energy = energy || x.policy == 2 || x.ctrl_mode != 0 || x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 ||
+             x.exec_noise != nullptr;
   }
   e = launch_sim(*P, energy, grid, L.smem, st);
   delete P;

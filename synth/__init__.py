@@ -20,6 +20,7 @@ Recipe (DESIGN.md "Input recipe"):
 
 from .traces import TraceSet, lognormal_params, gen_trace, concat_traces  # noqa: F401
 from .profiles import Profile, make_profile  # noqa: F401
+from .noise import exec_noise_table  # noqa: F401
 from .workload import (  # noqa: F401
     Slo, Layout, Workload, build_config, single_trace_workload, CONFIG_NAMES,
     INF_DELTA, POLICY_ECOROUTE, POLICY_RR, POLICY_ENERGY, CTRL_ECOFREQ, CTRL_ENERGY,

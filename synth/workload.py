@@ -39,6 +39,7 @@ class Layout:
     ctrl_mode: int = CTRL_ECOFREQ
     ctrl_interval_ms: float = 0.0      # window control: 0 = per-iteration
     freq_overhead_ms: float = 0.0      # blocking frequency set on a change (~50 ms nvidia-smi, ~3 ms pyNVML)
+    exec_noise: object = field(default=None, compare=False, repr=False)  # f64 factor table (noise.py), None = noiseless
 
 
 @dataclass

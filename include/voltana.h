@@ -205,7 +205,7 @@ typedef struct {            /* device arrays [n]                                
 
 typedef struct {            /* 128-byte per-scenario record                             */
   uint32_t status, n_requests, n_ttft_ok, n_itl_ok, n_both_ok;
-  uint32_t prefill_iters;   /* prefill batches started (the rest of steps_ctrl are decode iterations) */
+  uint32_t prefill_iters;   /* prefill batches started                                  */
   uint64_t steps_ctrl, steps_route, decision_hash;
   double sum_ttft_ms, sum_itl_mean_ms, e_prefill_busy_j, e_prefill_idle_j, e_decode_busy_j,
       e_decode_idle_j, busy_ms_prefill, busy_ms_decode, top_level_ms, horizon_ms;
@@ -220,6 +220,53 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
                                 const voltana_profile *profiles_h, int n_profiles,
                                 const voltana_scenarios *scen_h, size_t n, voltana_result *out,
                                 void *workspace, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------------------------------
+ * voltana_simulate_ex — voltana_simulate plus optional per-request records and per-instance
+ * iteration time series ("time series (frequency, n_req, n_kv per
+ * instance at event granularity)"; DESIGN E1-E3). outputs_h == NULL: same as
+ * voltana_simulate. All output pointers are device pointers; a group is off when its
+ * offset array is NULL. Contents for a scenario with status != 0 are unspecified.
+ *
+ * Per-request group (req_offset != NULL): scenario i writes request r of its trace (trace
+ * order) at index req_offset[i] + r; an empty range [req_offset[i], req_offset[i+1]) skips
+ * the scenario, any other length than the trace's request count sets status E_INPUT.
+ *   req_tfirst  first-token time = prefill end (ms); req_tdone last-token time (= tfirst
+ *   when out == 1); req_itl mean inter-token latency (0 when out == 1, A30);
+ *   req_decode decode instance, req_case routing case 0..7 (0xFF when out == 1).
+ * Iteration group (iter_offset != NULL): instance u of scenario i (prefill p: u = p, decode
+ * d: u = n_p + d) writes its j-th started iteration at iters[iter_offset[i] + u*iter_cap + j]
+ * for j < iter_cap and its total iteration count at iter_count[iter_offset[i]/iter_cap + u];
+ * iter_offset[i] must be a multiple of iter_cap with room for n_p + n_d instances.        */
+typedef struct {           /* 32-byte iteration record                                   */
+  double t_start;          /* START time t, ms (the iteration runs from t + overhead, C3) */
+  double dur_ms;           /* true duration = prediction x noise factor (D1)              */
+  uint32_t load;           /* N_bt (prefill) or N_req (decode) at START                   */
+  uint32_t n_kv;           /* N_kv at START (decode), 0 (prefill)                         */
+  uint16_t level;          /* ladder index                                                */
+  uint8_t flags;           /* bit0 controller decision taken (C1), bit1 overhead paid (C3),
+                              bit2 backlog (A5)                                            */
+  uint8_t reserved[5];
+} voltana_iteration;
+
+typedef struct {
+  const uint64_t *req_offset;  /* [n + 1] or NULL                                         */
+  double *req_tfirst, *req_tdone, *req_itl;
+  uint8_t *req_decode, *req_case;
+  const uint64_t *iter_offset; /* [n] or NULL                                             */
+  voltana_iteration *iters;
+  uint32_t *iter_count;
+  uint32_t iter_cap;           /* >= 1                                                    */
+  uint32_t reserved;
+} voltana_outputs;
+
+voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana_slo *slos_h,
+                                   int n_slos, const voltana_layout *layouts_h, int n_layouts,
+                                   const voltana_grid *grids_h, int n_grids,
+                                   const voltana_profile *profiles_h, int n_profiles,
+                                   const voltana_scenarios *scen_h, size_t n, voltana_result *out,
+                                   const voltana_outputs *outputs_h, void *workspace,
+                                   size_t ws_bytes, void *stream);
 
 /* Kernel-launch statistics of the last voltana_simulate on this thread (for the bench):
  * number of kernels launched. */

@@ -492,9 +492,11 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       int backlog = id < a; /* requests still waiting after the batch [A5] */
       double wait = t - arr[I->qhead];
       int k = I->cur;
+      int decided = 0;
       /* window gating: decide only when the interval has elapsed since
        * the last decision, boundary inclusive; interval 0 = every iteration [C1] */
       if (t - I->last_dec >= s->ctrl_interval_ms) {
+        decided = 1;
         if (diag && diag->force_level && force_pos < diag->n_force_level) {
           k = diag->force_level[force_pos++];
         } else {
@@ -510,7 +512,8 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       }
       /* blocking frequency set: the iteration starts after the overhead when the level
        * changes [C3] */
-      double t0 = (k != I->cur && s->freq_overhead_ms > 0.0) ? t + s->freq_overhead_ms : t;
+      int paid = k != I->cur && s->freq_overhead_ms > 0.0;
+      double t0 = paid ? t + s->freq_overhead_ms : t;
       I->cur = k;
       double dur = predict_ttft(p, L[k], nbt); /* execution time = prediction (noise 0) [A25] */
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
@@ -525,6 +528,9 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         diag->iter_dur[diag->iter_n] = dur;
         diag->iter_target[diag->iter_n] = prefill_budget(tgt_ttft, wait);
         if (diag->iter_start) diag->iter_start[diag->iter_n] = t;
+        if (diag->iter_load) diag->iter_load[diag->iter_n] = (uint32_t)nbt;
+        if (diag->iter_kv) diag->iter_kv[diag->iter_n] = 0;
+        if (diag->iter_flags) diag->iter_flags[diag->iter_n] = (uint8_t)(decided | paid << 1 | backlog << 2);
         diag->iter_n++;
       }
       I->end = t0 + dur;
@@ -564,7 +570,9 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       }
       int backlog = I->q_head < I->q_tail; /* KV-blocked admission queue [A5] */
       int k = I->cur;
+      int decided = 0;
       if (t - I->last_dec >= s->ctrl_interval_ms) { /* window gating [C1] */
+        decided = 1;
         if (diag && diag->force_level && force_pos < diag->n_force_level) {
           k = diag->force_level[force_pos++];
         } else {
@@ -576,7 +584,8 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         I->h = fold(I->h, 2, (uint64_t)d, (uint64_t)k, 0);
         I->last_dec = t;
       }
-      double t0 = (k != I->cur && s->freq_overhead_ms > 0.0) ? t + s->freq_overhead_ms : t; /* [C3] */
+      int paid = k != I->cur && s->freq_overhead_ms > 0.0; /* [C3] */
+      double t0 = paid ? t + s->freq_overhead_ms : t;
       I->cur = k;
       double dur = predict_itl(p, L[k], I->nreq, I->nkv);
       if (!(dur > 0.0)) { status = ORC_E_CONTRACT; break; }
@@ -596,6 +605,9 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         diag->iter_dur[diag->iter_n] = dur;
         diag->iter_target[diag->iter_n] = tgt_itl;
         if (diag->iter_start) diag->iter_start[diag->iter_n] = t;
+        if (diag->iter_load) diag->iter_load[diag->iter_n] = (uint32_t)I->nreq;
+        if (diag->iter_kv) diag->iter_kv[diag->iter_n] = (uint32_t)I->nkv;
+        if (diag->iter_flags) diag->iter_flags[diag->iter_n] = (uint8_t)(decided | paid << 1 | backlog << 2);
         diag->iter_n++;
       }
       I->end = t0 + dur;

@@ -89,6 +89,9 @@ typedef struct {
   double *iter_dur;        /* [iter_cap] duration ms                        */
   double *iter_target;     /* [iter_cap] controller target (budget) ms      */
   double *iter_start;      /* [iter_cap] START time t (the iteration runs from t + overhead) */
+  uint32_t *iter_load;     /* [iter_cap] N_bt (prefill) / N_req (decode)     */
+  uint32_t *iter_kv;       /* [iter_cap] N_kv (decode), 0 (prefill)          */
+  uint8_t *iter_flags;     /* [iter_cap] bit0 decision, bit1 overhead, bit2 backlog */
 } orc_diag;
 
 /* status codes (result.status / per-item status) */

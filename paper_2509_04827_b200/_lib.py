@@ -65,6 +65,16 @@ class Scenarios(C.Structure):
                 ("hash_seed", vp)]
 
 
+class Outputs(C.Structure):
+    _fields_ = [("req_offset", vp), ("req_tfirst", vp), ("req_tdone", vp), ("req_itl", vp), ("req_decode", vp),
+                ("req_case", vp), ("iter_offset", vp), ("iters", vp), ("iter_count", vp), ("iter_cap", C.c_uint32),
+                ("reserved", C.c_uint32)]
+
+
+ITERATION_DTYPE = np.dtype([("t_start", "<f8"), ("dur_ms", "<f8"), ("load", "<u4"), ("n_kv", "<u4"),
+                            ("level", "<u2"), ("flags", "u1"), ("reserved", "u1", (5,))])
+assert ITERATION_DTYPE.itemsize == 32
+
 RESULT_DTYPE = np.dtype([
     ("status", "<u4"), ("n_requests", "<u4"), ("n_ttft_ok", "<u4"), ("n_itl_ok", "<u4"),
     ("n_both_ok", "<u4"), ("prefill_iters", "<u4"),
@@ -76,7 +86,7 @@ RESULT_DTYPE = np.dtype([
 assert RESULT_DTYPE.itemsize == 128
 
 EXPORTS = ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_fit_workspace_bytes",
-           "voltana_simulate", "voltana_simulate_workspace_bytes", "voltana_status_string",
+           "voltana_simulate", "voltana_simulate_ex", "voltana_simulate_workspace_bytes", "voltana_status_string",
            "voltana_last_error_detail", "voltana_last_launch_count", "voltana_debug_set_timing")
 
 _lib = None
@@ -103,13 +113,16 @@ def lib():
     L.voltana_simulate_workspace_bytes.restype = C.c_size_t
     L.voltana_simulate.argtypes = [P(Traces), P(Slo), C.c_int, P(Layout), C.c_int, P(Grid), C.c_int, P(Profile),
                                    C.c_int, P(Scenarios), C.c_size_t, vp, vp, C.c_size_t, vp]
+    L.voltana_simulate_ex.argtypes = [P(Traces), P(Slo), C.c_int, P(Layout), C.c_int, P(Grid), C.c_int, P(Profile),
+                                      C.c_int, P(Scenarios), C.c_size_t, vp, P(Outputs), vp, C.c_size_t, vp]
     L.voltana_status_string.argtypes = [C.c_int]
     L.voltana_status_string.restype = C.c_char_p
     L.voltana_last_error_detail.restype = C.c_char_p
     L.voltana_last_launch_count.restype = C.c_int
     L.voltana_debug_set_timing.argtypes = [vp]
     L.voltana_debug_set_timing.restype = None
-    for name in ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_simulate"):
+    for name in ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_simulate",
+                 "voltana_simulate_ex"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

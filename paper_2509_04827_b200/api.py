@@ -222,6 +222,11 @@ class DeviceWorkload:
                                                           len(layouts), n))
         self.workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         self.n_layouts, self.n_slos, self.n_grids = len(layouts), len(slos), len(gs)
+        # host copies the optional outputs are laid out from (caller order)
+        self.traces_offset_host = offset
+        self.trace_id_host = np.asarray(scen["trace_id"], np.int64)
+        self.ninst_host = np.array([layouts[i].n_p + layouts[i].n_d for i in np.asarray(scen["layout_id"], np.int64)],
+                                   np.int64) if n else np.zeros(0, np.int64)
 
     def _up(self, a, dtype):
         if not isinstance(a, torch.Tensor) and np.size(a) == 0:
@@ -230,12 +235,25 @@ class DeviceWorkload:
         self.h2d_bytes += t.numel() * t.element_size()
         return t
 
-    def launch(self, stream=None):
-        """Enqueue voltana_simulate; records land in self.out (LPT order)."""
-        check(lib().voltana_simulate(C.byref(self.traces_struct), self.slos, self.n_slos, self.layouts,
-                                     self.n_layouts, self.grids, self.n_grids, self.profs, len(self.profiles),
-                                     C.byref(self.scen_struct), self.n, _p(self.out), _p(self.workspace),
-                                     self.workspace.numel(), _stream(stream)))
+    def launch(self, stream=None, outputs: "SimOutputs | None" = None):
+        """Enqueue voltana_simulate (voltana_simulate_ex with `outputs`); records land in
+        self.out (LPT order)."""
+        if outputs is None:
+            check(lib().voltana_simulate(C.byref(self.traces_struct), self.slos, self.n_slos, self.layouts,
+                                         self.n_layouts, self.grids, self.n_grids, self.profs, len(self.profiles),
+                                         C.byref(self.scen_struct), self.n, _p(self.out), _p(self.workspace),
+                                         self.workspace.numel(), _stream(stream)))
+        else:
+            check(lib().voltana_simulate_ex(C.byref(self.traces_struct), self.slos, self.n_slos, self.layouts,
+                                            self.n_layouts, self.grids, self.n_grids, self.profs,
+                                            len(self.profiles), C.byref(self.scen_struct), self.n, _p(self.out),
+                                            C.byref(outputs.struct), _p(self.workspace), self.workspace.numel(),
+                                            _stream(stream)))
+
+    def outputs(self, requests=False, iter_cap: int = 0) -> "SimOutputs":
+        """Allocate device buffers for per-request records (requests: True for every scenario or
+        a boolean mask in caller order) and per-instance iteration series (iter_cap > 0)."""
+        return SimOutputs(self, requests, iter_cap)
 
     # ---- end-to-end path from host memory (pinned staging buffers) ----------------
     def pin_host(self):
@@ -269,6 +287,64 @@ class DeviceWorkload:
         """Records in the caller's scenario order (synchronises)."""
         host = self.out.cpu().numpy().view(RESULT_DTYPE).reshape(-1)
         return host[self.inv]
+
+
+class SimOutputs:
+    """Device buffers of voltana_simulate_ex's optional outputs for one DeviceWorkload
+    (include/voltana.h: voltana_outputs), laid out in the kernel's scenario order."""
+
+    def __init__(self, w: DeviceWorkload, requests=False, iter_cap: int = 0):
+        self.w = w
+        dev = w.device
+        lens = np.diff(np.asarray(w.traces_offset_host, np.int64))
+        tid = np.asarray(w.trace_id_host, np.int64)[w.perm]          # kernel order
+        mask = np.ones(w.n, bool) if requests is True else (np.zeros(w.n, bool) if requests is False
+                                                            else np.asarray(requests, bool))
+        s = _lib.Outputs()
+        self.req_len = np.where(mask[w.perm], lens[tid], 0) if w.n else np.zeros(0, np.int64)
+        self.req_off = np.concatenate([[0], np.cumsum(self.req_len)]).astype(np.uint64)
+        self.req = None
+        if mask.any():
+            tot = max(int(self.req_off[-1]), 1)
+            self.req = dict(offset=_dev(self.req_off, torch.uint64, dev),
+                            tfirst=torch.zeros(tot, dtype=torch.float64, device=dev),
+                            tdone=torch.zeros(tot, dtype=torch.float64, device=dev),
+                            itl=torch.zeros(tot, dtype=torch.float64, device=dev),
+                            decode=torch.zeros(tot, dtype=torch.uint8, device=dev),
+                            case=torch.zeros(tot, dtype=torch.uint8, device=dev))
+            s.req_offset = _p(self.req["offset"])
+            s.req_tfirst, s.req_tdone, s.req_itl = _p(self.req["tfirst"]), _p(self.req["tdone"]), _p(self.req["itl"])
+            s.req_decode, s.req_case = _p(self.req["decode"]), _p(self.req["case"])
+        self.iter_cap = int(iter_cap)
+        self.it = None
+        if self.iter_cap > 0 and w.n:
+            ninst = w.ninst_host[w.perm]
+            self.inst_off = np.concatenate([[0], np.cumsum(ninst)]).astype(np.int64)   # instance index base
+            tot_inst = int(self.inst_off[-1])
+            self.it = dict(offset=_dev((self.inst_off[:-1] * self.iter_cap).astype(np.uint64), torch.uint64, dev),
+                           iters=torch.zeros((tot_inst * self.iter_cap, 32), dtype=torch.uint8, device=dev),
+                           count=torch.zeros(tot_inst, dtype=torch.int32, device=dev))
+            s.iter_offset, s.iters, s.iter_count = _p(self.it["offset"]), _p(self.it["iters"]), _p(self.it["count"])
+            s.iter_cap = self.iter_cap
+        self.struct = s
+
+    def requests(self, c: int) -> dict:
+        """Per-request arrays of caller scenario c (trace order)."""
+        k = int(self.w.inv[c])
+        a, b = int(self.req_off[k]), int(self.req_off[k + 1])
+        if self.req is None or a == b:
+            raise KeyError(f"scenario {c} has no per-request output")
+        return {f: self.req[f][a:b].cpu().numpy() for f in ("tfirst", "tdone", "itl", "decode", "case")}
+
+    def iterations(self, c: int) -> list:
+        """Per-instance iteration records of caller scenario c: [prefill 0.., decode 0..], each a
+        structured array (ITERATION_DTYPE) of min(count, iter_cap) entries, plus the counts."""
+        k = int(self.w.inv[c])
+        a, b = int(self.inst_off[k]), int(self.inst_off[k + 1])
+        cnt = self.it["count"][a:b].cpu().numpy().astype(np.int64)
+        raw = self.it["iters"][a * self.iter_cap:b * self.iter_cap].cpu().numpy()
+        rec = raw.reshape(-1).view(_lib.ITERATION_DTYPE).reshape(b - a, self.iter_cap)
+        return [rec[u, :min(int(cnt[u]), self.iter_cap)] for u in range(b - a)], cnt
 
 
 def simulate(traces, slos, layouts, grids, profiles, scen, device="cuda", stream=None) -> np.ndarray:

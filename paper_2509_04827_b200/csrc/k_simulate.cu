@@ -98,6 +98,8 @@ struct WarpSmem {
   const double *noise;             // execution-noise factor table or NULL [D1, D2]
   uint32_t noise_mask, np;         // np: N_P (decode instance d is noise instance N_P + d)
   uint64_t seed;                   // scenario hash seed (noise index)
+  uint64_t rq_base, it_base;       // outputs (E1-E3): request / iteration-slot base of the scenario
+  uint32_t rq_on, it_on;
   // ---- variant-kernel per-instance controller state [C1-C3]
   double dl_last[NI];              // decode lane: time of the last decision (-inf: none)
   uint32_t dl_cur[NI], dl_ndec[NI];  // decode lane: running level, decisions taken
@@ -258,7 +260,8 @@ __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
 
 // ITL accounting of deferred completion lists, in completion order (A30, A37); the head
 // nodes of up to four lists are loaded together.
-__device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d) {
+template <bool EN>
+__device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d, const voltana_outputs &O) {
   const double slo = W.slo_itl;
   for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
     Node h4[4];
@@ -270,18 +273,35 @@ __device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d) {
       if (e0 + u >= D.nfifo) continue;
       const double td = L.ft[e0 + u];
       Node nd = h4[u];
+      uint32_t id = L.fid[e0 + u];
       for (uint32_t hop = 0; hop < W.max_steps; ++hop) {
         const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
         ACC(sitl) = add(ACC(sitl), itl);
         const bool ok = itl <= slo;
         ACC(n_itl_ok) += ok;
         ACC(n_both) += ok && nd.tf > 0.0;
+        if (EN && W.rq_on) {  // per-request record (E1)
+          O.req_tdone[W.rq_base + id] = td;
+          O.req_itl[W.rq_base + id] = itl;
+        }
         if (nd.next == NIL) break;
-        nd = L.node[nd.next];
+        id = nd.next;
+        nd = L.node[id];
       }
     }
   }
   D.nfifo = 0;
+}
+
+// iteration record of the per-instance time series (E2)
+__device__ __forceinline__ void log_iter(const voltana_outputs &O, const WarpSmem &W, uint32_t u, uint32_t j,
+                                         double t, double dur, uint32_t load, uint32_t kv, int k, uint32_t flags) {
+  if (!W.it_on || j >= O.iter_cap) return;
+  voltana_iteration r;
+  r.t_start = t; r.dur_ms = dur; r.load = load; r.n_kv = kv; r.level = (uint16_t)k; r.flags = (uint8_t)flags;
+#pragma unroll
+  for (int x = 0; x < 5; ++x) r.reserved[x] = 0;
+  O.iters[W.it_base + (uint64_t)u * O.iter_cap + j] = r;
 }
 
 // Append request i (finishing at iteration fin) to its bucket; (lfin, lb) = the bucket
@@ -328,7 +348,8 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
 template <bool EN>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
-__device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E) {
+__device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E,
+                            const voltana_outputs &O) {
   if (D.dead) return;
   const uint32_t nbm = W.nb - 1u;
   for (;;) {
@@ -345,7 +366,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
         L.wheel[D.cur & nbm] = make_uint4(0u, 0u, 0u, 0u);
         L.fid[D.nfifo] = b.x - 1u;
         L.ft[D.nfifo] = tnow;
-        if (++D.nfifo == VT_ITL_FIFO) itl_drain(D, L, W, d);
+        if (++D.nfifo == VT_ITL_FIFO) itl_drain<EN>(D, L, W, d, O);
       }
       D.busy = false;
       ACC(tlast) = tnow;
@@ -399,10 +420,12 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     }
     double dur;
     int k;
+    uint32_t fl = backlog ? 4u : 0u;
     if (EN && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)W.dl_cur[d];
       dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv);
     } else {
+      fl |= 1u;
       if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
       else if (EN && W.ctrl) k = energy_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
       else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
@@ -417,8 +440,9 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     }
     double t0 = tnow;
     if (EN) {  // blocking frequency set on a level change [C3]
-      if (k != (int)W.dl_cur[d] && W.fs_ov > 0.0) t0 = add(tnow, W.fs_ov);
+      if (k != (int)W.dl_cur[d] && W.fs_ov > 0.0) { t0 = add(tnow, W.fs_ov); fl |= 2u; }
       W.dl_cur[d] = (uint32_t)k;
+      log_iter(O, W, W.np + (uint32_t)d, D.iters, tnow, dur, D.nreq, D.nkv, k, fl);
     }
     D.end = add(t0, dur);
     D.busy = true;
@@ -539,10 +563,12 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
     budget = budget > 0.0 ? budget : 0.0;
     double dur;
     int k;
+    uint32_t fl = backlog ? 4u : 0u;
     if (EN && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)cur;
       dur = ttft_at(W, k, nbt);
     } else {
+      fl |= 1u;
       if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
       else if (EN && W.ctrl) k = energy_ttft(W, nbt, budget, &dur);  // B4
       else k = lowest_ttft(W, nbt, budget, &dur);
@@ -558,8 +584,9 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
     }
     double t0 = ts;
     if (EN) {  // blocking frequency set on a level change [C3]
-      if (k != (int)cur && W.fs_ov > 0.0) t0 = add(ts, W.fs_ov);
+      if (k != (int)cur && W.fs_ov > 0.0) { t0 = add(ts, W.fs_ov); fl |= 2u; }
       cur = (uint32_t)k;
+      log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
     }
     const double end = add(t0, dur);
     ebusy = add(ebusy, mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), dur));  // W*ms (A23)
@@ -572,6 +599,13 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
       const bool ok = ttft <= slo_ttft;
       ttft_ok += ok;
       const uint32_t o = outl[i];
+      if (EN && W.rq_on) {  // per-request record (E1)
+        P.o.req_tfirst[W.rq_base + i] = end;
+        if (o == 1u) {
+          P.o.req_tdone[W.rq_base + i] = end; P.o.req_itl[W.rq_base + i] = 0.0;
+          P.o.req_decode[W.rq_base + i] = 0xFF; P.o.req_case[W.rq_base + i] = 0xFF;
+        }
+      }
       if (o == 1u) {  // first token came from prefill: done (A8, A30)
         itl_ok++;
         both += ok;
@@ -593,6 +627,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   W.pa_errt[p] = errt; W.pa_errc[p] = errc; W.pa_h[p] = h; W.pa_iters[p] = iters; W.pa_ttft_ok[p] = ttft_ok;
   W.pa_itl_ok[p] = itl_ok; W.pa_both[p] = both;
   if (EN) W.pa_ndec[p] = ndec;
+  if (EN && W.it_on) P.o.iter_count[W.it_base / P.o.iter_cap + p] = iters;
   *head_out = head;
 }
 
@@ -642,6 +677,18 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   const uint32_t N = (uint32_t)N64;
   const int NP = LY.n_p, ND = LY.n_d;
+  uint64_t rq_base = 0, it_base = 0;
+  bool rq_on = false;
+  if (EN && P.o.req_offset) {  // per-request range: empty (skip) or exactly the trace (E1)
+    rq_base = P.o.req_offset[s];
+    const uint64_t len = P.o.req_offset[s + 1] - rq_base;
+    if (len != 0 && len != N64) {
+      write_status(P, s, N, VOLTANA_ITEM_E_INPUT);
+      return;
+    }
+    rq_on = len != 0;
+  }
+  if (EN && P.o.iter_offset) it_base = P.o.iter_offset[s];
 
   // ---------------------------------------------------------------- stage constants and tables
   const uint32_t K = (uint32_t)GR.k, T = (uint32_t)PR.n_tiles;
@@ -662,6 +709,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.noise_mask = LY.noise_len - 1u;
     W.seed = P.hash_seed[s];
     W.np = (uint32_t)NP;
+    W.rq_on = rq_on; W.rq_base = rq_base;
+    W.it_on = EN && P.o.iter_offset != nullptr; W.it_base = it_base;
   }
   if (EN && lane < NI) {
     W.dl_last[lane] = -INF;
@@ -775,7 +824,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
-      dec_advance<EN>(D, lane, L, W, t, dE);
+      dec_advance<EN>(D, lane, L, W, t, dE, P.o);
       t_adv = t;
     }
     // ---- O8 EcoRoute
@@ -867,11 +916,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       if (eco) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
       if (ens) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_en = en_new; }
       dec_push(D, L, i, tf_i, in_i, io >> 16);
+      if (EN && W.rq_on) { P.o.req_decode[W.rq_base + i] = (uint8_t)dsel; P.o.req_case[W.rq_base + i] = (uint8_t)cse; }
     }
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
-  dec_advance<EN>(D, lane, L, W, INF, dE);
-  if (lane < ND && !D.dead) itl_drain(D, L, W, lane);
+  dec_advance<EN>(D, lane, L, W, INF, dE, P.o);
+  if (lane < ND && !D.dead) itl_drain<EN>(D, L, W, lane, P.o);
+  if (EN && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
   __syncwarp(gmask());
 
   // ================================================================ O9: record

@@ -312,7 +312,24 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
                                 int n_grids, const voltana_profile *profiles_h, int n_profiles,
                                 const voltana_scenarios *scen_h, size_t n, voltana_result *out, void *workspace,
                                 size_t ws_bytes, void *stream) {
+  return voltana_simulate_ex(traces_h, slos_h, n_slos, layouts_h, n_layouts, grids_h, n_grids, profiles_h,
+                             n_profiles, scen_h, n, out, nullptr, workspace, ws_bytes, stream);
+}
+
+voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana_slo *slos_h, int n_slos,
+                                   const voltana_layout *layouts_h, int n_layouts, const voltana_grid *grids_h,
+                                   int n_grids, const voltana_profile *profiles_h, int n_profiles,
+                                   const voltana_scenarios *scen_h, size_t n, voltana_result *out,
+                                   const voltana_outputs *outputs_h, void *workspace, size_t ws_bytes,
+                                   void *stream) {
   g_launches = 0;
+  if (outputs_h) {
+    const voltana_outputs &o = *outputs_h;
+    if (o.req_offset && (!o.req_tfirst || !o.req_tdone || !o.req_itl || !o.req_decode || !o.req_case))
+      return fail(VOLTANA_E_INVALID_ARG, "simulate: outputs.req_* null with req_offset set");
+    if (o.iter_offset && (!o.iters || !o.iter_count || o.iter_cap < 1))
+      return fail(VOLTANA_E_INVALID_ARG, "simulate: outputs.iters/iter_count null or iter_cap == 0");
+  }
   if (!traces_h || !slos_h || !layouts_h || !grids_h || !profiles_h || !scen_h)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: null table pointer");
   if (n_slos < 1 || n_slos > MAX_SLOS) return fail(VOLTANA_E_INVALID_ARG, "simulate: n_slos=%d (1..64)", n_slos);
@@ -389,6 +406,7 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
   P->n_slos = (uint32_t)n_slos; P->n_layouts = (uint32_t)n_layouts; P->n_grids = (uint32_t)n_grids;
   P->n_profiles = (uint32_t)n_profiles; P->n_traces = traces_h->n_traces;
   P->max_requests = traces_h->max_requests;
+  if (outputs_h) P->o = *outputs_h;  // zeroed (off) otherwise
   char *ws = (char *)workspace;
   P->counter = (uint32_t *)ws;
   P->slots = ws + L.slots_off;
@@ -417,6 +435,7 @@ voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_sl
     energy = energy || x.policy == 2 || x.ctrl_mode != 0 || x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 ||
              x.exec_noise != nullptr;
   }
+  energy = energy || P->o.req_offset != nullptr || P->o.iter_offset != nullptr;  // outputs (E1-E3)
   e = launch_sim(*P, energy, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");

@@ -49,6 +49,7 @@ struct SimParams {
   uint32_t itl_smem;           // stage the ladder's ITL table in shared memory
   uint32_t smem_per_warp;
   uint64_t *timing;            // debug: [n][2] globaltimer ns at scenario start/end | smid<<56 (NULL: off)
+  voltana_outputs o;           // optional per-request / per-instance outputs (variant kernel only)
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];

@@ -268,6 +268,26 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
                                    const voltana_outputs *outputs_h, void *workspace,
                                    size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------------------------
+ * voltana_series_to_samples — the fit -> simulate loop (DESIGN E4): map
+ * the iteration series written by voltana_simulate_ex (outputs_h: iters, iter_count,
+ * iter_offset ascending, iter_cap) into EcoPred calibration samples for
+ * voltana_fit_profile: slot x = iter_offset[s] + u*iter_cap + j becomes
+ * sample x — prefill instance (u < n_p): phase 0, level = grids[grid_id[s]].level[rec.level],
+ * n_bt = load; decode: phase 1, n_req = load, n_kv; lat_ms = true duration (noise included,
+ * overhead excluded). Slots with j >= count, and scenarios whose profile_id differs from
+ * `profile_id`, get phase 0xFF (skipped by the fit, counted invalid).
+ * scen_h, layouts_h, grids_h: as passed to voltana_simulate_ex (same kernel order).
+ * n_slots = total slots (iter_offset[n-1] + (n_p + n_d) * iter_cap of the last scenario).
+ * Outputs: device SoA [n_slots]. Errors: INVALID_ARG.                                   */
+voltana_status voltana_series_to_samples(const voltana_outputs *outputs_h,
+                                         const voltana_layout *layouts_h, int n_layouts,
+                                         const voltana_grid *grids_h, int n_grids,
+                                         const voltana_scenarios *scen_h, size_t n, size_t n_slots,
+                                         uint32_t profile_id, uint8_t *phase, uint16_t *level,
+                                         uint32_t *n_bt, uint32_t *n_req, uint32_t *n_kv,
+                                         double *lat_ms, void *stream);
+
 /* Kernel-launch statistics of the last voltana_simulate on this thread (for the bench):
  * number of kernels launched. */
 int voltana_last_launch_count(void);

@@ -86,7 +86,7 @@ RESULT_DTYPE = np.dtype([
 assert RESULT_DTYPE.itemsize == 128
 
 EXPORTS = ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_fit_workspace_bytes",
-           "voltana_simulate", "voltana_simulate_ex", "voltana_simulate_workspace_bytes", "voltana_status_string",
+           "voltana_simulate", "voltana_simulate_ex", "voltana_series_to_samples", "voltana_simulate_workspace_bytes", "voltana_status_string",
            "voltana_last_error_detail", "voltana_last_launch_count", "voltana_debug_set_timing")
 
 _lib = None
@@ -115,6 +115,8 @@ def lib():
                                    C.c_int, P(Scenarios), C.c_size_t, vp, vp, C.c_size_t, vp]
     L.voltana_simulate_ex.argtypes = [P(Traces), P(Slo), C.c_int, P(Layout), C.c_int, P(Grid), C.c_int, P(Profile),
                                       C.c_int, P(Scenarios), C.c_size_t, vp, P(Outputs), vp, C.c_size_t, vp]
+    L.voltana_series_to_samples.argtypes = [P(Outputs), P(Layout), C.c_int, P(Grid), C.c_int, P(Scenarios),
+                                            C.c_size_t, C.c_size_t, C.c_uint32, vp, vp, vp, vp, vp, vp, vp]
     L.voltana_status_string.argtypes = [C.c_int]
     L.voltana_status_string.restype = C.c_char_p
     L.voltana_last_error_detail.restype = C.c_char_p
@@ -122,7 +124,7 @@ def lib():
     L.voltana_debug_set_timing.argtypes = [vp]
     L.voltana_debug_set_timing.restype = None
     for name in ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_simulate",
-                 "voltana_simulate_ex"):
+                 "voltana_simulate_ex", "voltana_series_to_samples"):
         getattr(L, name).restype = C.c_int
     _lib = L
     return L

@@ -328,6 +328,26 @@ class SimOutputs:
             s.iter_cap = self.iter_cap
         self.struct = s
 
+    def samples(self, profile_id: int = 0, stream=None) -> dict:
+        """voltana_series_to_samples: the iteration series as EcoPred calibration samples
+        (device SoA, one per slot; empty slots have phase 0xFF) for fit_profile."""
+        if self.it is None:
+            raise ValueError("no iteration series (iter_cap = 0)")
+        n_slots = int(self.inst_off[-1]) * self.iter_cap
+        dev = self.w.device
+        out = dict(phase=torch.empty(n_slots, dtype=torch.uint8, device=dev),
+                   level=torch.empty(n_slots, dtype=torch.uint16, device=dev),
+                   n_bt=torch.empty(n_slots, dtype=torch.uint32, device=dev),
+                   n_req=torch.empty(n_slots, dtype=torch.uint32, device=dev),
+                   n_kv=torch.empty(n_slots, dtype=torch.uint32, device=dev),
+                   lat_ms=torch.empty(n_slots, dtype=torch.float64, device=dev))
+        w = self.w
+        check(lib().voltana_series_to_samples(C.byref(self.struct), w.layouts, w.n_layouts, w.grids, w.n_grids,
+                                              C.byref(w.scen_struct), w.n, n_slots, int(profile_id),
+                                              *[_p(out[k]) for k in ("phase", "level", "n_bt", "n_req", "n_kv",
+                                                                     "lat_ms")], _stream(stream)))
+        return out
+
     def requests(self, c: int) -> dict:
         """Per-request arrays of caller scenario c (trace order)."""
         k = int(self.w.inv[c])

@@ -15,8 +15,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "build")
 SO = os.path.join(HERE, "libvoltana.so")
-SOURCES = ["voltana_api.cu", "k_simulate.cu", "k_decide.cu", "k_fit.cu"]
-HEADERS = ["vt_device.cuh", "vt_sim.h", "vt_decide.h", "vt_fit.h"]
+SOURCES = ["voltana_api.cu", "k_simulate.cu", "k_decide.cu", "k_fit.cu", "k_series.cu"]
+HEADERS = ["vt_device.cuh", "vt_sim.h", "vt_decide.h", "vt_fit.h", "vt_series.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # -fmad=false: canonical fp64 arithmetic without FMA contraction (A33)
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-fmad=false", "-std=c++17",

@@ -10,6 +10,7 @@
 #include "vt_decide.h"
 #include "vt_device.cuh"
 #include "vt_fit.h"
+#include "vt_series.h"
 #include "vt_sim.h"
 
 using namespace vt;
@@ -439,6 +440,40 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   e = launch_sim(*P, energy, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
+  g_launches = 1;
+  return ok();
+}
+
+// ------------------------------------------------------------------ K5
+voltana_status voltana_series_to_samples(const voltana_outputs *o, const voltana_layout *layouts_h, int n_layouts,
+                                         const voltana_grid *grids_h, int n_grids, const voltana_scenarios *scen_h,
+                                         size_t n, size_t n_slots, uint32_t profile_id, uint8_t *phase,
+                                         uint16_t *level, uint32_t *n_bt, uint32_t *n_req, uint32_t *n_kv,
+                                         double *lat_ms, void *stream) {
+  g_launches = 0;
+  if (!o || !layouts_h || !grids_h || !scen_h)
+    return fail(VOLTANA_E_INVALID_ARG, "series_to_samples: null table pointer");
+  if (!o->iters || !o->iter_count || !o->iter_offset || o->iter_cap < 1)
+    return fail(VOLTANA_E_INVALID_ARG, "series_to_samples: outputs hold no iteration series");
+  if (n_layouts < 1 || n_layouts > SERIES_MAX_LAYOUTS || n_grids < 1 || n_grids > SERIES_MAX_GRIDS)
+    return fail(VOLTANA_E_INVALID_ARG, "series_to_samples: n_layouts=%d n_grids=%d (1..16)", n_layouts, n_grids);
+  if (n == 0 || n_slots == 0) return ok();
+  if (!scen_h->layout_id || !scen_h->grid_id || !scen_h->profile_id || !phase || !level || !n_bt || !n_req ||
+      !n_kv || !lat_ms)
+    return fail(VOLTANA_E_INVALID_ARG, "series_to_samples: null array pointer");
+  SeriesParams P;
+  memset(&P, 0, sizeof(P));
+  P.iters = o->iters; P.iter_count = o->iter_count; P.iter_offset = o->iter_offset; P.cap = o->iter_cap;
+  P.profile_id = profile_id;
+  P.layout_id = scen_h->layout_id; P.grid_id = scen_h->grid_id; P.scen_profile_id = scen_h->profile_id;
+  P.n = n; P.n_slots = n_slots;
+  P.phase = phase; P.level = level; P.n_bt = n_bt; P.n_req = n_req; P.n_kv = n_kv; P.lat = lat_ms;
+  for (int i = 0; i < n_layouts; ++i) P.n_p[i] = layouts_h[i].n_p;
+  for (int i = 0; i < n_grids; ++i) P.grid[i] = grids_h[i];
+  const size_t want = (n_slots + SERIES_THREADS - 1) / SERIES_THREADS;
+  const int grid = (int)(want < (size_t)sm_count() * 8 ? want : (size_t)sm_count() * 8);
+  cudaError_t e = launch_series(P, grid, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "series_to_samples launch");
   g_launches = 1;
   return ok();
 }

@@ -99,3 +99,53 @@ def test_outputs_do_not_change_records(vt, orc):
     dw = vt.DeviceWorkload(w.traces, w.slos, w.layouts, w.grids, w.profiles, w.scen)
     dw.launch(outputs=dw.outputs(requests=True, iter_cap=64))
     assert dw.records().tobytes() == base.tobytes()
+
+
+@pytest.mark.parametrize("sigma", [0.0, 0.05])
+def test_fit_simulate_loop(vt, orc, sigma):
+    """K4 series -> K5 samples -> K1 fit equals the oracle fit of the oracle's iteration log
+    (same samples in another order: within 1e-12), and the loop's profile drives K4 again."""
+    from test_oracle_loop import log_samples
+    w = synth.build_config("C4", scenarios=list(range(3584, 4096, 64)), duration_scale=0.3)
+    if sigma > 0:
+        w = dataclasses.replace(w, layouts=[dataclasses.replace(x, exec_noise=synth.exec_noise_table(sigma, 4096))
+                                            for x in w.layouts])
+    p = w.profiles[0]
+    dw = vt.DeviceWorkload(w.traces, w.slos, w.layouts, w.grids, w.profiles, w.scen)
+    outs = dw.outputs(iter_cap=1 << 14)
+    dw.launch(outputs=outs)
+    smp = outs.samples(profile_id=0)
+    fit = vt.fit_profile(smp["phase"], smp["level"], smp["n_bt"], smp["n_req"], smp["n_kv"], smp["lat_ms"],
+                         p.k, p.n_tiles, p.tile_w, 0.0)
+    torch.cuda.synchronize()
+    cols = []
+    for c in range(w.n):
+        r, d, lay, _ = _oracle_scenario(orc, w, c, 1 << 22)
+        cols.append(log_samples(d, w.grids[w.scen["grid_id"][c]], lay.n_p))
+    osmp = [np.concatenate([x[i] for x in cols]) for i in range(6)]
+    ref = orc.fit_profile(*osmp, p.k, p.n_tiles, p.tile_w, 0.0)
+    st = fit["cell_status"].cpu().numpy()
+    assert (st == ref["cell_status"]).all()
+    n_valid = int((smp["phase"] <= 1).sum().item())
+    assert n_valid == len(osmp[0])
+    assert int(fit["invalid"].cpu().numpy().view(np.uint64)[0]) == smp["phase"].numel() - n_valid
+    ok = st == 0
+    K = p.k
+    for name, sl in (("a1", slice(0, K)), ("c1", slice(0, K)), ("a2", slice(K, None)), ("b2", slice(K, None)),
+                     ("c2", slice(K, None))):
+        g = fit[name].cpu().numpy()
+        o = ref[name]
+        m = ok[sl]
+        err = np.abs(g[m] - o[m]) / np.maximum(np.abs(o[m]), 1e-9)
+        assert err.max() <= 1e-12 or np.abs(g[m] - o[m]).max() < 1e-12, (name, err.max())
+    # close the loop: the fitted profile drives the simulator again (ladder [0]: the level whose
+    # ITL cells the log covered), GPU and oracle on the same fitted tables
+    dp2 = vt.DeviceProfile.from_fit(fit, p.mhz, p.dyn, p.p_idle, p.tdp, p.u_half_prefill, p.u_half_decode,
+                                    p.n_tiles, p.tile_w)
+    host = {k: fit[k].cpu().numpy() for k in ("a1", "c1", "a2", "b2", "c2")}
+    p2 = dataclasses.replace(p, **host)
+    w2 = dataclasses.replace(w, grids=[np.array([0], np.uint16)], profiles=[p2],
+                             scen=dict(w.scen, grid_id=np.zeros(w.n, np.uint32)))
+    g2 = vt.simulate(w2.traces, w2.slos, w2.layouts, w2.grids, [dp2], w2.scen)
+    compare_records(g2, orc.simulate_workload(w2))
+    assert (g2["status"] == 0).all()

@@ -55,7 +55,38 @@
 #define VT_ITL_FIFO 1  // completion lists deferred before their ITL accounting runs (1..8; 1 measured best)
 #endif
 
+#ifndef VT_L2HINT
+#define VT_L2HINT 0    // wheel buckets loaded/stored with an L2 evict_last cache policy
+#endif
+#ifndef VT_ITL_SMEM_ONLY
+#define VT_ITL_SMEM_ONLY 0  // experiment: assume the ITL table is staged (no global fallback)
+#endif
+
 namespace vt {
+
+// ---- wheel bucket access (optionally pinned in L2 against the streaming node traffic)
+__device__ __forceinline__ uint4 wld(const uint4 *a) {
+#if VT_L2HINT
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  uint4 r;
+  asm volatile("ld.global.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(a), "l"(pol) : "memory");
+  return r;
+#else
+  return *a;
+#endif
+}
+__device__ __forceinline__ void wst(uint4 *a, uint4 v) {
+#if VT_L2HINT
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;"
+               :: "l"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol) : "memory");
+#else
+  *a = v;
+#endif
+}
 
 // ---- scenario groups: SPW scenarios per warp, GS lanes each; every collective is group-masked
 constexpr int GS = 32 / SPW;
@@ -113,14 +144,18 @@ struct WarpSmem {
 };
 
 // ------------------------------------------------------------------ EcoPred on staged tables
+// F ("fast tables"): the ITL table is staged, K <= 8 and the tile width is a power of two for
+// every scenario of the launch (host-checked): the dead general paths are compiled out.
+template <bool F>
 __device__ __forceinline__ uint32_t tile_j(const WarpSmem &W, uint32_t n) {
-  const uint32_t j = W.wshift >= 0 ? (n - 1u) >> W.wshift : (n - 1u) / W.W;
+  const uint32_t j = (F || W.wshift >= 0) ? (n - 1u) >> W.wshift : (n - 1u) / W.W;
   return j < W.T - 1u ? j : W.T - 1u;
 }
 
 // eq:pred-itl at ladder index k, tile j; dn = (double)N_req, dkv = (double)N_kv (exact)
+template <bool F>
 __device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, double dn, double dkv) {
-  if (W.itl_smem) {
+  if (F || VT_ITL_SMEM_ONLY || W.itl_smem) {
     const double *r = W.it + 3 * ((size_t)j * W.K + k);
     return add(add(mul(r[0], dn), mul(r[1], dkv)), r[2]);
   }
@@ -135,31 +170,33 @@ __device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt
 // Lowest ladder index whose prediction meets `target` (A1), else K-1 (A2);
 // *pred = the prediction there. Ascending scan with early exit, or an exact binary search
 // when the tables are coefficient-monotone in f (A32).
+template <bool F>
 __device__ int lowest_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
-  const uint32_t j = tile_j(W, n);
+  const uint32_t j = tile_j<F>(W, n);
   const int K = (int)W.K;
   const double dn = (double)n, dkv = (double)kv;
-  if (W.mono_it && K > 8) {
+  if (!F && W.mono_it && K > 8) {
     int lo = 0, hi = K;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (itl_at(W, j, mid, dn, dkv) <= target) hi = mid; else lo = mid + 1;
+      if (itl_at<F>(W, j, mid, dn, dkv) <= target) hi = mid; else lo = mid + 1;
     }
     const int k = lo < K ? lo : K - 1;
-    *pred = itl_at(W, j, k, dn, dkv);
+    *pred = itl_at<F>(W, j, k, dn, dkv);
     return k;
   }
   for (int k = 0; k < K - 1; ++k) {
-    const double p = itl_at(W, j, k, dn, dkv);
+    const double p = itl_at<F>(W, j, k, dn, dkv);
     if (p <= target) { *pred = p; return k; }
   }
-  *pred = itl_at(W, j, K - 1, dn, dkv);
+  *pred = itl_at<F>(W, j, K - 1, dn, dkv);
   return K - 1;
 }
 
+template <bool F>
 __device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, double *pred) {
   const int K = (int)W.K;
-  if (W.mono_tt && K > 8) {
+  if (!F && W.mono_tt && K > 8) {
     int lo = 0, hi = K;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
@@ -180,19 +217,20 @@ __device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
 // Energy-argmin controller [B4]: among the levels meeting the target, the lowest busy
 // energy P(k, load) * T(k) (eq:P-f P:187, energy = time x power P:74); ties -> lower level;
 // none feasible -> K-1 (A2). Full scan (the energy curve is not monotone).
+template <bool F>
 __device__ int energy_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
-  const uint32_t j = tile_j(W, n);
+  const uint32_t j = tile_j<F>(W, n);
   const int K = (int)W.K;
   const double dn = (double)n, dkv = (double)kv;
   int best = -1;
   double be = 0.0, bt = 0.0;
   for (int k = 0; k < K; ++k) {
-    const double t = itl_at(W, j, k, dn, dkv);
+    const double t = itl_at<F>(W, j, k, dn, dkv);
     if (!(t <= target)) continue;
     const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[K + k], n), t);
     if (best < 0 || e < be) { best = k; be = e; bt = t; }
   }
-  if (best < 0) { best = K - 1; bt = itl_at(W, j, K - 1, dn, dkv); }
+  if (best < 0) { best = K - 1; bt = itl_at<F>(W, j, K - 1, dn, dkv); }
   *pred = bt;
   return best;
 }
@@ -260,7 +298,7 @@ __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
 
 // ITL accounting of deferred completion lists, in completion order (A30, A37); the head
 // nodes of up to four lists are loaded together.
-template <bool EN>
+template <bool EN, bool F>
 __device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d, const voltana_outputs &O) {
   const double slo = W.slo_itl;
   for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
@@ -309,16 +347,16 @@ __device__ __forceinline__ void log_iter(const voltana_outputs &O, const WarpSme
 __device__ __forceinline__ void bucket_append(Dec &D, const Lane &L, uint32_t nbm, uint32_t i, uint32_t fin,
                                               uint32_t inout, uint32_t &lfin, uint4 &lb) {
 #if VT_BHPF
-  uint4 b = fin == lfin ? lb : (fin == D.bh_fin ? D.bh : L.wheel[fin & nbm]);
+  uint4 b = fin == lfin ? lb : (fin == D.bh_fin ? D.bh : wld(L.wheel + (fin & nbm)));
 #else
-  uint4 b = fin == lfin ? lb : L.wheel[fin & nbm];
+  uint4 b = fin == lfin ? lb : wld(L.wheel + (fin & nbm));
 #endif
   L.node[i].next = NIL;
   if (b.y == 0u) b.x = i + 1u; else L.node[b.y - 1u].next = i;
   b.y = i + 1u;
   b.z += 1u;
   b.w += inout;
-  L.wheel[fin & nbm] = b;
+  wst(L.wheel + (fin & nbm), b);
   lfin = fin;
   lb = b;
 #if VT_BHPF
@@ -347,7 +385,7 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
-template <bool EN>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
+template <bool EN, bool F>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
 __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E,
                             const voltana_outputs &O) {
   if (D.dead) return;
@@ -363,10 +401,10 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
       D.nreq -= b.z;
       D.nkv -= b.w;
       if (b.x != 0u) {
-        L.wheel[D.cur & nbm] = make_uint4(0u, 0u, 0u, 0u);
+        wst(L.wheel + (D.cur & nbm), make_uint4(0u, 0u, 0u, 0u));
         L.fid[D.nfifo] = b.x - 1u;
         L.ft[D.nfifo] = tnow;
-        if (++D.nfifo == VT_ITL_FIFO) itl_drain<EN>(D, L, W, d, O);
+        if (++D.nfifo == VT_ITL_FIFO) itl_drain<EN, F>(D, L, W, d, O);
       }
       D.busy = false;
       ACC(tlast) = tnow;
@@ -423,12 +461,12 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     uint32_t fl = backlog ? 4u : 0u;
     if (EN && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)W.dl_cur[d];
-      dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv);
+      dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv);
     } else {
       fl |= 1u;
-      if (backlog) { k = (int)W.K - 1; dur = itl_at(W, tile_j(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
-      else if (EN && W.ctrl) k = energy_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
-      else k = lowest_itl(W, D.nreq, D.nkv, W.tgt_itl, &dur);
+      if (backlog) { k = (int)W.K - 1; dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
+      else if (EN && W.ctrl) k = energy_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
+      else k = lowest_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);
       ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
       if (EN) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
     }
@@ -451,11 +489,11 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     if (k == (int)W.K - 1) ACC(top) = add(ACC(top), dur);
     D.cur = D.iters;
     D.iters += 1u;
-    D.bcur = L.wheel[D.cur & nbm];  // final now: read at the END of this iteration
+    D.bcur = wld(L.wheel + (D.cur & nbm));  // final now: read at the END of this iteration
 #if VT_BHPF
     if (D.qh != NIL) {
       D.bh_fin = D.iters + (uint32_t)queue_head(D, L).out - 2u;
-      D.bh = L.wheel[D.bh_fin & nbm];
+      D.bh = wld(L.wheel + (D.bh_fin & nbm));
     } else {
       D.bh_fin = NIL;
     }
@@ -482,6 +520,9 @@ __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, doub
   }
   D.qt = i;
 }
+
+// x mod nd for x < 2 nd (cursor arithmetic without an integer division)
+__device__ __forceinline__ uint32_t wrap_nd(uint32_t x, uint32_t nd) { return x >= nd ? x - nd : x; }
 
 // warp-wide min of a non-negative double held by lanes with `valid`; returns the lowest lane
 // attaining it, or -1 if no lane is valid. Bit patterns of non-negative doubles order as u64.
@@ -520,7 +561,7 @@ __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uin
 }
 
 // ------------------------------------------------------------------ phase A: prefill lane p
-template <bool EN>
+template <bool EN, bool F>
 __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const double *arr, const uint32_t *inl,
                              const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0,
                              uint32_t *head_out) {
@@ -571,7 +612,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
       fl |= 1u;
       if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
       else if (EN && W.ctrl) k = energy_ttft(W, nbt, budget, &dur);  // B4
-      else k = lowest_ttft(W, nbt, budget, &dur);
+      else k = lowest_ttft<F>(W, nbt, budget, &dur);
       h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
       if (EN) { last = ts; ndec++; }
     }
@@ -631,7 +672,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   *head_out = head;
 }
 
-template <bool EN>
+template <bool EN, bool F>
 __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WarpSmem &W) {
   const int lane = glane();
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -752,7 +793,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
   // ================================================================ PHASE A: prefill lanes
   uint32_t p_head = NIL;
-  if (lane < NP) prefill_lane<EN>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
+  if (lane < NP) prefill_lane<EN, F>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
   __syncwarp(gmask());
 
   // ================================================================ PHASE B: routing + decode lanes
@@ -824,7 +865,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
-      dec_advance<EN>(D, lane, L, W, t, dE, P.o);
+      dec_advance<EN, F>(D, lane, L, W, t, dE, P.o);
       t_adv = t;
     }
     // ---- O8 EcoRoute
@@ -839,18 +880,18 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         if (n != 0u) {
           if (n != c_n || kv != c_kv) {
             double pr;
-            const int k0 = lowest_itl(W, n, kv, W.tgt_itl, &pr);  // EcoFreq level now (A10/A11)
+            const int k0 = lowest_itl<F>(W, n, kv, W.tgt_itl, &pr);  // EcoFreq level now (A10/A11)
             c_en = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k0], n), pr);
             c_n = n; c_kv = kv;
           }
           enow = c_en;
         }
         const uint32_t n1 = n + 1u, kv1 = kv + in_i + 1u;  // A12
-        const uint32_t j = tile_j(W, n1);
+        const uint32_t j = tile_j<F>(W, n1);
         const double dn = (double)n1, dkv = (double)kv1;
         double best = 0.0, t = 0.0;
         for (int k = 0; k < (int)W.K; ++k) {
-          t = itl_at(W, j, k, dn, dkv);
+          t = itl_at<F>(W, j, k, dn, dkv);
           if (!(t <= W.tgt_itl)) continue;
           const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], n1), t);
           if (!feas) en_new = e;                    // the successor's own EcoFreq-level P*T
@@ -865,11 +906,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       const unsigned inset = any ? min_set(score, feas) : min_set(tmax, act);
       cse = any ? 6 : 7;
       const unsigned rot = ((inset >> cursor) | (inset << (ND - (int)cursor))) & ((1u << ND) - 1u);
-      dsel = (int)((cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND);
-      if (__popc(inset) >= 2) cursor = (uint32_t)(dsel + 1) % (uint32_t)ND;
+      dsel = (int)wrap_nd(cursor + (uint32_t)ffs0(rot), (uint32_t)ND);
+      if (__popc(inset) >= 2) cursor = wrap_nd((uint32_t)dsel + 1u, (uint32_t)ND);
     } else if (!eco) {
       dsel = (int)cursor;
-      cursor = (cursor + 1u) % (uint32_t)ND;
+      cursor = wrap_nd(cursor + 1u, (uint32_t)ND);
       cse = 0;
     } else {
       int fnow = 0x7fffffff, faft = 0x7fffffff;
@@ -878,10 +919,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         double pr;
         int kn = 0;                                                            // A10, A11
         if (n != 0u) {
-          if (n != c_n || kv != c_kv) { c_lvl = lowest_itl(W, n, kv, W.tgt_itl, &pr); c_n = n; c_kv = kv; }
+          if (n != c_n || kv != c_kv) { c_lvl = lowest_itl<F>(W, n, kv, W.tgt_itl, &pr); c_n = n; c_kv = kv; }
           kn = c_lvl;
         }
-        const int ka = lowest_itl(W, n + 1u, kv + in_i + 1u, W.tgt_itl, &pr);  // A12
+        const int ka = lowest_itl<F>(W, n + 1u, kv + in_i + 1u, W.tgt_itl, &pr);  // A12
         ka_last = ka;
         fnow = W.mhz[kn];
         faft = W.mhz[ka];
@@ -907,8 +948,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       }
       // round robin among the candidate set from the cursor (A17)
       const unsigned rot = ((inset >> cursor) | (inset << (ND - (int)cursor))) & ((1u << ND) - 1u);
-      dsel = (int)((cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND);
-      if (__popc(inset) >= 2) cursor = (uint32_t)(dsel + 1) % (uint32_t)ND;
+      dsel = (int)wrap_nd(cursor + (uint32_t)ffs0(rot), (uint32_t)ND);
+      if (__popc(inset) >= 2) cursor = wrap_nd((uint32_t)dsel + 1u, (uint32_t)ND);
     }
     steps_route++;
     h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
@@ -920,8 +961,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
-  dec_advance<EN>(D, lane, L, W, INF, dE, P.o);
-  if (lane < ND && !D.dead) itl_drain<EN>(D, L, W, lane, P.o);
+  dec_advance<EN, F>(D, lane, L, W, INF, dE, P.o);
+  if (lane < ND && !D.dead) itl_drain<EN, F>(D, L, W, lane, P.o);
   if (EN && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
   __syncwarp(gmask());
 
@@ -936,7 +977,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     const uint32_t cd = gshfl(dE.code, wd >= 0 ? wd : 0);
     write_status(P, s, N, (wp >= 0 && tp <= td) ? W.pa_errc[wp] : cd);
     if (lane < ND)  // leave the wheel clean for the next scenario of this warp
-      for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint4(0u, 0u, 0u, 0u);
+      for (uint32_t b = 0; b < P.nb; ++b) wst(wheels + (size_t)lane * P.nb + b, make_uint4(0u, 0u, 0u, 0u));
     return;
   }
   const int dd = lane < ND ? lane : 0;
@@ -1005,7 +1046,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
 // EN = false: the paper's EcoFreq/EcoRoute/RR only (the default kernel); EN = true also runs
 // the energy variants [B1-B4] (selected on the host when any layout asks for them).
-template <bool EN>
+template <bool EN, bool F>
 __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(const __grid_constant__ SimParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = glane();
@@ -1033,7 +1074,7 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
     if (s >= P.n) break;
     uint64_t t0 = 0;
     if (P.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    run_scenario<EN>(P, s, slot, wheels, W);
+    run_scenario<EN, F>(P, s, slot, wheels, W);
     __syncwarp(gmask());
     if (P.timing && lane == 0) {
       uint64_t t1;
@@ -1048,15 +1089,19 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
 
 size_t sim_smem_fixed() { return (sizeof(WarpSmem) - sizeof(double) + 15) & ~(size_t)15; }
 
-const void *sim_kernel_ptr(bool energy) {
-  return energy ? (const void *)simulate_kernel<true> : (const void *)simulate_kernel<false>;
+const void *sim_kernel_ptr(bool energy, bool fast) {
+  if (energy) return fast ? (const void *)simulate_kernel<true, true> : (const void *)simulate_kernel<true, false>;
+  return fast ? (const void *)simulate_kernel<false, true> : (const void *)simulate_kernel<false, false>;
 }
 
-cudaError_t launch_sim(const SimParams &P, bool energy, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(energy), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t launch_sim(const SimParams &P, bool energy, bool fast, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(energy, fast), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
   if (e != cudaSuccess) return e;
-  if (energy) simulate_kernel<true><<<grid, SIM_THREADS, smem, st>>>(P);
-  else simulate_kernel<false><<<grid, SIM_THREADS, smem, st>>>(P);
+  if (energy && fast) simulate_kernel<true, true><<<grid, SIM_THREADS, smem, st>>>(P);
+  else if (energy) simulate_kernel<true, false><<<grid, SIM_THREADS, smem, st>>>(P);
+  else if (fast) simulate_kernel<false, true><<<grid, SIM_THREADS, smem, st>>>(P);
+  else simulate_kernel<false, false><<<grid, SIM_THREADS, smem, st>>>(P);
   return cudaGetLastError();
 }
 

@@ -259,8 +259,10 @@ int resident_warps(size_t smem_per_block) {
   if (smem_per_block != cached_smem) {
     int nb = 0;
     // both instantiations are built for the same bound (128 registers, 4 CTAs per SM)
-    cudaFuncSetAttribute(sim_kernel_ptr(false), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_per_block);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(false), SIM_THREADS, smem_per_block) !=
+    cudaFuncSetAttribute(sim_kernel_ptr(false, false), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem_per_block);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(false, false), SIM_THREADS,
+                                                      smem_per_block) !=
             cudaSuccess || nb < 1) {
       cudaGetLastError();
       nb = 1;
@@ -437,7 +439,9 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
              x.exec_noise != nullptr;
   }
   energy = energy || P->o.req_offset != nullptr || P->o.iter_offset != nullptr;  // outputs (E1-E3)
-  e = launch_sim(*P, energy, grid, L.smem, st);
+  bool fast = L.itl_smem && kmax <= 8;
+  for (int i = 0; i < n_profiles; ++i) fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0;
+  e = launch_sim(*P, energy, fast, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
   g_launches = 1;

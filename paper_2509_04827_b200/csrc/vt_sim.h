@@ -21,7 +21,10 @@ constexpr int SPW = VT_SPW;           // scenarios per warp (lane groups of 32 /
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
 size_t sim_smem_fixed();  // per-warp shared-memory block without the staged ITL table
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size
-constexpr uint32_t SIM_WHEEL_MAX = 1024;    // decode wheel buckets (L2-resident); longer requests use the far list
+#ifndef VT_NBMAX
+#define VT_NBMAX 1024
+#endif
+constexpr uint32_t SIM_WHEEL_MAX = VT_NBMAX; // decode wheel buckets (L2-resident); longer requests use the far list
 
 struct SimParams {
   // traces (device)
@@ -57,7 +60,10 @@ struct SimParams {
   DevProfile prof[MAX_PROFILES];
 };
 
-const void *sim_kernel_ptr(bool energy);  // energy: the instantiation that also runs [B1-B4]
-cudaError_t launch_sim(const SimParams &P, bool energy, int grid, size_t smem, cudaStream_t st);
+// energy: the instantiation that also runs the variants [B1-B4, C1-C3, D1-D2, E1-E2];
+// fast: every ladder has K <= 8, every tile width is a power of two and the ITL tables are
+// staged in shared memory, so the general table paths are compiled out.
+const void *sim_kernel_ptr(bool energy, bool fast);
+cudaError_t launch_sim(const SimParams &P, bool energy, bool fast, int grid, size_t smem, cudaStream_t st);
 
 }  // namespace vt

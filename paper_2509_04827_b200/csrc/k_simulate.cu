@@ -58,6 +58,9 @@
 #ifndef VT_L2HINT
 #define VT_L2HINT 0    // wheel buckets loaded/stored with an L2 evict_last cache policy
 #endif
+#ifndef VT_PIPE_ARGMIN
+#define VT_PIPE_ARGMIN 0  // select the next request right after advancing the stream (overlap)
+#endif
 #ifndef VT_ITL_SMEM_ONLY
 #define VT_ITL_SMEM_ONLY 0  // experiment: assume the ITL table is staged (no global fallback)
 #endif
@@ -848,12 +851,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const bool eco = LY.policy == 0 && ND > 1;
   const bool ens = EN && LY.policy == 2 && ND > 1;
   const int32_t delta = LY.delta_mhz;
+  int w = argmin_time(fabs(hn.tf), hd != NIL);  // next PrefillDone request in (t, p, id) order
   for (;;) {
-    const double ht = fabs(hn.tf);
-    const int w = argmin_time(ht, hd != NIL);  // next PrefillDone request in (t, p, id) order
     if (w < 0) break;
     if (steps_route > N) { dE.t = 0.0; dE.code = VOLTANA_ITEM_E_INTERNAL; break; }  // watchdog
-    const double t = gshfl(ht, w);
+    const double t = gshfl(fabs(hn.tf), w);
     const uint32_t i = gshfl(hd, w);
     const uint32_t io = gshfl((uint32_t)hn.in | ((uint32_t)hn.out << 16), w);
     const double tf_i = gshfl(hn.tf, w);  // signed: carries the TTFT verdict
@@ -863,6 +865,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       hn = nn;
       if (hd != NIL && hn.next != NIL) nn = node[hn.next];
     }
+#if VT_PIPE_ARGMIN
+    // the next request depends only on the stream heads: its selection overlaps this route
+    const int w_next = argmin_time(fabs(hn.tf), hd != NIL);
+#endif
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
       dec_advance<EN, F>(D, lane, L, W, t, dE, P.o);
@@ -959,6 +965,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       dec_push(D, L, i, tf_i, in_i, io >> 16);
       if (EN && W.rq_on) { P.o.req_decode[W.rq_base + i] = (uint8_t)dsel; P.o.req_case[W.rq_base + i] = (uint8_t)cse; }
     }
+#if VT_PIPE_ARGMIN
+    w = w_next;
+#else
+    w = argmin_time(fabs(hn.tf), hd != NIL);
+#endif
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
   dec_advance<EN, F>(D, lane, L, W, INF, dE, P.o);

@@ -9,7 +9,10 @@
 
 namespace vt {
 
-constexpr int SIM_THREADS = 128;      // 4 warps per CTA, one scenario per warp
+#ifndef VT_SIM_THREADS
+#define VT_SIM_THREADS 128
+#endif
+constexpr int SIM_THREADS = VT_SIM_THREADS;  // 4 warps per CTA, one scenario per warp
 #ifndef VT_SIM_MIN_BLOCKS
 #define VT_SIM_MIN_BLOCKS 4
 #endif

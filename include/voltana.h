@@ -53,15 +53,17 @@ typedef enum {
 
 /* One calibrated profile (the output of the offline profiling pass).
  * Host struct holding DEVICE table pointers. Level l of the profile grid runs at
- * mhz[l]; tables are indexed by level, ITL tables are [n_tiles][k] (row = tile). */
+ * mhz[l]; tables are indexed by level, ITL tables are [n_tiles][k] and TTFT tables
+ * [n_ptiles][k] (row = tile). Prefill tile of a batch (Appendix B) [F1]:
+ * n_ptiles <= 1 -> 0; N_bt > prefill_cutoff -> n_ptiles-1; else min(n_ptiles-1, (N_bt-1)/W). */
 typedef struct {
   int32_t k;          /* levels on the grid, 1..1024                                   */
   int32_t n_tiles;    /* ITL tiles T >= 1 (batch-size boundaries)               */
   int32_t tile_w;     /* tile width W >= 1 (128)                                */
-  int32_t reserved;
+  int32_t n_ptiles;   /* prefill tiles T_p, 0 or 1 = a single TTFT tile, <= 64 [F1]     */
   const int32_t *mhz; /* device [k] strictly increasing MHz                            */
-  const double *a1;   /* device [k]   eq:pred-ttft T = a1*N_bt + c1, ms/token  */
-  const double *c1;   /* device [k]   ms                                               */
+  const double *a1;   /* device [max(1,n_ptiles)*k] eq:pred-ttft T = a1*N_bt + c1 */
+  const double *c1;   /* device [max(1,n_ptiles)*k] ms                                 */
   const double *a2;   /* device [n_tiles*k] eq:pred-itl, ms per request         */
   const double *b2;   /* device [n_tiles*k] ms per KV token                            */
   const double *c2;   /* device [n_tiles*k] ms                                         */
@@ -70,6 +72,8 @@ typedef struct {
   double p_idle;      /* W, idle draw at any frequency                                 */
   double tdp;         /* W, power clip                                         */
   double u_half_prefill, u_half_decode; /* utilisation u = load / (load + u_half)      */
+  int32_t prefill_cutoff; /* N_bt above which prefill uses the last tile (2000) [F1] */
+  int32_t reserved;
 } voltana_profile;
 
 /* ------------------------------------------------------------------------------------
@@ -116,23 +120,25 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
 
 /* ------------------------------------------------------------------------------------
  * voltana_fit_profile — EcoPred calibration: ordinary least squares
- * per cell. TTFT cell = (prefill, level l): lat ~ a1*N_bt + c1. ITL cell = (decode,
- * level l, tile j = min(T-1, (N_req-1)/W)): lat ~ a2*N_req + b2*N_kv + c2. Empty ITL tile
- * j > 0 inherits tile j-1 plus tile_step on c2; MAE per fitted cell.
+ * per cell. TTFT cell = (prefill, level l, prefill tile jp as in voltana_profile [F1]):
+ * lat ~ a1*N_bt + c1. ITL cell = (decode, level l, tile j = min(T-1, (N_req-1)/W)):
+ * lat ~ a2*N_req + b2*N_kv + c2. An empty tile j > 0 (prefill: jp > 0) inherits tile j-1
+ * plus tile_step on c2 (c1) [F2]; MAE per fitted cell.
  * Samples (device SoA, length n): phase u8 (0/1), level u16 (< k), n_bt/n_req/n_kv u32,
- * lat_ms f64. Outputs (device): a1,c1 [k]; a2,b2,c2 [T*k]; mae [k + T*k];
- * cell_status [k + T*k] (0 fitted, 1 inherited, 2 empty, 3 degenerate) — cell index:
- * TTFT level l -> l, ITL (j, l) -> k + j*k + l.
+ * lat_ms f64. Outputs (device), Tp = n_ptiles >= 1: a1,c1 [Tp*k]; a2,b2,c2 [T*k];
+ * mae [Tp*k + T*k]; cell_status [Tp*k + T*k] (0 fitted, 1 inherited, 2 empty,
+ * 3 degenerate) — cell index: TTFT (jp, l) -> jp*k + l, ITL (j, l) -> Tp*k + j*k + l.
  * Returns OK after enqueueing; cell errors are reported in cell_status (read it back:
  * any 2 or 3 is the E_CALIBRATION condition). Sums use a fixed reduction order, so the
  * result is deterministic and within 1e-12 relative of the sequential oracle.
- * Samples with phase > 1, level >= k or (decode and n_req == 0) are ignored and counted
- * in invalid_count (device u64, may be NULL).                                           */
-size_t voltana_fit_workspace_bytes(size_t n_samples, int k, int n_tiles);
+ * Samples with phase > 1, level >= k, (decode and n_req == 0) or (prefill and n_bt == 0)
+ * are ignored and counted in invalid_count (device u64, may be NULL).                   */
+size_t voltana_fit_workspace_bytes(size_t n_samples, int k, int n_tiles, int n_ptiles);
 voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level,
                                    const uint32_t *n_bt, const uint32_t *n_req,
                                    const uint32_t *n_kv, const double *lat_ms, size_t n,
                                    int k, int n_tiles, int tile_w, double tile_step,
+                                   int n_ptiles, uint32_t prefill_cutoff,
                                    double *a1, double *c1, double *a2, double *b2, double *c2,
                                    double *mae, uint8_t *cell_status, uint64_t *invalid_count,
                                    void *workspace, size_t ws_bytes, void *stream);

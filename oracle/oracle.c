@@ -35,9 +35,21 @@ static int tile_index(const orc_profile *p, uint64_t n_req) {
   return (int)j;
 }
 
+/* prefill tile (Appendix B: a staircase below ~2000 batched tokens that "gradually
+ * becomes less significant" above): T_p <= 1 -> one tile; else N_bt above the
+ * cutoff -> the last tile T_p - 1, otherwise min(T_p - 1, floor((N_bt - 1) / W)) [F1] */
+static int ptile_index(const orc_profile *p, uint64_t n_bt) {
+  if (p->n_ptiles <= 1) return 0;
+  if (n_bt > (uint64_t)p->prefill_cutoff) return p->n_ptiles - 1;
+  uint64_t j = (n_bt - 1) / (uint64_t)p->tile_w;
+  if (j > (uint64_t)(p->n_ptiles - 1)) j = (uint64_t)(p->n_ptiles - 1);
+  return (int)j;
+}
+
 static double predict_ttft(const orc_profile *p, int lvl, uint64_t n_bt) {
-  /* eq:pred-ttft, evaluated as (a1 * N_bt) + c1 [A33] */
-  return (p->a1[lvl] * (double)n_bt) + p->c1[lvl];
+  /* eq:pred-ttft, evaluated as (a1 * N_bt) + c1 [A33], on the batch's prefill tile */
+  size_t idx = (size_t)ptile_index(p, n_bt) * (size_t)p->k + (size_t)lvl;
+  return (p->a1[idx] * (double)n_bt) + p->c1[idx];
 }
 
 static double predict_itl(const orc_profile *p, int lvl, uint64_t n_req, uint64_t n_kv) {
@@ -733,20 +745,32 @@ int oracle_route_batch(const orc_profile *p, const uint16_t *L, int K, int n_d,
 #define FIT_EMPTY 2
 #define FIT_DEGENERATE 3
 
+/* prefill tile of a sample, as ptile_index [F1] */
+static size_t fit_ptile(uint32_t nbt, int Tp, uint32_t cutoff, int W) {
+  if (Tp <= 1) return 0;
+  if (nbt > cutoff) return (size_t)(Tp - 1);
+  uint32_t j = (nbt - 1) / (uint32_t)W;
+  return j < (uint32_t)(Tp - 1) ? (size_t)j : (size_t)(Tp - 1);
+}
+
 int oracle_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32_t *n_bt,
                        const uint32_t *n_req, const uint32_t *n_kv, const double *lat_ms,
-                       size_t n, int K, int T, int W, double tile_step,
+                       size_t n, int K, int T, int W, double tile_step, int Tp, uint32_t cutoff,
                        double *a1, double *c1, double *a2, double *b2, double *c2,
                        double *mae, uint8_t *cell_status) {
-  /* F1: cells. TTFT cell k (prefill, level k) = index k; ITL cell (decode, level k,
-   * tile j) = index K + j*K + k, tile j = min(T-1, (N_req-1)/W). */
-  const size_t C = (size_t)K + (size_t)T * (size_t)K;
+  /* F1: cells. TTFT cell (prefill, level k, prefill tile jp) = index jp*K + k; ITL cell
+   * (decode, level k, tile j) = index Tp*K + j*K + k, tile j = min(T-1, (N_req-1)/W)
+   * (prefill tiles P:880-885). Tp <= 1: one prefill tile. */
+  if (Tp < 1) Tp = 1;
+  const size_t KP = (size_t)Tp * (size_t)K;
+  const size_t C = KP + (size_t)T * (size_t)K;
   for (size_t i = 0; i < n; ++i) {
     if (phase[i] > 1 || level[i] >= K) return 1;
     if (phase[i] == 1 && n_req[i] == 0) return 1;
+    if (phase[i] == 0 && n_bt[i] == 0) return 1;
   }
-  #define CELL(i) (phase[i] == 0 ? (size_t)level[i] : \
-      (size_t)K + (size_t)((n_req[i] - 1) / (uint32_t)W < (uint32_t)(T - 1) ? (n_req[i] - 1) / (uint32_t)W : (uint32_t)(T - 1)) * (size_t)K + level[i])
+  #define CELL(i) (phase[i] == 0 ? fit_ptile(n_bt[i], Tp, cutoff, W) * (size_t)K + level[i] : \
+      KP + (size_t)((n_req[i] - 1) / (uint32_t)W < (uint32_t)(T - 1) ? (n_req[i] - 1) / (uint32_t)W : (uint32_t)(T - 1)) * (size_t)K + level[i])
   double *cnt = calloc(C, sizeof(double));
   double *s1 = calloc(C, sizeof(double)), *s2 = calloc(C, sizeof(double)), *sy = calloc(C, sizeof(double));
   /* pass 1: means, sequential sums in sample order */
@@ -778,19 +802,26 @@ int oracle_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32
     }
   }
   int err = 0;
-  /* F2: TTFT per level: a = Sxy / Sxx, c = ybar - a xbar; needs >= 2 distinct N_bt [A31] */
-  for (int k = 0; k < K; ++k) {
-    size_t c = (size_t)k;
-    if (cnt[c] == 0.0) { cell_status[c] = FIT_EMPTY; a1[k] = c1[k] = 0.0; err = 1; continue; }
-    if (cnt[c] < 2.0 || !(S11[c] > 0.0)) { cell_status[c] = FIT_DEGENERATE; a1[k] = c1[k] = 0.0; err = 1; continue; }
-    a1[k] = S1y[c] / S11[c];
-    c1[k] = my[c] - (a1[k] * m1[c]);
-    cell_status[c] = FIT_OK;
+  /* F2: TTFT per (prefill tile, level): a = Sxy / Sxx, c = ybar - a xbar; needs >= 2 distinct
+   * N_bt [A31]; an empty prefill tile jp > 0 inherits jp - 1 with the step on c1 [F2] */
+  for (int jp = 0; jp < Tp; ++jp) {
+    for (int k = 0; k < K; ++k) {
+      size_t c = (size_t)jp * (size_t)K + (size_t)k;
+      if (cnt[c] == 0.0) {
+        if (jp == 0) { cell_status[c] = FIT_EMPTY; a1[c] = c1[c] = 0.0; err = 1; }
+        else { a1[c] = a1[c - (size_t)K]; c1[c] = c1[c - (size_t)K] + tile_step; cell_status[c] = FIT_INHERITED; }
+        continue;
+      }
+      if (cnt[c] < 2.0 || !(S11[c] > 0.0)) { cell_status[c] = FIT_DEGENERATE; a1[c] = c1[c] = 0.0; err = 1; continue; }
+      a1[c] = S1y[c] / S11[c];
+      c1[c] = my[c] - (a1[c] * m1[c]);
+      cell_status[c] = FIT_OK;
+    }
   }
   /* F3/F4: ITL per (tile, level), two regressors; empty tile j>0 inherits j-1 + step */
   for (int j = 0; j < T; ++j) {
     for (int k = 0; k < K; ++k) {
-      size_t c = (size_t)K + (size_t)j * (size_t)K + (size_t)k;
+      size_t c = KP + (size_t)j * (size_t)K + (size_t)k;
       size_t o = (size_t)j * (size_t)K + (size_t)k;
       if (cnt[c] == 0.0) {
         if (j == 0) { cell_status[c] = FIT_EMPTY; a2[o] = b2[o] = c2[o] = 0.0; err = 1; }
@@ -819,9 +850,9 @@ int oracle_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32
     if (cell_status[c] != FIT_OK) continue;
     double yh;
     if (phase[i] == 0) {
-      yh = (a1[level[i]] * (double)n_bt[i]) + c1[level[i]];
+      yh = (a1[c] * (double)n_bt[i]) + c1[c];
     } else {
-      size_t o = c - (size_t)K;
+      size_t o = c - KP;
       yh = ((a2[o] * (double)n_req[i]) + (b2[o] * (double)n_kv[i])) + c2[o];
     }
     ae[c] += fabs(lat_ms[i] - yh);
@@ -840,6 +871,7 @@ double oracle_predict_itl(const orc_profile *p, int level, uint32_t n_req, uint3
   return predict_itl(p, level, n_req, n_kv);
 }
 int oracle_tile_index(const orc_profile *p, uint32_t n_req) { return tile_index(p, n_req); }
+int oracle_ptile_index(const orc_profile *p, uint32_t n_bt) { return ptile_index(p, n_bt); }
 double oracle_busy_power(const orc_profile *p, int phase, int level, uint32_t load) {
   return busy_power(p, phase, level, load);
 }

@@ -25,12 +25,14 @@ typedef struct {
   int32_t k;             /* levels on the profile grid                       */
   int32_t n_tiles;       /* ITL tiles T                                      */
   int32_t tile_w;        /* tile width W (128)                        */
-  int32_t pad_;
+  int32_t n_ptiles;      /* prefill tiles T_p (<= 1: single tile) [F1]       */
   const int32_t *mhz;    /* [k] frequency of each level                      */
-  const double *a1, *c1; /* [k]                                              */
+  const double *a1, *c1; /* [n_ptiles*k], row = prefill tile                 */
   const double *a2, *b2, *c2; /* [n_tiles*k], row = tile                     */
   const double *dyn;     /* [2*k] prefill row then decode row (W)            */
   double p_idle, tdp, uh_prefill, uh_decode;
+  int32_t prefill_cutoff; /* N_bt above which prefill is the last tile [F1]  */
+  int32_t pad2_;
 } orc_profile;
 
 /* One scenario: trace x SLO x layout x frequency ladder (BASELINE north_star). */
@@ -116,7 +118,7 @@ int oracle_route_batch(const orc_profile *p, const uint16_t *ladder, int K, int 
 
 int oracle_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32_t *n_bt,
                        const uint32_t *n_req, const uint32_t *n_kv, const double *lat_ms,
-                       size_t n, int K, int T, int W, double tile_step,
+                       size_t n, int K, int T, int W, double tile_step, int Tp, uint32_t cutoff,
                        double *a1, double *c1, double *a2, double *b2, double *c2,
                        double *mae, uint8_t *cell_status);
 
@@ -124,6 +126,7 @@ int oracle_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32
 double oracle_predict_ttft(const orc_profile *p, int level, uint32_t n_bt);
 double oracle_predict_itl(const orc_profile *p, int level, uint32_t n_req, uint32_t n_kv);
 int oracle_tile_index(const orc_profile *p, uint32_t n_req);
+int oracle_ptile_index(const orc_profile *p, uint32_t n_bt);
 double oracle_busy_power(const orc_profile *p, int phase, int level, uint32_t load);
 double oracle_interval_energy(double power_w, double dur_ms);
 

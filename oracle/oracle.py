@@ -41,10 +41,10 @@ vp = C.c_void_p
 
 
 class OrcProfile(C.Structure):
-    _fields_ = [("k", C.c_int32), ("n_tiles", C.c_int32), ("tile_w", C.c_int32), ("pad_", C.c_int32),
+    _fields_ = [("k", C.c_int32), ("n_tiles", C.c_int32), ("tile_w", C.c_int32), ("n_ptiles", C.c_int32),
                 ("mhz", vp), ("a1", vp), ("c1", vp), ("a2", vp), ("b2", vp), ("c2", vp), ("dyn", vp),
                 ("p_idle", C.c_double), ("tdp", C.c_double), ("uh_prefill", C.c_double),
-                ("uh_decode", C.c_double)]
+                ("uh_decode", C.c_double), ("prefill_cutoff", C.c_int32), ("pad2_", C.c_int32)]
 
 
 class OrcScenario(C.Structure):
@@ -78,12 +78,13 @@ def lib():
         L.oracle_route_batch.argtypes = [P(OrcProfile), vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int32,
                                          C.c_int, vp, C.c_size_t, vp, vp, vp]
         L.oracle_fit_profile.argtypes = [vp, vp, vp, vp, vp, vp, C.c_size_t, C.c_int, C.c_int, C.c_int,
-                                         C.c_double, vp, vp, vp, vp, vp, vp, vp]
+                                         C.c_double, C.c_int, C.c_uint32, vp, vp, vp, vp, vp, vp, vp]
         L.oracle_predict_ttft.argtypes = [P(OrcProfile), C.c_int, C.c_uint32]
         L.oracle_predict_ttft.restype = C.c_double
         L.oracle_predict_itl.argtypes = [P(OrcProfile), C.c_int, C.c_uint32, C.c_uint32]
         L.oracle_predict_itl.restype = C.c_double
         L.oracle_tile_index.argtypes = [P(OrcProfile), C.c_uint32]
+        L.oracle_ptile_index.argtypes = [P(OrcProfile), C.c_uint32]
         L.oracle_busy_power.argtypes = [P(OrcProfile), C.c_int, C.c_int, C.c_uint32]
         L.oracle_busy_power.restype = C.c_double
         L.oracle_interval_energy.argtypes = [C.c_double, C.c_double]
@@ -105,10 +106,11 @@ class _ProfileHandle:
             c1=np.ascontiguousarray(prof.c1, np.float64), a2=np.ascontiguousarray(prof.a2, np.float64),
             b2=np.ascontiguousarray(prof.b2, np.float64), c2=np.ascontiguousarray(prof.c2, np.float64),
             dyn=np.ascontiguousarray(prof.dyn, np.float64))
-        self.s = OrcProfile(int(len(prof.mhz)), int(prof.n_tiles), int(prof.tile_w), 0,
+        self.s = OrcProfile(int(len(prof.mhz)), int(prof.n_tiles), int(prof.tile_w),
+                            int(getattr(prof, "n_ptiles", 1)),
                             *[_ptr(self.arrs[k]) for k in ("mhz", "a1", "c1", "a2", "b2", "c2", "dyn")],
                             float(prof.p_idle), float(prof.tdp), float(prof.u_half_prefill),
-                            float(prof.u_half_decode))
+                            float(prof.u_half_decode), int(getattr(prof, "prefill_cutoff", 2000)), 0)
 
 
 def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, hash_seed=0,
@@ -212,17 +214,18 @@ def route_batch(prof, ladder, n_d, n_req, n_kv, req_in, itl_target, delta_mhz, p
     return inst, case, st, cur
 
 
-def fit_profile(phase, level, n_bt, n_req, n_kv, lat_ms, K, T, W=128, tile_step=0.0):
+def fit_profile(phase, level, n_bt, n_req, n_kv, lat_ms, K, T, W=128, tile_step=0.0, Tp=1, cutoff=2000):
     arrs = [np.ascontiguousarray(phase, np.uint8), np.ascontiguousarray(level, np.uint16),
             np.ascontiguousarray(n_bt, np.uint32), np.ascontiguousarray(n_req, np.uint32),
             np.ascontiguousarray(n_kv, np.uint32), np.ascontiguousarray(lat_ms, np.float64)]
     n = len(arrs[0])
-    a1, c1 = np.zeros(K), np.zeros(K)
+    Tp = max(1, int(Tp))
+    a1, c1 = np.zeros(Tp * K), np.zeros(Tp * K)
     a2, b2, c2 = np.zeros(T * K), np.zeros(T * K), np.zeros(T * K)
-    mae = np.zeros(K + T * K)
-    cs = np.zeros(K + T * K, np.uint8)
-    rc = lib().oracle_fit_profile(*[_ptr(a) for a in arrs], n, int(K), int(T), int(W), float(tile_step),
-                                  _ptr(a1), _ptr(c1), _ptr(a2), _ptr(b2), _ptr(c2), _ptr(mae), _ptr(cs))
+    mae = np.zeros(Tp * K + T * K)
+    cs = np.zeros(Tp * K + T * K, np.uint8)
+    rc = lib().oracle_fit_profile(*[_ptr(a) for a in arrs], n, int(K), int(T), int(W), float(tile_step), Tp,
+                                  int(cutoff), _ptr(a1), _ptr(c1), _ptr(a2), _ptr(b2), _ptr(c2), _ptr(mae), _ptr(cs))
     return dict(rc=rc, a1=a1, c1=c1, a2=a2, b2=b2, c2=c2, mae=mae, cell_status=cs)
 
 
@@ -239,6 +242,11 @@ def predict_itl(prof, level, n_req, n_kv):
 def tile_index(prof, n_req):
     ph = _ProfileHandle(prof)
     return lib().oracle_tile_index(C.byref(ph.s), int(n_req))
+
+
+def ptile_index(prof, n_bt):
+    ph = _ProfileHandle(prof)
+    return lib().oracle_ptile_index(C.byref(ph.s), int(n_bt))
 
 
 def busy_power(prof, phase, level, load):

@@ -32,10 +32,10 @@ class VoltanaError(RuntimeError):
 
 
 class Profile(C.Structure):
-    _fields_ = [("k", C.c_int32), ("n_tiles", C.c_int32), ("tile_w", C.c_int32), ("reserved", C.c_int32),
+    _fields_ = [("k", C.c_int32), ("n_tiles", C.c_int32), ("tile_w", C.c_int32), ("n_ptiles", C.c_int32),
                 ("mhz", vp), ("a1", vp), ("c1", vp), ("a2", vp), ("b2", vp), ("c2", vp), ("dyn", vp),
                 ("p_idle", C.c_double), ("tdp", C.c_double), ("u_half_prefill", C.c_double),
-                ("u_half_decode", C.c_double)]
+                ("u_half_decode", C.c_double), ("prefill_cutoff", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Slo(C.Structure):
@@ -105,9 +105,10 @@ def lib():
     L.voltana_control_step.argtypes = [P(Profile), C.c_int, C.c_int, vp, C.c_int, vp, vp, vp, vp, vp, C.c_size_t, vp, vp, vp]
     L.voltana_route_batch.argtypes = [P(Profile), vp, C.c_int, C.c_int, vp, vp, vp, vp, C.c_int32, C.c_int, vp,
                                       C.c_size_t, vp, vp, vp, vp]
-    L.voltana_fit_workspace_bytes.argtypes = [C.c_size_t, C.c_int, C.c_int]
+    L.voltana_fit_workspace_bytes.argtypes = [C.c_size_t, C.c_int, C.c_int, C.c_int]
     L.voltana_fit_workspace_bytes.restype = C.c_size_t
     L.voltana_fit_profile.argtypes = [vp, vp, vp, vp, vp, vp, C.c_size_t, C.c_int, C.c_int, C.c_int, C.c_double,
+                                      C.c_int, C.c_uint32,
                                       vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
     L.voltana_simulate_workspace_bytes.argtypes = [P(Traces), P(Layout), C.c_int, C.c_size_t]
     L.voltana_simulate_workspace_bytes.restype = C.c_size_t

@@ -47,18 +47,20 @@ class DeviceProfile:
 
     @classmethod
     def from_fit(cls, fit: "FitOutput", mhz, dyn, p_idle, tdp, u_half_prefill, u_half_decode, n_tiles,
-                 tile_w=128, device="cuda"):
+                 tile_w=128, device="cuda", n_ptiles: int = 1, prefill_cutoff: int = 2000):
         """Profile whose EcoPred tables are the (device-resident) output of fit_profile."""
         self = cls.__new__(cls)
         self.k = int(len(mhz))
         self.n_tiles = int(n_tiles)
         self.tile_w = int(tile_w)
+        self.n_ptiles, self.prefill_cutoff = int(n_ptiles), int(prefill_cutoff)
         self.mhz_host = np.asarray(mhz, np.int32).copy()
         self.t = dict(mhz=_dev(mhz, torch.int32, device), a1=fit["a1"], c1=fit["c1"], a2=fit["a2"], b2=fit["b2"],
                       c2=fit["c2"], dyn=_dev(dyn, torch.float64, device))
-        self.struct = _lib.Profile(self.k, self.n_tiles, self.tile_w, 0,
+        self.struct = _lib.Profile(self.k, self.n_tiles, self.tile_w, self.n_ptiles,
                                    *[_p(self.t[n]) for n in ("mhz", "a1", "c1", "a2", "b2", "c2", "dyn")],
-                                   float(p_idle), float(tdp), float(u_half_prefill), float(u_half_decode))
+                                   float(p_idle), float(tdp), float(u_half_prefill), float(u_half_decode),
+                                   self.prefill_cutoff, 0)
         return self
 
     def __init__(self, prof, device="cuda"):
@@ -70,10 +72,12 @@ class DeviceProfile:
                       c1=_dev(prof.c1, torch.float64, device), a2=_dev(prof.a2, torch.float64, device),
                       b2=_dev(prof.b2, torch.float64, device), c2=_dev(prof.c2, torch.float64, device),
                       dyn=_dev(prof.dyn, torch.float64, device))
-        self.struct = _lib.Profile(self.k, self.n_tiles, self.tile_w, 0,
+        self.n_ptiles = int(getattr(prof, "n_ptiles", 1))
+        self.prefill_cutoff = int(getattr(prof, "prefill_cutoff", 2000))
+        self.struct = _lib.Profile(self.k, self.n_tiles, self.tile_w, self.n_ptiles,
                                    *[_p(self.t[n]) for n in ("mhz", "a1", "c1", "a2", "b2", "c2", "dyn")],
                                    float(prof.p_idle), float(prof.tdp), float(prof.u_half_prefill),
-                                   float(prof.u_half_decode))
+                                   float(prof.u_half_decode), self.prefill_cutoff, 0)
 
 
 def _ladder(ladder):
@@ -119,31 +123,34 @@ class FitOutput(dict):
     pass
 
 
-def fit_workspace_bytes(n_samples: int, k: int, n_tiles: int) -> int:
-    return int(lib().voltana_fit_workspace_bytes(int(n_samples), int(k), int(n_tiles)))
+def fit_workspace_bytes(n_samples: int, k: int, n_tiles: int, n_ptiles: int = 1) -> int:
+    return int(lib().voltana_fit_workspace_bytes(int(n_samples), int(k), int(n_tiles), int(n_ptiles)))
 
 
 def fit_profile(phase, level, n_bt, n_req, n_kv, lat_ms, k: int, n_tiles: int, tile_w: int = 128,
-                tile_step: float = 0.0, workspace=None, out: FitOutput | None = None, stream=None) -> FitOutput:
+                tile_step: float = 0.0, workspace=None, out: FitOutput | None = None, stream=None,
+                n_ptiles: int = 1, prefill_cutoff: int = 2000) -> FitOutput:
     """EcoPred least-squares calibration (voltana_fit_profile) on device sample SoA."""
     n = int(lat_ms.numel())
     dev = lat_ms.device
-    cells = k + n_tiles * k
+    n_ptiles = max(1, int(n_ptiles))
+    cells = n_ptiles * k + n_tiles * k
     if out is None:
-        out = FitOutput(a1=torch.empty(k, dtype=torch.float64, device=dev),
-                        c1=torch.empty(k, dtype=torch.float64, device=dev),
+        out = FitOutput(a1=torch.empty(n_ptiles * k, dtype=torch.float64, device=dev),
+                        c1=torch.empty(n_ptiles * k, dtype=torch.float64, device=dev),
                         a2=torch.empty(n_tiles * k, dtype=torch.float64, device=dev),
                         b2=torch.empty(n_tiles * k, dtype=torch.float64, device=dev),
                         c2=torch.empty(n_tiles * k, dtype=torch.float64, device=dev),
                         mae=torch.empty(cells, dtype=torch.float64, device=dev),
                         cell_status=torch.empty(cells, dtype=torch.uint8, device=dev),
                         invalid=torch.zeros(1, dtype=torch.uint64, device=dev))
-    need = fit_workspace_bytes(n, k, n_tiles)
+    need = fit_workspace_bytes(n, k, n_tiles, n_ptiles)
     if workspace is None or workspace.numel() < need:
         workspace = torch.empty(need, dtype=torch.uint8, device=dev)
     out["workspace"] = workspace
     check(lib().voltana_fit_profile(_p(phase), _p(level), _p(n_bt), _p(n_req), _p(n_kv), _p(lat_ms), n, int(k),
-                                    int(n_tiles), int(tile_w), float(tile_step), _p(out["a1"]), _p(out["c1"]),
+                                    int(n_tiles), int(tile_w), float(tile_step), n_ptiles, int(prefill_cutoff),
+                                    _p(out["a1"]), _p(out["c1"]),
                                     _p(out["a2"]), _p(out["b2"]), _p(out["c2"]), _p(out["mae"]),
                                     _p(out["cell_status"]), _p(out["invalid"]), _p(workspace),
                                     workspace.numel(), _stream(stream)))

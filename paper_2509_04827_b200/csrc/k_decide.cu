@@ -20,22 +20,39 @@ struct SmemTables {
   const int *mhz;     // [K]
 };
 
-// Layout (doubles): [K][2] a1,c1 | [T][K][3] a2,b2,c2 | [K] DYN row of `dyn_phase`; then int [K] MHz.
-__device__ __forceinline__ double *dyn_smem(double *sm, int K, int T) { return sm + 2 * K + 3 * T * K; }
-__device__ __forceinline__ int *mhz_smem(double *sm, int K, int T) { return (int *)(sm + 3 * K + 3 * T * K); }
+// Layout (doubles): [T_p][K][2] a1,c1 | [T][K][3] a2,b2,c2 | [K] DYN row of `dyn_phase`;
+// then int [K] MHz. T_p = prefill tiles (F1).
+__device__ __forceinline__ int tt_len(int K, const DevProfile &PR) { return 2 * PR.n_ptiles * K; }
+__device__ __forceinline__ double *itl_smem(double *sm, int K, const DevProfile &PR) { return sm + tt_len(K, PR); }
+__device__ __forceinline__ double *dyn_smem(double *sm, int K, const DevProfile &PR) {
+  return sm + tt_len(K, PR) + 3 * PR.n_tiles * K;
+}
+__device__ __forceinline__ int *mhz_smem(double *sm, int K, const DevProfile &PR) {
+  return (int *)(sm + tt_len(K, PR) + 3 * PR.n_tiles * K + K);
+}
+// TTFT row {a1, c1}[K] of the batch's prefill tile
+__device__ __forceinline__ const double *tt_row(const double *sm, int K, const DevProfile &PR, uint32_t nbt) {
+  return sm + 2 * K * (int)ptile_of(nbt, (uint32_t)PR.tile_w, (uint32_t)PR.n_ptiles, PR.pcut);
+}
 
 __device__ void stage_tables(const DevProfile &PR, const LadderParam &LP, bool need_tt, bool need_it,
                              int dyn_phase, double *sm, int *smi) {
   const int K = LP.k, T = PR.n_tiles;
-  double *dy = dyn_smem(sm, K, T);
+  double *dy = dyn_smem(sm, K, PR);
   for (int x = threadIdx.x; x < K; x += blockDim.x) {
     int lv = LP.level[x];
-    if (need_tt) { sm[2 * x] = PR.a1[lv]; sm[2 * x + 1] = PR.c1[lv]; }
     if (dyn_phase >= 0) dy[x] = PR.dyn[dyn_phase * PR.k + lv];
     smi[x] = PR.mhz[lv];
   }
+  if (need_tt) {
+    for (int x = threadIdx.x; x < PR.n_ptiles * K; x += blockDim.x) {
+      const int jp = x / K, k = x - jp * K;
+      const size_t o = (size_t)jp * PR.k + LP.level[k];
+      sm[2 * x] = PR.a1[o]; sm[2 * x + 1] = PR.c1[o];
+    }
+  }
   if (need_it) {
-    double *it = sm + 2 * K;
+    double *it = itl_smem(sm, K, PR);
     for (int x = threadIdx.x; x < T * K; x += blockDim.x) {
       int j = x / K, k = x - j * K;
       size_t o = (size_t)j * PR.k + LP.level[k];
@@ -114,10 +131,11 @@ template <int PHASE>
 __global__ void __launch_bounds__(DECIDE_THREADS)
 control_kernel(const __grid_constant__ ControlParams P) {
   extern __shared__ double sm[];
-  int *smi = mhz_smem(sm, P.lad.k, P.prof.n_tiles);
+  int *smi = mhz_smem(sm, P.lad.k, P.prof);
   stage_tables(P.prof, P.lad, PHASE == 0, PHASE == 1, P.mode == 1 ? PHASE : -1, sm, smi);
   const int K = P.lad.k;
-  const double *dy = dyn_smem(sm, K, P.prof.n_tiles);
+  const double *dy = dyn_smem(sm, K, P.prof);
+  const double *its = itl_smem(sm, K, P.prof);
   const bool emode = P.mode == 1;
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
   // DECIDE_UNROLL items per thread per tile, block-strided: every load instruction is
@@ -150,7 +168,8 @@ control_kernel(const __grid_constant__ ControlParams P) {
         } else {
           double b = sub(tgt[u], wait[u]);
           b = b > 0.0 ? b : 0.0;
-          lvl = (uint16_t)(emode ? energy_ttft(sm, dy, P.prof, K, load[u], b) : scan_ttft(sm, K, load[u], b));
+          const double *ttr = tt_row(sm, K, P.prof, load[u]);   // prefill tile (F1)
+          lvl = (uint16_t)(emode ? energy_ttft(ttr, dy, P.prof, K, load[u], b) : scan_ttft(ttr, K, load[u], b));
         }
       } else {
         if (load[u] == 0u || kv[u] < load[u]) {
@@ -158,8 +177,8 @@ control_kernel(const __grid_constant__ ControlParams P) {
         } else if (q[u] > 0u) {
           lvl = (uint16_t)(K - 1);
         } else {
-          lvl = (uint16_t)(emode ? energy_itl(sm + 2 * K, dy, P.prof, K, load[u], kv[u], tgt[u], wshift)
-                                 : scan_itl(sm + 2 * K, P.prof, K, load[u], kv[u], tgt[u], wshift));
+          lvl = (uint16_t)(emode ? energy_itl(its, dy, P.prof, K, load[u], kv[u], tgt[u], wshift)
+                                 : scan_itl(its, P.prof, K, load[u], kv[u], tgt[u], wshift));
         }
       }
       P.out_level[i] = lvl;
@@ -281,11 +300,11 @@ template <int ND_MAX>
 __global__ void __launch_bounds__(DECIDE_THREADS)
 route_kernel(const __grid_constant__ RouteParams P) {
   extern __shared__ double sm[];
-  int *smi = mhz_smem(sm, P.lad.k, P.prof.n_tiles);
+  int *smi = mhz_smem(sm, P.lad.k, P.prof);
   stage_tables(P.prof, P.lad, false, true, P.policy == 2 ? 1 : -1, sm, smi);
   const int K = P.lad.k, ND = P.n_d;
-  const double *it = sm + 2 * K;
-  const double *dy = dyn_smem(sm, K, P.prof.n_tiles);
+  const double *it = itl_smem(sm, K, P.prof);
+  const double *dy = dyn_smem(sm, K, P.prof);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
   constexpr int U = ND_MAX <= 2 ? DECIDE_UNROLL : 2;
   const size_t tile = (size_t)blockDim.x * U;
@@ -326,8 +345,9 @@ route_kernel(const __grid_constant__ RouteParams P) {
   }
 }
 
-size_t decide_smem_bytes(int k, int n_tiles) {
-  return (size_t)(3 * k + 3 * n_tiles * k) * sizeof(double) + (size_t)k * sizeof(int);
+size_t decide_smem_bytes(int k, int n_tiles, int n_ptiles) {
+  const int tp = n_ptiles < 1 ? 1 : n_ptiles;
+  return (size_t)(2 * tp * k + 3 * n_tiles * k + k) * sizeof(double) + (size_t)k * sizeof(int);
 }
 
 cudaError_t launch_control(const ControlParams &P, int phase, int grid, size_t smem, cudaStream_t st) {

@@ -29,14 +29,18 @@ __device__ __forceinline__ Sample load_sample(const FitParams &P, size_t i, bool
   if (!in_range) return s;
   const uint32_t ph = P.phase[i], lv = P.level[i];
   const uint32_t nr = P.n_req[i];
-  if (ph > 1u || lv >= (uint32_t)P.k || (ph == 1u && nr == 0u)) { s.cell = -2; return s; }
+  const uint32_t nb = ph == 0u ? P.n_bt[i] : 1u;
+  if (ph > 1u || lv >= (uint32_t)P.k || (ph == 1u && nr == 0u) || nb == 0u) { s.cell = -2; return s; }
   s.y = P.lat[i];
   if (ph == 0u) {
-    s.cell = (int)lv;
-    s.x1 = P.n_bt[i];
+    // prefill tile (F1): T_p <= 1 one tile; N_bt above the cutoff the last; else (N_bt-1)/W
+    uint32_t jp = 0;
+    if (P.n_ptiles > 1) jp = nb > P.pcut ? (uint32_t)P.n_ptiles - 1u : tile_of(nb, (uint32_t)P.tile_w, (uint32_t)P.n_ptiles);
+    s.cell = (int)jp * P.k + (int)lv;
+    s.x1 = nb;
   } else {
     uint32_t j = tile_of(nr, (uint32_t)P.tile_w, (uint32_t)P.n_tiles);
-    s.cell = P.k + (int)j * P.k + (int)lv;
+    s.cell = P.kp + (int)j * P.k + (int)lv;
     s.x1 = nr;
     s.x2 = P.n_kv[i];
   }
@@ -82,7 +86,7 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
         double dy = sub(s.y, m[2]);
         v[0] = mul(dx1, dx1);
         v[4] = mul(dx1, dy);   // S1y
-        if (s.cell >= P.k) {
+        if (s.cell >= P.kp) {
           double dx2 = sub((double)s.x2, m[1]);
           v[1] = mul(dx1, dx2);
           v[2] = mul(dx2, dx2);
@@ -94,10 +98,10 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
     } else {
       if (s.cell >= 0 && P.status[s.cell] == 0) {
         double yh;
-        if (s.cell < P.k) {
+        if (s.cell < P.kp) {
           yh = ttft_pred(P.a1[s.cell], P.c1[s.cell], s.x1);
         } else {
-          int o = s.cell - P.k;
+          int o = s.cell - P.kp;
           yh = itl_pred(P.a2[o], P.b2[o], P.c2[o], s.x1, s.x2);
         }
         v[0] = fabs(sub(s.y, yh));
@@ -187,26 +191,30 @@ __global__ void fit_solve_kernel(const __grid_constant__ FitParams P) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int K = P.k, T = P.n_tiles;
   if (t >= 2 * K) return;
-  if (t < K) {
-    const int c = t;
-    const double *m = P.means + 3 * (size_t)c;
-    const double *r = P.red + 5 * (size_t)c;
-    double a = 0.0, cc = 0.0;
-    uint8_t st;
-    const double s11 = r[0], s1y = r[4];
-    if (P.cnt[c] == 0) st = 2;
-    else if (P.cnt[c] < 2 || !(s11 > 0.0)) st = 3;   // A31
-    else {
-      a = div(s1y, s11);
-      cc = sub(m[2], mul(a, m[0]));
-      st = 0;
+  if (t < K) {  // TTFT level t over prefill tiles jp = 0..T_p-1 (empty jp > 0 inherits jp-1, F2)
+    for (int jp = 0; jp < P.n_ptiles; ++jp) {
+      const int c = jp * K + t;
+      const double *m = P.means + 3 * (size_t)c;
+      const double *r = P.red + 5 * (size_t)c;
+      double a = 0.0, cc = 0.0;
+      uint8_t st;
+      const double s11 = r[0], s1y = r[4];
+      if (P.cnt[c] == 0) {
+        if (jp == 0) st = 2;
+        else { a = P.a1[c - K]; cc = add(P.c1[c - K], P.tile_step); st = 1; }
+      } else if (P.cnt[c] < 2 || !(s11 > 0.0)) st = 3;   // A31
+      else {
+        a = div(s1y, s11);
+        cc = sub(m[2], mul(a, m[0]));
+        st = 0;
+      }
+      P.a1[c] = a; P.c1[c] = cc; P.status[c] = st;
     }
-    P.a1[c] = a; P.c1[c] = cc; P.status[c] = st;
     return;
   }
   const int k = t - K;
   for (int j = 0; j < T; ++j) {
-    const int c = K + j * K + k, o = j * K + k;
+    const int c = P.kp + j * K + k, o = j * K + k;
     const double *m = P.means + 3 * (size_t)c;
     const double *r = P.red + 5 * (size_t)c;
     double a = 0.0, b = 0.0, cc = 0.0;

@@ -124,6 +124,8 @@ struct WarpSmem {
   // ---- scenario constants
   double tau, slo_itl, tgt_itl, slo_ttft, tgt_ttft, p_idle, tdp, uh_p, uh_d;
   const double *a2g, *b2g, *c2g;   // profile ITL tables (when not staged)
+  const double *a1g, *c1g;         // profile TTFT tables [T_p][kp] (read when T_p > 1, F1)
+  uint32_t ptiles, pcut;           // prefill tiles T_p (>= 1), cutoff
   uint32_t kvcap, max_steps, B, K, T, W, kp, nb;
   int32_t wshift;
   uint32_t itl_smem, mono_tt, mono_it;
@@ -166,8 +168,12 @@ __device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, d
   return add(add(mul(__ldg(W.a2g + o), dn), mul(__ldg(W.b2g + o), dkv)), __ldg(W.c2g + o));
 }
 
+template <bool F>
 __device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt) {
-  return ttft_pred(W.tt[2 * k], W.tt[2 * k + 1], nbt);
+  if (F || W.ptiles <= 1u) return ttft_pred(W.tt[2 * k], W.tt[2 * k + 1], nbt);
+  // prefill tiles (F1): the batch's tile row of the profile tables
+  const size_t o = (size_t)ptile_of(nbt, W.W, W.ptiles, W.pcut) * W.kp + W.lad[k];
+  return ttft_pred(__ldg(W.a1g + o), __ldg(W.c1g + o), nbt);
 }
 
 // Lowest ladder index whose prediction meets `target` (A1), else K-1 (A2);
@@ -203,17 +209,17 @@ __device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
     int lo = 0, hi = K;
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (ttft_at(W, mid, nbt) <= budget) hi = mid; else lo = mid + 1;
+      if (ttft_at<F>(W, mid, nbt) <= budget) hi = mid; else lo = mid + 1;
     }
     const int k = lo < K ? lo : K - 1;
-    *pred = ttft_at(W, k, nbt);
+    *pred = ttft_at<F>(W, k, nbt);
     return k;
   }
   for (int k = 0; k < K - 1; ++k) {
-    const double p = ttft_at(W, k, nbt);
+    const double p = ttft_at<F>(W, k, nbt);
     if (p <= budget) { *pred = p; return k; }
   }
-  *pred = ttft_at(W, K - 1, nbt);
+  *pred = ttft_at<F>(W, K - 1, nbt);
   return K - 1;
 }
 
@@ -238,17 +244,18 @@ __device__ int energy_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double tar
   return best;
 }
 
+template <bool F>
 __device__ int energy_ttft(const WarpSmem &W, uint32_t nbt, double budget, double *pred) {
   const int K = (int)W.K;
   int best = -1;
   double be = 0.0, bt = 0.0;
   for (int k = 0; k < K; ++k) {
-    const double t = ttft_at(W, k, nbt);
+    const double t = ttft_at<F>(W, k, nbt);
     if (!(t <= budget)) continue;
     const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), t);
     if (best < 0 || e < be) { best = k; be = e; bt = t; }
   }
-  if (best < 0) { best = K - 1; bt = ttft_at(W, K - 1, nbt); }
+  if (best < 0) { best = K - 1; bt = ttft_at<F>(W, K - 1, nbt); }
   *pred = bt;
   return best;
 }
@@ -610,11 +617,11 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
     uint32_t fl = backlog ? 4u : 0u;
     if (EN && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)cur;
-      dur = ttft_at(W, k, nbt);
+      dur = ttft_at<F>(W, k, nbt);
     } else {
       fl |= 1u;
-      if (backlog) { k = (int)K - 1; dur = ttft_at(W, k, nbt); }
-      else if (EN && W.ctrl) k = energy_ttft(W, nbt, budget, &dur);  // B4
+      if (backlog) { k = (int)K - 1; dur = ttft_at<F>(W, k, nbt); }
+      else if (EN && W.ctrl) k = energy_ttft<F>(W, nbt, budget, &dur);  // B4
       else k = lowest_ttft<F>(W, nbt, budget, &dur);
       h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
       if (EN) { last = ts; ndec++; }
@@ -742,6 +749,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.tgt_ttft = mul(SL.scale, SL.ttft_ms);
     W.p_idle = PR.p_idle; W.tdp = PR.tdp; W.uh_p = PR.uh[0]; W.uh_d = PR.uh[1];
     W.a2g = PR.a2; W.b2g = PR.b2; W.c2g = PR.c2;
+    W.a1g = PR.a1; W.c1g = PR.c1; W.ptiles = (uint32_t)PR.n_ptiles; W.pcut = PR.pcut;
     W.kvcap = LY.kv_capacity; W.max_steps = tok_total; W.B = LY.max_batch_tokens;
     W.K = K; W.T = T; W.W = (uint32_t)PR.tile_w; W.kp = (uint32_t)PR.k; W.nb = P.nb;
     W.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
@@ -786,7 +794,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       const size_t o0 = (size_t)j * PR.k + GR.level[k], o1 = (size_t)j * PR.k + GR.level[k + 1];
       mi = mi && PR.a2[o1] <= PR.a2[o0] && PR.b2[o1] <= PR.b2[o0] && PR.c2[o1] <= PR.c2[o0];
     }
-    mt = __all_sync(gmask(), mt);
+    mt = __all_sync(gmask(), mt) && PR.n_ptiles <= 1;  // tiled TTFT: the ascending scan (F1)
     mi = __all_sync(gmask(), mi);
     if (lane == 0) { W.mono_tt = mt; W.mono_it = mi; }
   }

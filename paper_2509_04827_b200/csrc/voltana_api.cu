@@ -48,6 +48,10 @@ voltana_status check_profile(const voltana_profile *p, const char *what) {
   if (p->n_tiles < 1 || p->n_tiles > 64)
     return fail(VOLTANA_E_INVALID_ARG, "%s: profile.n_tiles=%d outside 1..64", what, p->n_tiles);
   if (p->tile_w < 1) return fail(VOLTANA_E_INVALID_ARG, "%s: profile.tile_w=%d < 1", what, p->tile_w);
+  if (p->n_ptiles < 0 || p->n_ptiles > 64)
+    return fail(VOLTANA_E_INVALID_ARG, "%s: profile.n_ptiles=%d outside 0..64", what, p->n_ptiles);
+  if (p->n_ptiles > 1 && p->prefill_cutoff < p->tile_w)
+    return fail(VOLTANA_E_INVALID_ARG, "%s: profile.prefill_cutoff=%d < tile_w (S:100)", what, p->prefill_cutoff);
   if (!p->mhz || !p->a1 || !p->c1 || !p->a2 || !p->b2 || !p->c2 || !p->dyn)
     return fail(VOLTANA_E_INVALID_ARG, "%s: profile table pointer is null", what);
   if (!std::isfinite(p->p_idle) || !std::isfinite(p->tdp) || !(p->u_half_prefill > 0) || !(p->u_half_decode > 0))
@@ -123,7 +127,7 @@ voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, in
   P.load = load; P.n_kv = n_kv; P.queue_len = queue_len; P.wait = wait_ms; P.target = target_ms;
   P.n = n; P.out_level = out_level; P.out_status = out_status;
   P.mode = mode;
-  cudaError_t e = launch_control(P, phase, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles),
+  cudaError_t e = launch_control(P, phase, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles, prof_h->n_ptiles),
                                  (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "control_step launch");
   g_launches = 1;
@@ -153,7 +157,7 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
   P.n_d = n_d; P.policy = policy; P.delta = delta_mhz;
   P.n_req = n_req; P.n_kv = n_kv; P.req_in = req_in; P.target = itl_target_ms; P.cursor = cursor;
   P.n = n; P.out_instance = out_instance; P.out_case = out_case; P.out_status = out_status;
-  cudaError_t e = launch_route(P, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles), (cudaStream_t)stream);
+  cudaError_t e = launch_route(P, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles, prof_h->n_ptiles), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "route_batch launch");
   g_launches = 1;
   return ok();
@@ -163,9 +167,9 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
 namespace {
 struct FitLayout { int cells, wpb, blocks; size_t chunk, part, red, means, cnt, total; };
 
-FitLayout fit_layout(size_t n, int k, int n_tiles) {
+FitLayout fit_layout(size_t n, int k, int n_tiles, int n_ptiles) {
   FitLayout L;
-  L.cells = k + n_tiles * k;
+  L.cells = (n_ptiles < 1 ? 1 : n_ptiles) * k + n_tiles * k;
   L.wpb = fit_warps_per_block(L.cells);
   size_t warps_want = (n + 2047) / 2048;               // >= 2048 samples per warp
   size_t cap = (size_t)sm_count() * 2 * L.wpb;         // two CTAs per SM at most
@@ -184,25 +188,27 @@ FitLayout fit_layout(size_t n, int k, int n_tiles) {
 }
 }  // namespace
 
-size_t voltana_fit_workspace_bytes(size_t n_samples, int k, int n_tiles) {
-  if (k < 1 || n_tiles < 1) return 0;
-  return fit_layout(n_samples, k, n_tiles).total;
+size_t voltana_fit_workspace_bytes(size_t n_samples, int k, int n_tiles, int n_ptiles) {
+  if (k < 1 || n_tiles < 1 || n_ptiles < 1) return 0;
+  return fit_layout(n_samples, k, n_tiles, n_ptiles).total;
 }
 
 voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, const uint32_t *n_bt,
                                    const uint32_t *n_req, const uint32_t *n_kv, const double *lat_ms, size_t n,
-                                   int k, int n_tiles, int tile_w, double tile_step, double *a1, double *c1,
+                                   int k, int n_tiles, int tile_w, double tile_step, int n_ptiles,
+                                   uint32_t prefill_cutoff, double *a1, double *c1,
                                    double *a2, double *b2, double *c2, double *mae, uint8_t *cell_status,
                                    uint64_t *invalid_count, void *workspace, size_t ws_bytes, void *stream) {
   g_launches = 0;
   if (k < 1 || k > 1024 || n_tiles < 1 || n_tiles > 64 || tile_w < 1)
     return fail(VOLTANA_E_INVALID_ARG, "fit_profile: k=%d n_tiles=%d tile_w=%d", k, n_tiles, tile_w);
+  if (n_ptiles < 1 || n_ptiles > 64) return fail(VOLTANA_E_INVALID_ARG, "fit_profile: n_ptiles=%d (1..64)", n_ptiles);
   if (!a1 || !c1 || !a2 || !b2 || !c2 || !mae || !cell_status)
     return fail(VOLTANA_E_INVALID_ARG, "fit_profile: null output pointer");
   if (n > 0 && (!phase || !level || !n_bt || !n_req || !n_kv || !lat_ms))
     return fail(VOLTANA_E_INVALID_ARG, "fit_profile: null sample pointer");
   if (!std::isfinite(tile_step)) return fail(VOLTANA_E_INVALID_ARG, "fit_profile: tile_step not finite");
-  FitLayout L = fit_layout(n, k, n_tiles);
+  FitLayout L = fit_layout(n, k, n_tiles, n_ptiles);
   if (L.cells * 5 * sizeof(double) * (size_t)L.wpb > 227 * 1024)
     return fail(VOLTANA_E_INVALID_ARG, "fit_profile: %d cells exceed shared memory", L.cells);
   if (!workspace || ws_bytes < L.total)
@@ -212,6 +218,7 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, 
   P.phase = phase; P.level = level; P.n_bt = n_bt; P.n_req = n_req; P.n_kv = n_kv; P.lat = lat_ms;
   P.n = n; P.chunk = L.chunk; P.k = k; P.n_tiles = n_tiles; P.tile_w = tile_w; P.cells = L.cells;
   P.tile_step = tile_step;
+  P.n_ptiles = n_ptiles; P.kp = n_ptiles * k; P.pcut = prefill_cutoff;
   P.a1 = a1; P.c1 = c1; P.a2 = a2; P.b2 = b2; P.c2 = c2; P.mae = mae; P.status = cell_status;
   P.invalid_count = invalid_count;
   char *ws = (char *)workspace;
@@ -440,7 +447,8 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   }
   energy = energy || P->o.req_offset != nullptr || P->o.iter_offset != nullptr;  // outputs (E1-E3)
   bool fast = L.itl_smem && kmax <= 8;
-  for (int i = 0; i < n_profiles; ++i) fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0;
+  for (int i = 0; i < n_profiles; ++i)
+    fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0 && profiles_h[i].n_ptiles <= 1;
   e = launch_sim(*P, energy, fast, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");

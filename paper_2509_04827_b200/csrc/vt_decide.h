@@ -40,7 +40,7 @@ struct RouteParams {
   uint8_t *out_case, *out_status;
 };
 
-size_t decide_smem_bytes(int k, int n_tiles);
+size_t decide_smem_bytes(int k, int n_tiles, int n_ptiles);
 cudaError_t launch_control(const ControlParams &P, int phase, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_route(const RouteParams &P, int grid, size_t smem, cudaStream_t st);
 

@@ -22,15 +22,17 @@ __device__ __forceinline__ double div(double a, double b) { return __ddiv_rn(a, 
 
 // Device-side copy of one profile (kernel parameter / constant bank).
 struct DevProfile {
-  int32_t k, n_tiles, tile_w, pad;
+  int32_t k, n_tiles, tile_w, n_ptiles;  // n_ptiles >= 1 (prefill tiles, F1)
   const int32_t *mhz;
   const double *a1, *c1, *a2, *b2, *c2, *dyn;
   double p_idle, tdp, uh[2];
+  uint32_t pcut, pad;                    // prefill cutoff (N_bt above it: the last prefill tile)
 };
 
 __host__ __device__ inline DevProfile to_dev(const voltana_profile &p) {
   DevProfile d;
-  d.k = p.k; d.n_tiles = p.n_tiles; d.tile_w = p.tile_w; d.pad = 0;
+  d.k = p.k; d.n_tiles = p.n_tiles; d.tile_w = p.tile_w; d.n_ptiles = p.n_ptiles < 1 ? 1 : p.n_ptiles;
+  d.pcut = p.prefill_cutoff < 0 ? 0u : (uint32_t)p.prefill_cutoff; d.pad = 0;
   d.mhz = p.mhz; d.a1 = p.a1; d.c1 = p.c1; d.a2 = p.a2; d.b2 = p.b2; d.c2 = p.c2; d.dyn = p.dyn;
   d.p_idle = p.p_idle; d.tdp = p.tdp; d.uh[0] = p.u_half_prefill; d.uh[1] = p.u_half_decode;
   return d;
@@ -40,6 +42,15 @@ __host__ __device__ inline DevProfile to_dev(const voltana_profile &p) {
 __device__ __forceinline__ uint32_t tile_of(uint32_t n_req, uint32_t tile_w, uint32_t n_tiles) {
   uint32_t j = (n_req - 1u) / tile_w;
   return j < n_tiles - 1u ? j : n_tiles - 1u;
+}
+
+// prefill tile (Appendix B; F1): one tile, or N_bt above the cutoff -> the last,
+// else min(T_p - 1, (N_bt - 1) / W)
+__device__ __forceinline__ uint32_t ptile_of(uint32_t n_bt, uint32_t tile_w, uint32_t n_ptiles, uint32_t pcut) {
+  if (n_ptiles <= 1u) return 0u;
+  if (n_bt > pcut) return n_ptiles - 1u;
+  const uint32_t j = (n_bt - 1u) / tile_w;
+  return j < n_ptiles - 1u ? j : n_ptiles - 1u;
 }
 
 // eq:pred-ttft: (a1 * N_bt) + c1

@@ -43,6 +43,8 @@ class Profile:
     tile_w: int
     n_tiles: int
     params: dict = field(default_factory=dict)
+    n_ptiles: int = 1              # prefill tiles (Appendix B); a1/c1 are [n_ptiles*K]
+    prefill_cutoff: int = 2000     # N_bt above which prefill is the last (linear) tile
 
     @property
     def k(self) -> int:
@@ -87,8 +89,13 @@ def _params(kind: str) -> dict:
     raise ValueError(kind)
 
 
-def make_profile(kind: str, **overrides) -> Profile:
-    """Build the tables of a named profile (L8, L8_LINEAR, Q32, B200)."""
+def make_profile(kind: str, prefill_tiles: bool = False, **overrides) -> Profile:
+    """Build the tables of a named profile (L8, L8_LINEAR, Q32, B200).
+
+    prefill_tiles: TTFT coefficients per prefill tile (Appendix B): below
+    the 2000-token cutoff one tile per W = 128 batched tokens with the intercept stepping up
+    by dc1 per tile (a staircase like decode's, `fig:ttft_vs_tokens-small`), above it one
+    linear tile continuing from the last step."""
     p = _params(kind)
     p.update(overrides)
     mhz = np.arange(p["f_lo"], p["f_hi"] + 1, p["step"], dtype=np.int32)
@@ -105,8 +112,15 @@ def make_profile(kind: str, **overrides) -> Profile:
     span = p["tdp"] - p["p_idle"]
     dyn = np.concatenate([p["ps_prefill"] * span * xr, p["ps_decode"] * span * xr])
     assert a2.shape == (T * K,) and dyn.shape == (2 * K,)
+    tp, cutoff = 1, int(p.get("prefill_cutoff", 2000))
+    if prefill_tiles:
+        W = int(p["tile_w"])
+        tp = -(-cutoff // W) + 1                        # ceil(cutoff / W) small tiles + the large one
+        dc1 = p.get("dc1", 0.1 * p["c1"]) * rm          # memory-bound like c1
+        a1 = np.tile(a1, tp)
+        c1 = np.concatenate([c1 + jp * dc1 for jp in range(tp)])
     return Profile(kind, mhz, a1, c1, a2, b2, c2, dyn, float(p["p_idle"]), float(p["tdp"]),
-                   float(p["uh_prefill"]), float(p["uh_decode"]), int(p["tile_w"]), T, p)
+                   float(p["uh_prefill"]), float(p["uh_decode"]), int(p["tile_w"]), T, p, tp, cutoff)
 
 
 def custom_profile(mhz, a1, c1, a2, b2, c2, dyn, *, p_idle=60.0, tdp=400.0,

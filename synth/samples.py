@@ -26,12 +26,21 @@ def profile_samples(prof: Profile, n_ttft_per_level: int = 64, n_itl_per_cell: i
     levels = range(K) if levels is None else levels
     tiles = range(T) if tiles is None else tiles
     ph, lv, nbt, nreq, nkv, lat = [], [], [], [], [], []
+    tp, cut = getattr(prof, "n_ptiles", 1), getattr(prof, "prefill_cutoff", 2000)
     for k in levels:
-        x = rng.integers(1, max_nbt + 1, n_ttft_per_level)
-        y = prof.a1[k] * x + prof.c1[k]
-        ph.append(np.zeros(len(x), np.uint8)); lv.append(np.full(len(x), k, np.uint16))
-        nbt.append(x); nreq.append(np.zeros(len(x), np.int64)); nkv.append(np.zeros(len(x), np.int64))
-        lat.append(y)
+        for jp in range(tp):   # one prefill tile (tp = 1) covers [1, max_nbt]
+            if tp == 1:
+                lo, hi = 1, max_nbt
+            elif jp == tp - 1:
+                lo, hi = cut + 1, max(max_nbt, cut + 2)
+            else:
+                lo, hi = jp * W + 1, min((jp + 1) * W, cut)
+            x = rng.integers(lo, hi + 1, n_ttft_per_level)
+            o = jp * K + k
+            y = prof.a1[o] * x + prof.c1[o]
+            ph.append(np.zeros(len(x), np.uint8)); lv.append(np.full(len(x), k, np.uint16))
+            nbt.append(x); nreq.append(np.zeros(len(x), np.int64)); nkv.append(np.zeros(len(x), np.int64))
+            lat.append(y)
         for j in tiles:
             lo = j * W + 1
             hi = (j + 1) * W if j < T - 1 else T * W + 2 * W

@@ -67,9 +67,9 @@ def test_host_validation_errors(vt):
     lad = np.array([0, 2], np.uint16)
     rc = L.voltana_route_batch(C.byref(p), lad.ctypes.data, 2, 9, 1, 1, 1, 1, 150, 0, 1, 10, 1, 1, 1, None)
     assert rc == 5
-    rc = L.voltana_fit_profile(1, 1, 1, 1, 1, 1, 100, 0, 1, 128, 0.0, 1, 1, 1, 1, 1, 1, 1, None, None, 0, None)
+    rc = L.voltana_fit_profile(1, 1, 1, 1, 1, 1, 100, 0, 1, 128, 0.0, 1, 2000, 1, 1, 1, 1, 1, 1, 1, None, None, 0, None)
     assert rc == 1
-    rc = L.voltana_fit_profile(1, 1, 1, 1, 1, 1, 100, 3, 1, 128, 0.0, 1, 1, 1, 1, 1, 1, 1, None, None, 0, None)
+    rc = L.voltana_fit_profile(1, 1, 1, 1, 1, 1, 100, 3, 1, 128, 0.0, 1, 2000, 1, 1, 1, 1, 1, 1, 1, None, None, 0, None)
     assert rc == 6
 
 

@@ -188,6 +188,21 @@ def test_simulate_c4_full_size_sampled(vt, orc):
     compare_records(g[idx], orc.simulate_workload(w, idx))
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name,n_sample", [("C2", 16), ("C3", 16), ("C5", 12)])
+def test_simulate_full_size_sampled(vt, orc, name, n_sample):
+    """The other BASELINE configs at full size in one launch each (C5: 16384 scenarios, 4P4D,
+    60-level ladder, the general-table instantiation): invariants on every record, a spread
+    sample against the oracle."""
+    w = synth.build_config(name)
+    g = gpu_records(vt, w)
+    assert (g["status"] == 0).all()
+    assert (g["n_requests"] == w.traces.lengths()[w.scen["trace_id"]]).all()
+    assert (g["n_ttft_ok"] <= g["n_requests"]).all() and (g["n_both_ok"] <= g["n_itl_ok"]).all()
+    idx = np.unique(np.linspace(0, w.n - 1, n_sample).round().astype(int))
+    compare_records(g[idx], orc.simulate_workload(w, idx))
+
+
 def _one(vt, orc, arrival, inl, outl, D, prof, slo, lay, grid, seed=7):
     w = single_trace_workload(arrival, inl, outl, D, prof, slo, lay, grid, hash_seed=seed)
     g = gpu_records(vt, w)

@@ -806,6 +806,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   uint32_t p_head = NIL;
   if (lane < NP) prefill_lane<EN, F>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
   __syncwarp(gmask());
+#ifdef VT_PHASE_TIMING
+  if (P.timing && glane() == 0) {  // experiment: phase-A end time replaces the start stamp
+    uint64_t ta;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ta));
+    P.timing[2 * s] = ta;
+  }
+#endif
 
   // ================================================================ PHASE B: routing + decode lanes
   const int dl = lane < ND ? lane : 0;
@@ -1100,7 +1107,11 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
       uint32_t sm;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+#ifdef VT_PHASE_TIMING
+      P.timing[2 * s] -= t0;       // phase-A duration (ns)
+#else
       P.timing[2 * s] = t0;
+#endif
       P.timing[2 * s + 1] = (t1 - t0) | ((uint64_t)sm << 56);
     }
   }

@@ -320,7 +320,9 @@ def run_ours(args):
         x = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         e2e_ms = float(x.item())
-        e2e_steps_total *= world
+        y = torch.tensor([e2e_steps_total], dtype=torch.int64, device=dev)   # ranks sweep different seeds
+        dist.all_reduce(y, op=dist.ReduceOp.SUM)
+        e2e_steps_total = int(y.item())
     e2e = {"value": e2e_steps_total / (e2e_ms / 1000.0), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(d2h),
            "path": "DeviceWorkload.stage_inputs (pinned H2D of traces+scenario tables) -> fit_profile -> "

@@ -61,6 +61,9 @@
 #ifndef VT_PIPE_ARGMIN
 #define VT_PIPE_ARGMIN 0  // select the next request right after advancing the stream (overlap)
 #endif
+#ifndef VT_PF
+#define VT_PF 2        // software prefetch: 1 next stream line, 2 + the queue head admission bucket (3, 4: measured no gain)
+#endif
 #ifndef VT_ITL_SMEM_ONLY
 #define VT_ITL_SMEM_ONLY 0  // experiment: assume the ITL table is staged (no global fallback)
 #endif
@@ -90,6 +93,8 @@ __device__ __forceinline__ void wst(uint4 *a, uint4 v) {
   *a = v;
 #endif
 }
+
+__device__ __forceinline__ void prefetch_l1(const void *p) { asm volatile("prefetch.global.L1 [%0];" :: "l"(p)); }
 
 // ---- scenario groups: SPW scenarios per warp, GS lanes each; every collective is group-masked
 constexpr int GS = 32 / SPW;
@@ -287,6 +292,9 @@ struct Dec {               // decode instance d, owned by lane d
 #if VT_BHPF
   uint32_t bh_fin;
   uint4 bh;
+#endif
+#if VT_PF >= 4
+  uint32_t nxh;            // head (+1) of the next iteration's bucket as read one START early (prefetch only)
 #endif
 };
 
@@ -500,6 +508,15 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     D.cur = D.iters;
     D.iters += 1u;
     D.bcur = wld(L.wheel + (D.cur & nbm));  // final now: read at the END of this iteration
+#if VT_PF >= 4
+    // the completion list of this iteration was (most likely) known one START ago: pull its
+    // head node towards L1 for the ITL walk at END; then peek at the next iteration's bucket
+    if (D.nxh != 0u) prefetch_l1(L.node + (D.nxh - 1u));
+    D.nxh = L.wheel[(D.cur + 1u) & nbm].x;
+#endif
+#if VT_PF >= 3
+    if (D.qh != NIL) prefetch_l1(L.wheel + ((D.iters + (uint32_t)queue_head(D, L).out - 2u) & nbm));
+#endif
 #if VT_BHPF
     if (D.qh != NIL) {
       D.bh_fin = D.iters + (uint32_t)queue_head(D, L).out - 2u;
@@ -513,12 +530,15 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
 
 // Append request i (routed at its first-token time) to instance d's admission queue.
 __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, double tf, uint32_t in,
-                                         uint32_t out) {
+                                         uint32_t out, uint32_t nbm) {
   D.pn += 1u;
   D.pkv += in + 1u;
   L.node[i].next = NIL;
   if (D.qt == NIL) {
     D.qh = i;
+#if VT_PF >= 2
+    prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // its bucket at the next START
+#endif
 #if VT_QCACHE
     D.qhn.tf = tf; D.qhn.next = NIL; D.qhn.in = (uint16_t)in; D.qhn.out = (uint16_t)out;
 #endif
@@ -838,6 +858,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
   }
   D.bcur = make_uint4(0u, 0u, 0u, 0u);
+#if VT_PF >= 4
+  D.nxh = 0u;
+#endif
 #if VT_QCACHE
   D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.in = 0; D.qhn.out = 0;
 #endif
@@ -878,7 +901,12 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     if (lane == w) {                                  // advance that stream; prefetch one further
       hd = hn.next;
       hn = nn;
-      if (hd != NIL && hn.next != NIL) nn = node[hn.next];
+      if (hd != NIL && hn.next != NIL) {
+        nn = node[hn.next];
+#if VT_PF >= 1
+        prefetch_l1(node + hn.next + 8u);  // the stream's next line (ids advance by N_P)
+#endif
+      }
     }
 #if VT_PIPE_ARGMIN
     // the next request depends only on the stream heads: its selection overlaps this route
@@ -977,7 +1005,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     if (lane == dsel) {
       if (eco) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
       if (ens) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_en = en_new; }
-      dec_push(D, L, i, tf_i, in_i, io >> 16);
+      dec_push(D, L, i, tf_i, in_i, io >> 16, W.nb - 1u);
       if (EN && W.rq_on) { P.o.req_decode[W.rq_base + i] = (uint8_t)dsel; P.o.req_case[W.rq_base + i] = (uint8_t)cse; }
     }
 #if VT_PIPE_ARGMIN

@@ -64,6 +64,9 @@
 #ifndef VT_PF
 #define VT_PF 2        // software prefetch: 1 next stream line, 2 + the queue head admission bucket (3, 4: measured no gain)
 #endif
+#ifndef VT_PFA
+#define VT_PFA 0       // prefill lanes: prefetch the trace this many requests ahead (0 = off)
+#endif
 #ifndef VT_ITL_SMEM_ONLY
 #define VT_ITL_SMEM_ONLY 0  // experiment: assume the ITL table is staged (no global fallback)
 #endif
@@ -608,6 +611,13 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   Node pend;
   pend.tf = 0.0; pend.next = NIL; pend.in = 0; pend.out = 0;
   while (nxt < N) {
+#if VT_PFA
+    if (nxt + VT_PFA < N) {  // the trace stream ahead of the batch being formed
+      prefetch_l1(arr + nxt + VT_PFA);
+      prefetch_l1(inl + nxt + VT_PFA);
+      prefetch_l1(outl + nxt + VT_PFA);
+    }
+#endif
     const double a0 = arr[nxt];
     const double ts = tfree > a0 ? tfree : a0;  // START: instance idle and queue non-empty
     // FCFS prefix of the arrived queue with sum(in) <= B, at least one request (A6)

@@ -342,17 +342,22 @@ def run_ours(args):
     comp_bytes = trace_bytes + 128 * wl.n
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    traffic = None
+    traffic, ncu_k4 = None, {}
     tj = os.path.join(ROOT, "profiles", "ncu_traffic.json")   # committed summary of one ncu --set full capture
     if os.path.exists(tj):
-        traffic = json.load(open(tj)).get("simulate_kernel", {}).get("dram_bytes_per_launch")
+        ncu_k4 = json.load(open(tj)).get("simulate_kernel", {})
+        traffic = ncu_k4.get("dram_bytes_per_launch")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
             "traffic": traffic, "kernel": "vt::simulate_kernel",
             "note": "algorithmic FP64 ops of the decision procedure (prefill ctrl 2K, decode ctrl 4K, route "
                     "8*N_D*K per decision) / mean kernel time; peak = 148 SM x 64 FP64 lanes x 1965 MHz "
                     "(non-FMA ops); the kernel is latency/issue-bound on the serial event loop",
             "hbm_compulsory": {"bytes": comp_bytes, "gbs": comp_bytes / sim_s / 1e9,
-                               "frac_of_measured_hbm": comp_bytes / sim_s / 1e9 / peaks["hbm_gbs"]}}
+                               "frac_of_measured_hbm": comp_bytes / sim_s / 1e9 / peaks["hbm_gbs"]},
+            "issue": {"issue_active_pct": ncu_k4.get("issue_pct"), "occupancy_pct": ncu_k4.get("occupancy_pct"),
+                      "source": "profiles/ncu_traffic.json (ncu --set full of the same kernel): the limiter is "
+                                "the latency of each scenario's serial chain (stalls: L2/DRAM long scoreboard, "
+                                "fixed-latency dependencies), not FP64 throughput or HBM bandwidth"}}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; DESIGN.md input recipe)",

@@ -52,7 +52,7 @@ def parse():
     return ap.parse_args()
 
 
-def streaming_kernels(vt, torch, dev, hbm_gbs, reps=10):
+def streaming_kernels(vt, torch, dev, hbm_gbs, reps=100):
     """K2 control_step, K3 route_batch and K1 fit_profile on large SoA batches (HBM-bound):
     algorithmic bytes per launch / mean CUDA-event time, against the measured copy bandwidth."""
     import synth
@@ -70,7 +70,8 @@ def streaming_kernels(vt, torch, dev, hbm_gbs, reps=10):
     out = {}
 
     def timed(fn):
-        fn()
+        for _ in range(20):                     # warm-up: clocks and caches settle
+            fn()
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()

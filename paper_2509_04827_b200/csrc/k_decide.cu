@@ -127,8 +127,11 @@ __device__ __forceinline__ int energy_itl(const double *it, const double *dy, co
 }
 
 // ---------------------------------------------------------------- K2 control_step
+#ifndef VT_CTL_MINB
+#define VT_CTL_MINB 8     // 8 CTAs x 8 warps per SM with 2 items per thread: measured best (55 % of HBM)
+#endif
 template <int PHASE>
-__global__ void __launch_bounds__(DECIDE_THREADS)
+__global__ void __launch_bounds__(DECIDE_THREADS, VT_CTL_MINB)
 control_kernel(const __grid_constant__ ControlParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
@@ -188,14 +191,16 @@ control_kernel(const __grid_constant__ ControlParams P) {
 }
 
 // ---------------------------------------------------------------- K3 route_batch
-// One EcoRoute decision on caller-given effective states.
+// One EcoRoute decision on caller-given effective states; NI = the kernel's
+// instance bound (2, 4 or 8), so the per-instance arrays stay in registers at that size.
+template <int NI>
 __device__ __forceinline__ void route_item(const RouteParams &P, const double *it, const double *dy, const int *smi,
                                            int K, int ND, int wshift, uint32_t in, double tgt, uint32_t &cursor,
                                            const uint32_t *n, const uint32_t *kv, uint16_t &dsel, uint8_t &cse,
                                            uint8_t &st) {
   bool bad = cursor >= (uint32_t)ND || in == 0u;
 #pragma unroll
-  for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d)
+  for (int d = 0; d < NI; ++d)
     if (d < ND) bad = bad || kv[d] < n[d];
   dsel = 0xFFFF; cse = 0xFF; st = VOLTANA_ITEM_E_CONTRACT;
   if (bad) return;
@@ -208,11 +213,11 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   }
   unsigned inset = 0;
   if (P.policy == 2) {  // energy-scored router [B1-B3]
-    double score[VOLTANA_MAX_INSTANCES], tmax[VOLTANA_MAX_INSTANCES];
-    bool feas[VOLTANA_MAX_INSTANCES];
+    double score[NI], tmax[NI];
+    bool feas[NI];
     bool any = false;
 #pragma unroll
-    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) {
+    for (int d = 0; d < NI; ++d) {
       score[d] = tmax[d] = 0.0;
       feas[d] = false;
       if (d >= ND) continue;
@@ -240,20 +245,20 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
     double m = 0.0;
     bool first = true;
 #pragma unroll
-    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) {
+    for (int d = 0; d < NI; ++d) {
       if (d >= ND || (any && !feas[d])) continue;
       const double v = any ? score[d] : tmax[d];
       if (first || v < m) { m = v; first = false; }
     }
 #pragma unroll
-    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d)
+    for (int d = 0; d < NI; ++d)
       if (d < ND && (any ? (feas[d] && score[d] == m) : tmax[d] == m)) inset |= 1u << d;
     cse = any ? 6 : 7;
   } else {
-  int fnow[VOLTANA_MAX_INSTANCES], faft[VOLTANA_MAX_INSTANCES];
+  int fnow[NI], faft[NI];
   int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
 #pragma unroll
-  for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) {
+  for (int d = 0; d < NI; ++d) {
     fnow[d] = faft[d] = 0;
     if (d < ND) {
       const int kn = n[d] == 0u ? 0 : scan_itl(it, P.prof, K, n[d], kv[d], tgt, wshift);   // A10, A11
@@ -270,23 +275,23 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   }
   if (ncross == 0) {
 #pragma unroll
-    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
+    for (int d = 0; d < NI; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
     cse = __popc(inset) == 1 ? 1 : 2;
   } else if (ncross < ND) {
     const long long g = (long long)mu - (long long)mr;                                  // A14, A15
     if (g <= (long long)P.delta) {
 #pragma unroll
-      for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d)
+      for (int d = 0; d < NI; ++d)
         if (d < ND && !(faft[d] > fnow[d]) && fnow[d] == mu) inset |= 1u << d;
       cse = 3;
     } else {
 #pragma unroll
-      for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
+      for (int d = 0; d < NI; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
       cse = 4;
     }
   } else {
 #pragma unroll
-    for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) if (d < ND && faft[d] == ma) inset |= 1u << d;
+    for (int d = 0; d < NI; ++d) if (d < ND && faft[d] == ma) inset |= 1u << d;
     cse = 5;
   }
   }
@@ -296,8 +301,14 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   if (__popc(inset) >= 2) cursor = (d + 1u) % (uint32_t)ND;                             // A17
 }
 
+#ifndef VT_ROUTE_MINB
+#define VT_ROUTE_MINB 4   // 4 CTAs x 8 warps per SM (<= 64 registers): measured best with 2 items/thread
+#endif
+#ifndef VT_ROUTE_U2
+#define VT_ROUTE_U2 2     // items per thread per tile when N_D <= 2
+#endif
 template <int ND_MAX>
-__global__ void __launch_bounds__(DECIDE_THREADS)
+__global__ void __launch_bounds__(DECIDE_THREADS, VT_ROUTE_MINB)
 route_kernel(const __grid_constant__ RouteParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
@@ -306,7 +317,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
   const double *it = itl_smem(sm, K, P.prof);
   const double *dy = dyn_smem(sm, K, P.prof);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
-  constexpr int U = ND_MAX <= 2 ? DECIDE_UNROLL : 2;
+  constexpr int U = ND_MAX <= 2 ? VT_ROUTE_U2 : 2;
   const size_t tile = (size_t)blockDim.x * U;
   for (size_t base = (size_t)blockIdx.x * tile; base < P.n; base += (size_t)gridDim.x * tile) {
     uint32_t inv[U], cur[U], n[U][ND_MAX], kv[U][ND_MAX];
@@ -328,15 +339,9 @@ route_kernel(const __grid_constant__ RouteParams P) {
     for (int u = 0; u < U; ++u) {
       const size_t i = base + threadIdx.x + (size_t)u * blockDim.x;
       if (i >= P.n) continue;
-      uint32_t nn[VOLTANA_MAX_INSTANCES], kk[VOLTANA_MAX_INSTANCES];
-#pragma unroll
-      for (int d = 0; d < VOLTANA_MAX_INSTANCES; ++d) {
-        nn[d] = d < ND_MAX ? n[u][d < ND_MAX ? d : 0] : 0u;
-        kk[d] = d < ND_MAX ? kv[u][d < ND_MAX ? d : 0] : 0u;
-      }
       uint16_t dsel;
       uint8_t cse, st;
-      route_item(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], nn, kk, dsel, cse, st);
+      route_item<ND_MAX>(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], n[u], kv[u], dsel, cse, st);
       P.out_instance[i] = dsel;
       P.out_case[i] = cse;
       P.out_status[i] = st;

@@ -10,7 +10,10 @@
 namespace vt {
 
 constexpr int DECIDE_THREADS = 256;
-constexpr int DECIDE_UNROLL = 4;   // items per thread per tile (independent loads in flight)
+#ifndef VT_DECIDE_UNROLL
+#define VT_DECIDE_UNROLL 2
+#endif
+constexpr int DECIDE_UNROLL = VT_DECIDE_UNROLL;  // items per thread per tile (independent loads in flight)
 
 struct LadderParam {
   int32_t k;

@@ -11,6 +11,10 @@
 #include "vt_decide.h"
 #include "vt_device.cuh"
 
+#ifndef VT_ROUTE_LOCKSTEP
+#define VT_ROUTE_LOCKSTEP 0  // K3: the 2*N_D what-if scans of an item advance in lockstep over the levels
+#endif
+
 namespace vt {
 
 // ---------------------------------------------------------------- shared-memory tables
@@ -79,6 +83,11 @@ __device__ __forceinline__ const double *itl_row(const double *it, const DevProf
 
 __device__ __forceinline__ double itl_eval(const double *row, int k, double dn, double dkv) {
   return add(add(mul(row[3 * k], dn), mul(row[3 * k + 1], dkv)), row[3 * k + 2]);
+}
+
+__device__ __forceinline__ uint32_t itl_tile(const DevProfile &PR, uint64_t n, int wshift) {
+  uint64_t j = wshift >= 0 ? (n - 1u) >> wshift : (n - 1u) / (uint64_t)PR.tile_w;
+  return j > (uint64_t)(PR.n_tiles - 1) ? (uint32_t)(PR.n_tiles - 1) : (uint32_t)j;
 }
 
 __device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, int K, uint64_t n,
@@ -257,12 +266,43 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   } else {
   int fnow[NI], faft[NI];
   int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
+#if VT_ROUTE_LOCKSTEP
+  // all 2*N_D what-if scans advance together over the levels (independent evaluations
+  // interleave); each stops at its lowest feasible level exactly like scan_itl
+  int lv[2 * NI], row[2 * NI];
+  double xn[2 * NI], xk[2 * NI];
+  bool dn[2 * NI];
+#pragma unroll
+  for (int q = 0; q < 2 * NI; ++q) {
+    const int d = q >> 1;
+    const uint64_t nn = (uint64_t)n[d < NI ? d : 0] + (q & 1), kk = (uint64_t)kv[d < NI ? d : 0] + ((q & 1) ? in + 1u : 0u);
+    lv[q] = (q & 1) == 0 && nn == 0 ? 0 : K - 1;
+    dn[q] = d >= ND || ((q & 1) == 0 && nn == 0);
+    row[q] = dn[q] ? 0 : 3 * K * (int)itl_tile(P.prof, nn, wshift);
+    xn[q] = (double)nn; xk[q] = (double)kk;
+  }
+  for (int k = 0; k < K - 1; ++k) {
+    bool all = true;
+#pragma unroll
+    for (int q = 0; q < 2 * NI; ++q) {
+      if (dn[q]) continue;
+      const double *r = it + row[q] + 3 * k;
+      if (add(add(mul(r[0], xn[q]), mul(r[1], xk[q])), r[2]) <= tgt) { lv[q] = k; dn[q] = true; }
+      all = all && dn[q];
+    }
+    if (all) break;
+  }
+#endif
 #pragma unroll
   for (int d = 0; d < NI; ++d) {
     fnow[d] = faft[d] = 0;
     if (d < ND) {
+#if VT_ROUTE_LOCKSTEP
+      const int kn = lv[2 * d], ka = lv[2 * d + 1];
+#else
       const int kn = n[d] == 0u ? 0 : scan_itl(it, P.prof, K, n[d], kv[d], tgt, wshift);   // A10, A11
       const int ka = scan_itl(it, P.prof, K, (uint64_t)n[d] + 1u, (uint64_t)kv[d] + in + 1u, tgt, wshift);  // A12
+#endif
       fnow[d] = smi[kn];
       faft[d] = smi[ka];
       const bool cr = faft[d] > fnow[d];                                                 // A13

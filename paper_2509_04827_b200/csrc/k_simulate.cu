@@ -134,6 +134,7 @@ struct WarpSmem {
   const double *a2g, *b2g, *c2g;   // profile ITL tables (when not staged)
   const double *a1g, *c1g;         // profile TTFT tables [T_p][kp] (read when T_p > 1, F1)
   uint32_t ptiles, pcut;           // prefill tiles T_p (>= 1), cutoff
+  const double *ut;                // VT_UTAB: this profile's utilisation tables [2][SIM_UTAB]
   uint32_t kvcap, max_steps, B, K, T, W, kp, nb;
   int32_t wshift;
   uint32_t itl_smem, mono_tt, mono_it;
@@ -231,6 +232,19 @@ __device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
   return K - 1;
 }
 
+// busy power (eq:P-f P:187, A22) with the utilisation from the launch's table when tabulated
+// (VT_UTAB; the entries are the same division, so the value is identical)
+__device__ __forceinline__ double bpow(const WarpSmem &W, int phase, double dyn, uint32_t load) {
+#if VT_UTAB
+  const double uh = phase ? W.uh_d : W.uh_p;
+  const double u = load < SIM_UTAB ? __ldg(W.ut + phase * SIM_UTAB + load) : div((double)load, add((double)load, uh));
+  const double w = add(W.p_idle, mul(u, dyn));
+  return w < W.tdp ? w : W.tdp;
+#else
+  return busy_power(W.p_idle, W.tdp, phase ? W.uh_d : W.uh_p, dyn, load);
+#endif
+}
+
 // Energy-argmin controller [B4]: among the levels meeting the target, the lowest busy
 // energy P(k, load) * T(k) (eq:P-f P:187, energy = time x power P:74); ties -> lower level;
 // none feasible -> K-1 (A2). Full scan (the energy curve is not monotone).
@@ -244,7 +258,7 @@ __device__ int energy_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double tar
   for (int k = 0; k < K; ++k) {
     const double t = itl_at<F>(W, j, k, dn, dkv);
     if (!(t <= target)) continue;
-    const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[K + k], n), t);
+    const double e = mul(bpow(W, 1, W.dyn[K + k], n), t);
     if (best < 0 || e < be) { best = k; be = e; bt = t; }
   }
   if (best < 0) { best = K - 1; bt = itl_at<F>(W, j, K - 1, dn, dkv); }
@@ -260,7 +274,7 @@ __device__ int energy_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
   for (int k = 0; k < K; ++k) {
     const double t = ttft_at<F>(W, k, nbt);
     if (!(t <= budget)) continue;
-    const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), t);
+    const double e = mul(bpow(W, 0, W.dyn[k], nbt), t);
     if (best < 0 || e < be) { best = k; be = e; bt = t; }
   }
   if (best < 0) { best = K - 1; bt = ttft_at<F>(W, K - 1, nbt); }
@@ -505,7 +519,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     }
     D.end = add(t0, dur);
     D.busy = true;
-    ACC(ebusy) = add(ACC(ebusy), mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
+    ACC(ebusy) = add(ACC(ebusy), mul(bpow(W, 1, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
     ACC(bms) = add(ACC(bms), dur);
     if (k == (int)W.K - 1) ACC(top) = add(ACC(top), dur);
     D.cur = D.iters;
@@ -670,7 +684,7 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
       log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
     }
     const double end = add(t0, dur);
-    ebusy = add(ebusy, mul(busy_power(W.p_idle, W.tdp, W.uh_p, W.dyn[k], nbt), dur));  // W*ms (A23)
+    ebusy = add(ebusy, mul(bpow(W, 0, W.dyn[k], nbt), dur));  // W*ms (A23)
     bms = add(bms, dur);
     if (k == (int)K - 1) top = add(top, dur);
     // ---- O5 PrefillDone at `end`, batch in FCFS order
@@ -780,6 +794,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.p_idle = PR.p_idle; W.tdp = PR.tdp; W.uh_p = PR.uh[0]; W.uh_d = PR.uh[1];
     W.a2g = PR.a2; W.b2g = PR.b2; W.c2g = PR.c2;
     W.a1g = PR.a1; W.c1g = PR.c1; W.ptiles = (uint32_t)PR.n_ptiles; W.pcut = PR.pcut;
+    W.ut = VT_UTAB ? P.utab + (size_t)P.profile_id[s] * 2 * SIM_UTAB : nullptr;
     W.kvcap = LY.kv_capacity; W.max_steps = tok_total; W.B = LY.max_batch_tokens;
     W.K = K; W.T = T; W.W = (uint32_t)PR.tile_w; W.kp = (uint32_t)PR.k; W.nb = P.nb;
     W.wshift = (PR.tile_w & (PR.tile_w - 1)) == 0 ? __ffs(PR.tile_w) - 1 : -1;
@@ -940,7 +955,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
           if (n != c_n || kv != c_kv) {
             double pr;
             const int k0 = lowest_itl<F>(W, n, kv, W.tgt_itl, &pr);  // EcoFreq level now (A10/A11)
-            c_en = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k0], n), pr);
+            c_en = mul(bpow(W, 1, W.dyn[W.K + k0], n), pr);
             c_n = n; c_kv = kv;
           }
           enow = c_en;
@@ -952,13 +967,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         for (int k = 0; k < (int)W.K; ++k) {
           t = itl_at<F>(W, j, k, dn, dkv);
           if (!(t <= W.tgt_itl)) continue;
-          const double e = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + k], n1), t);
+          const double e = mul(bpow(W, 1, W.dyn[W.K + k], n1), t);
           if (!feas) en_new = e;                    // the successor's own EcoFreq-level P*T
           if (!feas || e < best) best = e;
           feas = true;
         }
         tmax = t;                                   // T at K-1
-        if (!feas) en_new = mul(busy_power(W.p_idle, W.tdp, W.uh_d, W.dyn[W.K + W.K - 1], n1), tmax);
+        if (!feas) en_new = mul(bpow(W, 1, W.dyn[W.K + W.K - 1], n1), tmax);
         score = sub(best, enow);
       }
       const bool any = gballot(feas) != 0u;
@@ -1156,6 +1171,20 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
 }
 
 size_t sim_smem_fixed() { return (sizeof(WarpSmem) - sizeof(double) + 15) & ~(size_t)15; }
+
+__global__ void utab_kernel(const __grid_constant__ SimParams P) {
+  const uint32_t total = P.n_profiles * 2u * SIM_UTAB;
+  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
+    const uint32_t pr = x / (2u * SIM_UTAB), ph = (x / SIM_UTAB) & 1u, l = x % SIM_UTAB;
+    const double uh = P.prof[pr].uh[ph];
+    ((double *)P.utab)[x] = div((double)l, add((double)l, uh));
+  }
+}
+
+cudaError_t launch_utab(const SimParams &P, cudaStream_t st) {
+  utab_kernel<<<64, 256, 0, st>>>(P);
+  return cudaGetLastError();
+}
 
 const void *sim_kernel_ptr(bool energy, bool fast) {
   if (energy) return fast ? (const void *)simulate_kernel<true, true> : (const void *)simulate_kernel<true, false>;

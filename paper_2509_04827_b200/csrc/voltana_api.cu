@@ -254,7 +254,7 @@ uint32_t wheel_buckets(uint32_t max_out) {
 }
 
 struct SimLayout {
-  size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem;
+  size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
   uint32_t n_slots, nb, itl_smem;
 };
 
@@ -297,6 +297,10 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.slots_off = 256;
   L.wheels_off = align256(L.slots_off + (size_t)L.n_slots * L.slot);
   L.total = L.wheels_off + (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint4);
+#if VT_UTAB
+  L.utab_off = align256(L.total);
+  L.total = L.utab_off + (size_t)MAX_PROFILES * 2 * SIM_UTAB * sizeof(double);
+#endif
   return L;
 }
 
@@ -423,6 +427,9 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->slot_bytes = L.slot;
   P->node_bytes = L.node;
   P->wheels = (uint4 *)(ws + L.wheels_off);
+#if VT_UTAB
+  P->utab = (const double *)(ws + L.utab_off);
+#endif
   P->wheel_per_slot = L.wheel_per_slot;
   P->itl_smem = L.itl_smem;
   P->smem_per_warp = (uint32_t)L.smem_per_warp;
@@ -449,10 +456,14 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   bool fast = L.itl_smem && kmax <= 8;
   for (int i = 0; i < n_profiles; ++i)
     fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0 && profiles_h[i].n_ptiles <= 1;
+#if VT_UTAB
+  e = launch_utab(*P, st);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate utab launch"); }
+#endif
   e = launch_sim(*P, energy, fast, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
-  g_launches = 1;
+  g_launches = 1 + VT_UTAB;
   return ok();
 }
 

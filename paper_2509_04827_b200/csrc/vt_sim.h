@@ -27,6 +27,10 @@ constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in s
 #ifndef VT_NBMAX
 #define VT_NBMAX 1024
 #endif
+#ifndef VT_UTAB
+#define VT_UTAB 1  // utilisation table for busy power (one 1-MB setup launch; measured -0.5 %)
+#endif
+constexpr uint32_t SIM_UTAB = 8192;         // loads with a tabulated utilisation (VT_UTAB)
 constexpr uint32_t SIM_WHEEL_MAX = VT_NBMAX; // decode wheel buckets (L2-resident); longer requests use the far list
 
 struct SimParams {
@@ -56,6 +60,7 @@ struct SimParams {
   uint32_t smem_per_warp;
   uint64_t *timing;            // debug: [n][2] globaltimer ns at scenario start/end | smid<<56 (NULL: off)
   voltana_outputs o;           // optional per-request / per-instance outputs (variant kernel only)
+  const double *utab;          // VT_UTAB: [MAX_PROFILES][2][SIM_UTAB] utilisation u = l / (l + u_half)
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];
@@ -68,5 +73,6 @@ struct SimParams {
 // staged in shared memory, so the general table paths are compiled out.
 const void *sim_kernel_ptr(bool energy, bool fast);
 cudaError_t launch_sim(const SimParams &P, bool energy, bool fast, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_utab(const SimParams &P, cudaStream_t st);  // VT_UTAB: fill P.utab
 
 }  // namespace vt

@@ -310,7 +310,7 @@ struct Dec {               // decode instance d, owned by lane d
   uint32_t bh_fin;
   uint4 bh;
 #endif
-#if VT_PF >= 4
+#if VT_PF == 4
   uint32_t nxh;            // head (+1) of the next iteration's bucket as read one START early (prefetch only)
 #endif
 };
@@ -525,13 +525,13 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     D.cur = D.iters;
     D.iters += 1u;
     D.bcur = wld(L.wheel + (D.cur & nbm));  // final now: read at the END of this iteration
-#if VT_PF >= 4
+#if VT_PF == 4
     // the completion list of this iteration was (most likely) known one START ago: pull its
     // head node towards L1 for the ITL walk at END; then peek at the next iteration's bucket
     if (D.nxh != 0u) prefetch_l1(L.node + (D.nxh - 1u));
     D.nxh = L.wheel[(D.cur + 1u) & nbm].x;
 #endif
-#if VT_PF >= 3
+#if VT_PF == 3 || VT_PF == 4
     if (D.qh != NIL) prefetch_l1(L.wheel + ((D.iters + (uint32_t)queue_head(D, L).out - 2u) & nbm));
 #endif
 #if VT_BHPF
@@ -551,9 +551,12 @@ __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, doub
   D.pn += 1u;
   D.pkv += in + 1u;
   L.node[i].next = NIL;
+#if VT_PF == 5
+  prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // every pushed request's bucket at the next START
+#endif
   if (D.qt == NIL) {
     D.qh = i;
-#if VT_PF >= 2
+#if VT_PF >= 2 && VT_PF != 5
     prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // its bucket at the next START
 #endif
 #if VT_QCACHE
@@ -883,7 +886,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
   }
   D.bcur = make_uint4(0u, 0u, 0u, 0u);
-#if VT_PF >= 4
+#if VT_PF == 4
   D.nxh = 0u;
 #endif
 #if VT_QCACHE

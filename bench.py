@@ -176,19 +176,31 @@ class Clocks:
         self.p = None
 
     def start(self):
+        """Start sampling every 100 ms and return once the first sample is written (so the timed
+        region that follows is covered from its start)."""
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                       "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
                                       stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 10.0 and self.p.poll() is None:
+            self.f.flush()
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.05)
+        self.skip = len(open(self.f.name).read().strip().splitlines())   # samples taken before the region
 
     def stop(self):
         if self.p is None:
             return None
         self.p.terminate()
         self.p.wait()
-        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 8]
+        lines = open(self.f.name).read().strip().splitlines()
+        lines = lines[getattr(self, "skip", 0):] or lines[-1:]       # the timed region's samples
+        rows = [r.split(",") for r in lines if r.count(",") >= 8]
         if not rows:
             return None
         sm = [float(r[1]) for r in rows]

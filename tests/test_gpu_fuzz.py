@@ -44,12 +44,15 @@ def _trace(rng, kind):
 @pytest.mark.parametrize("seed", list(range(1, 11)))
 def test_random_scenarios(vt, orc, seed):
     rng = np.random.default_rng(1000 + seed)
-    profiles = [synth.make_profile("L8"), synth.make_profile("B200"), synth.make_profile("Q32", n_tiles=4),
-                synth.make_profile("L8", prefill_tiles=True)]
+    # even seeds: untiled profiles and K <= 8 (the fast-table kernel); odd seeds: a tiled
+    # profile, and every third seed ladders up to 28 levels (binary search on monotone tables)
+    profiles = [synth.make_profile("L8"), synth.make_profile("B200"), synth.make_profile("Q32", n_tiles=4)]
+    if seed % 2:
+        profiles.append(synth.make_profile("L8", prefill_tiles=True))
+    kmax = 28 if seed % 3 == 0 else 8
     grids = []
     for _ in range(8):
-        p = profiles[int(rng.integers(0, 2))]
-        k = int(rng.integers(1, 9))
+        k = int(rng.integers(1, kmax + 1))
         grids.append(np.sort(rng.choice(min(p.k, 28), k, replace=False)).astype(np.uint16))
     slos = [Slo(float(rng.uniform(50, 2000)), float(rng.uniform(5, 120)), float(rng.choice([1.0, 0.9, 0.75])))
             for _ in range(16)]

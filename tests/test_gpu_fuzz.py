@@ -53,7 +53,7 @@ def test_random_scenarios(vt, orc, seed):
     grids = []
     for _ in range(8):
         k = int(rng.integers(1, kmax + 1))
-        grids.append(np.sort(rng.choice(min(p.k, 28), k, replace=False)).astype(np.uint16))
+        grids.append(np.sort(rng.choice(28, k, replace=False)).astype(np.uint16))
     slos = [Slo(float(rng.uniform(50, 2000)), float(rng.uniform(5, 120)), float(rng.choice([1.0, 0.9, 0.75])))
             for _ in range(16)]
     layouts = []

@@ -380,7 +380,8 @@ def run_ours(args):
                          "all_gather": statistics.mean(t_gather) if world > 1 else 0.0},
            "fit_samples": n_samp, "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roof,
            "cpu_baseline": cpu,
-           "streaming": streaming_kernels(vt, torch, dev, peaks["hbm_gbs"]) if not args.no_streaming else None}
+           "streaming": (streaming_kernels(vt, torch, dev, peaks["hbm_gbs"])
+                         if not args.no_streaming and rank == 0 else None)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

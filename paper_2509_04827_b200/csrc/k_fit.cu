@@ -15,6 +15,10 @@
 #include "vt_device.cuh"
 #include "vt_fit.h"
 
+#ifndef VT_FIT_PF
+#define VT_FIT_PF 8
+#endif
+
 namespace vt {
 
 struct Sample {
@@ -23,15 +27,36 @@ struct Sample {
   double y;
 };
 
-__device__ __forceinline__ Sample load_sample(const FitParams &P, size_t i, bool in_range) {
+// A sample's raw fields: every load is unconditional, so the loads of the chunks ahead issue
+// back to back (a load predicated on another load's value would stall the warp at issue).
+struct Raw {
+  uint8_t ph;
+  uint16_t lv;
+  uint32_t nb, nr, kv;
+  double y;
+  bool in;
+};
+
+__device__ __forceinline__ Raw load_raw(const FitParams &P, size_t i, bool in_range) {
+  Raw r;
+  r.in = in_range;
+  r.ph = 0; r.lv = 0; r.nb = 0; r.nr = 0; r.kv = 0; r.y = 0.0;
+  if (in_range) {  // predicate from the index only: the six loads issue together
+    r.ph = P.phase[i]; r.lv = P.level[i];
+    r.nb = P.n_bt[i]; r.nr = P.n_req[i]; r.kv = P.n_kv[i];
+    r.y = P.lat[i];
+  }
+  return r;
+}
+
+__device__ __forceinline__ Sample decode_sample(const FitParams &P, const Raw &r) {
   Sample s;
   s.cell = -1; s.x1 = 0; s.x2 = 0; s.y = 0.0;
-  if (!in_range) return s;
-  const uint32_t ph = P.phase[i], lv = P.level[i];
-  const uint32_t nr = P.n_req[i];
-  const uint32_t nb = ph == 0u ? P.n_bt[i] : 1u;
+  if (!r.in) return s;
+  const uint32_t ph = r.ph, lv = r.lv, nr = r.nr;
+  const uint32_t nb = ph == 0u ? r.nb : 1u;
   if (ph > 1u || lv >= (uint32_t)P.k || (ph == 1u && nr == 0u) || nb == 0u) { s.cell = -2; return s; }
-  s.y = P.lat[i];
+  s.y = r.y;
   if (ph == 0u) {
     // prefill tile (F1): T_p <= 1 one tile; N_bt above the cutoff the last; else (N_bt-1)/W
     uint32_t jp = 0;
@@ -42,7 +67,7 @@ __device__ __forceinline__ Sample load_sample(const FitParams &P, size_t i, bool
     uint32_t j = tile_of(nr, (uint32_t)P.tile_w, (uint32_t)P.n_tiles);
     s.cell = P.kp + (int)j * P.k + (int)lv;
     s.x1 = nr;
-    s.x2 = P.n_kv[i];
+    s.x2 = r.kv;
   }
   return s;
 }
@@ -61,18 +86,18 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
   const size_t gw = (size_t)blockIdx.x * wpb + wib;
   const size_t lo = gw * P.chunk, hi = lo + P.chunk < P.n ? lo + P.chunk : P.n;
   uint64_t invalid = 0;
-  constexpr int PF = 4;  // 32-sample chunks loaded ahead (processed strictly in order)
-  Sample buf[PF];
+  constexpr int PF = VT_FIT_PF;  // 32-sample chunks loaded ahead (processed strictly in order)
+  Raw buf[PF];
 #pragma unroll
-  for (int u = 0; u < PF; ++u) buf[u] = load_sample(P, lo + (size_t)u * 32 + lane, lo + (size_t)u * 32 + lane < hi);
+  for (int u = 0; u < PF; ++u) buf[u] = load_raw(P, lo + (size_t)u * 32 + lane, lo + (size_t)u * 32 + lane < hi);
   int slot = 0;
   for (size_t base = lo; base < hi; base += 32) {
-    Sample s = buf[0];
+    const Sample s = decode_sample(P, buf[0]);
 #pragma unroll
     for (int u = 0; u + 1 < PF; ++u) buf[u] = buf[u + 1];
     {
       const size_t ni = base + (size_t)PF * 32 + lane;
-      buf[PF - 1] = load_sample(P, ni, ni < hi);
+      buf[PF - 1] = load_raw(P, ni, ni < hi);
     }
     (void)slot;
     if (s.cell == -2) invalid++;

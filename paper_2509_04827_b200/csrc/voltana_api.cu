@@ -171,7 +171,10 @@ FitLayout fit_layout(size_t n, int k, int n_tiles, int n_ptiles) {
   FitLayout L;
   L.cells = (n_ptiles < 1 ? 1 : n_ptiles) * k + n_tiles * k;
   L.wpb = fit_warps_per_block(L.cells);
-  size_t warps_want = (n + 2047) / 2048;               // >= 2048 samples per warp
+#ifndef VT_FIT_SPW
+#define VT_FIT_SPW 2048
+#endif
+  size_t warps_want = (n + VT_FIT_SPW - 1) / VT_FIT_SPW;  // >= VT_FIT_SPW samples per warp
   size_t cap = (size_t)sm_count() * 2 * L.wpb;         // two CTAs per SM at most
   size_t warps = warps_want < 1 ? 1 : (warps_want < cap ? warps_want : cap);
   L.blocks = (int)((warps + L.wpb - 1) / L.wpb);

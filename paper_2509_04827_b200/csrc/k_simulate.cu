@@ -64,6 +64,9 @@
 #ifndef VT_PF
 #define VT_PF 2        // software prefetch: 1 next stream line, 2 + the queue head admission bucket (3, 4: measured no gain)
 #endif
+#ifndef VT_SWHEEL
+#define VT_SWHEEL 0    // near timing-wheel window in shared memory (buckets; power of two, 0 = off)
+#endif
 #ifndef VT_PFA
 #define VT_PFA 0       // prefill lanes: prefetch the trace this many requests ahead (0 = off)
 #endif
@@ -113,11 +116,12 @@ struct Node {       // 16 B per request (workspace)
   uint16_t in, out;
 };
 
-constexpr int ITL_FIFO = 8;  // deferred completion lists per decode lane
+constexpr int ITL_FIFO = VT_ITL_FIFO;  // deferred completion lists per decode lane
 constexpr int NI = VOLTANA_MAX_INSTANCES;
 
 // Per-warp shared-memory block (one scenario at a time). Sized by SIM_SMEM_FIXED.
-struct WarpSmem {
+template <int KC>  // KC: level capacity of the staged tables (8 in the fast-table kernel, else 64)
+struct WarpSmemT {
   // ---- deferred ITL accounting: completion-list heads and times, per decode lane
   uint32_t fid[NI][ITL_FIFO];
   double ft[NI][ITL_FIFO];
@@ -125,10 +129,12 @@ struct WarpSmem {
   double pa_ebusy[NI], pa_bms[NI], pa_top[NI], pa_sttft[NI], pa_tlast[NI], pa_errt[NI];
   uint64_t pa_h[NI];
   uint32_t pa_iters[NI], pa_ttft_ok[NI], pa_itl_ok[NI], pa_both[NI], pa_errc[NI];
+#if VT_DACC_SMEM
   // ---- decode-lane accumulators (VT_DACC_SMEM)
   double da_ebusy[NI], da_bms[NI], da_top[NI], da_sitl[NI], da_tlast[NI];
   uint64_t da_h[NI];
   uint32_t da_n_itl_ok[NI], da_n_both[NI];
+#endif
   // ---- scenario constants
   double tau, slo_itl, tgt_itl, slo_ttft, tgt_ttft, p_idle, tdp, uh_p, uh_d;
   const double *a2g, *b2g, *c2g;   // profile ITL tables (when not staged)
@@ -150,25 +156,25 @@ struct WarpSmem {
   uint32_t dl_cur[NI], dl_ndec[NI];  // decode lane: running level, decisions taken
   uint32_t pa_ndec[NI];            // prefill lane: decisions taken
   // ---- staged ladder tables
-  uint16_t lad[VOLTANA_MAX_LEVELS];
-  int32_t mhz[VOLTANA_MAX_LEVELS];
-  double tt[2 * VOLTANA_MAX_LEVELS];   // [K][2]: a1, c1
-  double dyn[2 * VOLTANA_MAX_LEVELS];  // [2][K]: prefill, decode
+  uint16_t lad[KC];
+  int32_t mhz[KC];
+  double tt[2 * KC];   // [K][2]: a1, c1
+  double dyn[2 * KC];  // [2][K]: prefill, decode
   double it[1];                        // [T][K][3]: a2, b2, c2 (flexible; itl_smem)
 };
 
 // ------------------------------------------------------------------ EcoPred on staged tables
 // F ("fast tables"): the ITL table is staged, K <= 8 and the tile width is a power of two for
 // every scenario of the launch (host-checked): the dead general paths are compiled out.
-template <bool F>
-__device__ __forceinline__ uint32_t tile_j(const WarpSmem &W, uint32_t n) {
+template <bool F, class WS>
+__device__ __forceinline__ uint32_t tile_j(const WS &W, uint32_t n) {
   const uint32_t j = (F || W.wshift >= 0) ? (n - 1u) >> W.wshift : (n - 1u) / W.W;
   return j < W.T - 1u ? j : W.T - 1u;
 }
 
 // eq:pred-itl at ladder index k, tile j; dn = (double)N_req, dkv = (double)N_kv (exact)
-template <bool F>
-__device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, double dn, double dkv) {
+template <bool F, class WS>
+__device__ __forceinline__ double itl_at(const WS &W, uint32_t j, int k, double dn, double dkv) {
   if (F || VT_ITL_SMEM_ONLY || W.itl_smem) {
     const double *r = W.it + 3 * ((size_t)j * W.K + k);
     return add(add(mul(r[0], dn), mul(r[1], dkv)), r[2]);
@@ -177,8 +183,8 @@ __device__ __forceinline__ double itl_at(const WarpSmem &W, uint32_t j, int k, d
   return add(add(mul(__ldg(W.a2g + o), dn), mul(__ldg(W.b2g + o), dkv)), __ldg(W.c2g + o));
 }
 
-template <bool F>
-__device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt) {
+template <bool F, class WS>
+__device__ __forceinline__ double ttft_at(const WS &W, int k, uint32_t nbt) {
   if (F || W.ptiles <= 1u) return ttft_pred(W.tt[2 * k], W.tt[2 * k + 1], nbt);
   // prefill tiles (F1): the batch's tile row of the profile tables
   const size_t o = (size_t)ptile_of(nbt, W.W, W.ptiles, W.pcut) * W.kp + W.lad[k];
@@ -188,8 +194,8 @@ __device__ __forceinline__ double ttft_at(const WarpSmem &W, int k, uint32_t nbt
 // Lowest ladder index whose prediction meets `target` (A1), else K-1 (A2);
 // *pred = the prediction there. Ascending scan with early exit, or an exact binary search
 // when the tables are coefficient-monotone in f (A32).
-template <bool F>
-__device__ int lowest_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
+template <bool F, class WS>
+__device__ int lowest_itl(const WS &W, uint32_t n, uint32_t kv, double target, double *pred) {
   const uint32_t j = tile_j<F>(W, n);
   const int K = (int)W.K;
   const double dn = (double)n, dkv = (double)kv;
@@ -211,8 +217,8 @@ __device__ int lowest_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double tar
   return K - 1;
 }
 
-template <bool F>
-__device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, double *pred) {
+template <bool F, class WS>
+__device__ int lowest_ttft(const WS &W, uint32_t nbt, double budget, double *pred) {
   const int K = (int)W.K;
   if (!F && W.mono_tt && K > 8) {
     int lo = 0, hi = K;
@@ -234,7 +240,8 @@ __device__ int lowest_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
 
 // busy power (eq:P-f P:187, A22) with the utilisation from the launch's table when tabulated
 // (VT_UTAB; the entries are the same division, so the value is identical)
-__device__ __forceinline__ double bpow(const WarpSmem &W, int phase, double dyn, uint32_t load) {
+template <class WS>
+__device__ __forceinline__ double bpow(const WS &W, int phase, double dyn, uint32_t load) {
 #if VT_UTAB
   const double uh = phase ? W.uh_d : W.uh_p;
   const double u = load < SIM_UTAB ? __ldg(W.ut + phase * SIM_UTAB + load) : div((double)load, add((double)load, uh));
@@ -248,8 +255,8 @@ __device__ __forceinline__ double bpow(const WarpSmem &W, int phase, double dyn,
 // Energy-argmin controller [B4]: among the levels meeting the target, the lowest busy
 // energy P(k, load) * T(k) (eq:P-f P:187, energy = time x power P:74); ties -> lower level;
 // none feasible -> K-1 (A2). Full scan (the energy curve is not monotone).
-template <bool F>
-__device__ int energy_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double target, double *pred) {
+template <bool F, class WS>
+__device__ int energy_itl(const WS &W, uint32_t n, uint32_t kv, double target, double *pred) {
   const uint32_t j = tile_j<F>(W, n);
   const int K = (int)W.K;
   const double dn = (double)n, dkv = (double)kv;
@@ -266,8 +273,8 @@ __device__ int energy_itl(const WarpSmem &W, uint32_t n, uint32_t kv, double tar
   return best;
 }
 
-template <bool F>
-__device__ int energy_ttft(const WarpSmem &W, uint32_t nbt, double budget, double *pred) {
+template <bool F, class WS>
+__device__ int energy_ttft(const WS &W, uint32_t nbt, double budget, double *pred) {
   const int K = (int)W.K;
   int best = -1;
   double be = 0.0, bt = 0.0;
@@ -284,7 +291,8 @@ __device__ int energy_ttft(const WarpSmem &W, uint32_t nbt, double budget, doubl
 
 // [D2] execution-noise factor of iteration j of instance inst: counter-based index into the
 // host-drawn table (no transcendental on either side).
-__device__ __forceinline__ double noise_at(const WarpSmem &W, uint64_t inst, uint64_t j) {
+template <class WS>
+__device__ __forceinline__ double noise_at(const WS &W, uint64_t inst, uint64_t j) {
   const uint64_t x = W.seed ^ 0xD1B54A32D192ED03ull ^ (inst << 40) ^ j;
   return __ldg(W.noise + (splitmix64(x) & W.noise_mask));
 }
@@ -316,6 +324,9 @@ struct Dec {               // decode instance d, owned by lane d
 };
 
 struct Lane {              // per-lane pointers
+#if VT_SWHEEL
+  uint4 *sw;               // near wheel in shared memory: buckets [iters, iters + VT_SWHEEL)
+#endif
   Node *node;
   uint32_t *farfin;        // [N] finishing iteration of requests on the far list
   uint4 *wheel;            // this lane's decode instance: [NB] buckets
@@ -333,8 +344,8 @@ __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
 
 // ITL accounting of deferred completion lists, in completion order (A30, A37); the head
 // nodes of up to four lists are loaded together.
-template <bool EN, bool F>
-__device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d, const voltana_outputs &O) {
+template <bool EN, bool F, class WS>
+__device__ void itl_drain(Dec &D, const Lane &L, WS &W, int d, const voltana_outputs &O) {
   const double slo = W.slo_itl;
   for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
     Node h4[4];
@@ -367,7 +378,8 @@ __device__ void itl_drain(Dec &D, const Lane &L, WarpSmem &W, int d, const volta
 }
 
 // iteration record of the per-instance time series (E2)
-__device__ __forceinline__ void log_iter(const voltana_outputs &O, const WarpSmem &W, uint32_t u, uint32_t j,
+template <class WS>
+__device__ __forceinline__ void log_iter(const voltana_outputs &O, const WS &W, uint32_t u, uint32_t j,
                                          double t, double dur, uint32_t load, uint32_t kv, int k, uint32_t flags) {
   if (!W.it_on || j >= O.iter_cap) return;
   voltana_iteration r;
@@ -377,21 +389,36 @@ __device__ __forceinline__ void log_iter(const voltana_outputs &O, const WarpSme
   O.iters[W.it_base + (uint64_t)u * O.iter_cap + j] = r;
 }
 
+// Bucket of finishing iteration fin >= D.iters during a START (before the iteration counter
+// advances): the near window [iters, iters + VT_SWHEEL) lives in shared memory.
+__device__ __forceinline__ uint4 bkt_ld(const Dec &D, const Lane &L, uint32_t nbm, uint32_t fin) {
+#if VT_SWHEEL
+  if (fin - D.iters < (uint32_t)VT_SWHEEL) return L.sw[fin & (VT_SWHEEL - 1)];
+#endif
+  return wld(L.wheel + (fin & nbm));
+}
+__device__ __forceinline__ void bkt_st(const Dec &D, const Lane &L, uint32_t nbm, uint32_t fin, uint4 b) {
+#if VT_SWHEEL
+  if (fin - D.iters < (uint32_t)VT_SWHEEL) { L.sw[fin & (VT_SWHEEL - 1)] = b; return; }
+#endif
+  wst(L.wheel + (fin & nbm), b);
+}
+
 // Append request i (finishing at iteration fin) to its bucket; (lfin, lb) = the bucket
 // written last during this START, kept coherent with the prefetched copy.
 __device__ __forceinline__ void bucket_append(Dec &D, const Lane &L, uint32_t nbm, uint32_t i, uint32_t fin,
                                               uint32_t inout, uint32_t &lfin, uint4 &lb) {
 #if VT_BHPF
-  uint4 b = fin == lfin ? lb : (fin == D.bh_fin ? D.bh : wld(L.wheel + (fin & nbm)));
+  uint4 b = fin == lfin ? lb : (fin == D.bh_fin ? D.bh : bkt_ld(D, L, nbm, fin));
 #else
-  uint4 b = fin == lfin ? lb : wld(L.wheel + (fin & nbm));
+  uint4 b = fin == lfin ? lb : bkt_ld(D, L, nbm, fin);
 #endif
   L.node[i].next = NIL;
   if (b.y == 0u) b.x = i + 1u; else L.node[b.y - 1u].next = i;
   b.y = i + 1u;
   b.z += 1u;
   b.w += inout;
-  wst(L.wheel + (fin & nbm), b);
+  bkt_st(D, L, nbm, fin, b);
   lfin = fin;
   lb = b;
 #if VT_BHPF
@@ -420,8 +447,8 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
-template <bool EN, bool F>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
-__device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_lim, Err &E,
+template <bool EN, bool F, class WS>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
+__device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, Err &E,
                             const voltana_outputs &O) {
   if (D.dead) return;
   const uint32_t nbm = W.nb - 1u;
@@ -436,7 +463,11 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
       D.nreq -= b.z;
       D.nkv -= b.w;
       if (b.x != 0u) {
+#if VT_SWHEEL
+        L.sw[D.cur & (VT_SWHEEL - 1)] = make_uint4(0u, 0u, 0u, 0u);
+#else
         wst(L.wheel + (D.cur & nbm), make_uint4(0u, 0u, 0u, 0u));
+#endif
         L.fid[D.nfifo] = b.x - 1u;
         L.ft[D.nfifo] = tnow;
         if (++D.nfifo == VT_ITL_FIFO) itl_drain<EN, F>(D, L, W, d, O);
@@ -453,6 +484,16 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     // ---- O7 START_DECODE at tnow
     uint32_t lfin = NIL;
     uint4 lb = make_uint4(0u, 0u, 0u, 0u);
+#if VT_SWHEEL
+    {  // bucket iters + VT_SWHEEL - 1 enters the near window: global -> shared (its slot held
+       // bucket iters - 1, completed and cleared at the previous END)
+      const uint32_t m = D.iters + (uint32_t)VT_SWHEEL - 1u;
+      const uint4 g = wld(L.wheel + (m & nbm));
+      L.sw[m & (VT_SWHEEL - 1)] = g;
+      if (g.z != 0u) wst(L.wheel + (m & nbm), make_uint4(0u, 0u, 0u, 0u));
+      prefetch_l1(L.wheel + ((m + 1u) & nbm));   // the next START's migration
+    }
+#endif
     // far requests whose finishing iteration entered the window join their bucket now,
     // before any direct admission can reach that bucket (admission order, A37)
     while (D.far_h != NIL && D.far_hfin - D.iters < W.nb) {
@@ -524,7 +565,11 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WarpSmem &W, double t_
     if (k == (int)W.K - 1) ACC(top) = add(ACC(top), dur);
     D.cur = D.iters;
     D.iters += 1u;
+#if VT_SWHEEL
+    D.bcur = L.sw[D.cur & (VT_SWHEEL - 1)];  // final now: read at the END of this iteration
+#else
     D.bcur = wld(L.wheel + (D.cur & nbm));  // final now: read at the END of this iteration
+#endif
 #if VT_PF == 4
     // the completion list of this iteration was (most likely) known one START ago: pull its
     // head node towards L1 for the ITL walk at END; then peek at the next iteration's bucket
@@ -557,7 +602,8 @@ __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, doub
   if (D.qt == NIL) {
     D.qh = i;
 #if VT_PF >= 2 && VT_PF != 5
-    prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // its bucket at the next START
+    if (!VT_SWHEEL || out - 2u >= (uint32_t)VT_SWHEEL)
+      prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // its bucket at the next START
 #endif
 #if VT_QCACHE
     D.qhn.tf = tf; D.qhn.next = NIL; D.qhn.in = (uint16_t)in; D.qhn.out = (uint16_t)out;
@@ -611,8 +657,8 @@ __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uin
 }
 
 // ------------------------------------------------------------------ phase A: prefill lane p
-template <bool EN, bool F>
-__device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const double *arr, const uint32_t *inl,
+template <bool EN, bool F, class WS>
+__device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double *arr, const uint32_t *inl,
                              const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0,
                              uint32_t *head_out) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -729,8 +775,8 @@ __device__ void prefill_lane(const SimParams &P, WarpSmem &W, Node *node, const 
   *head_out = head;
 }
 
-template <bool EN, bool F>
-__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WarpSmem &W) {
+template <bool EN, bool F, class WS>
+__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WS &W) {
   const int lane = glane();
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   // ---------------------------------------------------------------- ids and table rows
@@ -865,6 +911,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   // ================================================================ PHASE B: routing + decode lanes
   const int dl = lane < ND ? lane : 0;
   Lane L;
+#if VT_SWHEEL
+  L.sw = (uint4 *)((char *)&W + P.sw_off) + (size_t)dl * VT_SWHEEL;
+  if (lane < ND)
+    for (uint32_t b = 0; b < (uint32_t)VT_SWHEEL; ++b) L.sw[b] = make_uint4(0u, 0u, 0u, 0u);
+#endif
   L.node = node;
   L.farfin = (uint32_t *)(slot + P.node_bytes);
   L.wheel = wheels + (size_t)dl * P.nb;
@@ -1063,7 +1114,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     return;
   }
   const int dd = lane < ND ? lane : 0;
-#define LACC(f) (VT_DACC_SMEM ? W.da_##f[dd] : D.f)
+#if VT_DACC_SMEM
+#define LACC(f) W.da_##f[dd]
+#else
+#define LACC(f) D.f
+#endif
   double tl = lane < ND ? LACC(tlast) : 0.0;
   if (lane < NP) tl = tl > W.pa_tlast[lane] ? tl : W.pa_tlast[lane];
   for (int o = GS / 2; o > 0; o >>= 1) {
@@ -1138,7 +1193,8 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
   if (sid >= P.n_slots) return;
   char *slot = P.slots + (size_t)sid * P.slot_bytes;
   uint4 *wheels = P.wheels + (size_t)sid * P.wheel_per_slot;
-  WarpSmem &W = *(WarpSmem *)(smem + (size_t)(wib * SPW + grp) * P.smem_per_warp);
+  using WS = WarpSmemT<F ? 8 : VOLTANA_MAX_LEVELS>;
+  WS &W = *(WS *)(smem + (size_t)(wib * SPW + grp) * P.smem_per_warp);
   for (;;) {
     uint32_t s = 0;
 #if VT_TWO_ENDED
@@ -1173,7 +1229,10 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
   }
 }
 
-size_t sim_smem_fixed() { return (sizeof(WarpSmem) - sizeof(double) + 15) & ~(size_t)15; }
+size_t sim_smem_fixed(bool fast) {
+  const size_t b = fast ? sizeof(WarpSmemT<8>) : sizeof(WarpSmemT<VOLTANA_MAX_LEVELS>);
+  return (b - sizeof(double) + 15) & ~(size_t)15;
+}
 
 __global__ void utab_kernel(const __grid_constant__ SimParams P) {
   const uint32_t total = P.n_profiles * 2u * SIM_UTAB;

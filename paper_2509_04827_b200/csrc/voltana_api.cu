@@ -258,7 +258,7 @@ uint32_t wheel_buckets(uint32_t max_out) {
 
 struct SimLayout {
   size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
-  uint32_t n_slots, nb, itl_smem;
+  uint32_t n_slots, nb, itl_smem, sw_off;
 };
 
 int resident_warps(size_t smem_per_block) {
@@ -283,13 +283,18 @@ int resident_warps(size_t smem_per_block) {
   return cached;
 }
 
+// fast: the fast-table instantiation (K <= 8 staged tables) will run [DESIGN §5 item 7]
 SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n_layouts, int kmax, int tmax,
-                     size_t n) {
+                     size_t n, bool fast = false) {
   SimLayout L;
   L.nb = wheel_buckets(tr->max_out);
   size_t itl_bytes = (size_t)kmax * tmax * 24;
   L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
-  L.smem_per_warp = (sim_smem_fixed() + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
+  L.smem_per_warp = (sim_smem_fixed(fast) + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
+  L.sw_off = (uint32_t)L.smem_per_warp;
+#ifdef VT_SWHEEL
+  L.smem_per_warp += (size_t)max_nd(lays, n_layouts) * VT_SWHEEL * 16;
+#endif
   L.smem = L.smem_per_warp * (SIM_THREADS / 32) * SPW;  // per-scenario block x scenarios per CTA
   L.node = align256((size_t)tr->max_requests * 16);
   L.slot = L.node + align256((size_t)tr->max_requests * 4);
@@ -406,7 +411,11 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     return fail(VOLTANA_E_INVALID_ARG, "simulate: null device array");
   int kmax, tmax;
   table_extent(grids_h, n_grids, profiles_h, n_profiles, &kmax, &tmax);
-  SimLayout L = sim_layout(traces_h, layouts_h, n_layouts, kmax, tmax, n);
+  // fast tables: every ladder K <= 8, ITL tables staged, pow2 tiles, no prefill tiles
+  bool fast = (size_t)kmax * tmax * 24 <= SIM_ITL_SMEM_MAX && kmax <= 8;
+  for (int i = 0; i < n_profiles; ++i)
+    fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0 && profiles_h[i].n_ptiles <= 1;
+  SimLayout L = sim_layout(traces_h, layouts_h, n_layouts, kmax, tmax, n, fast);
   const size_t need = voltana_simulate_workspace_bytes(traces_h, layouts_h, n_layouts, n);
   if (!workspace || ws_bytes < need || ws_bytes < L.total)
     return fail(VOLTANA_E_WORKSPACE, "simulate: workspace %zu < %zu bytes", ws_bytes, need);
@@ -436,6 +445,7 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->wheel_per_slot = L.wheel_per_slot;
   P->itl_smem = L.itl_smem;
   P->smem_per_warp = (uint32_t)L.smem_per_warp;
+  P->sw_off = L.sw_off;
   P->timing = g_debug_timing;
   for (int i = 0; i < n_slos; ++i) P->slo[i] = slos_h[i];
   for (int i = 0; i < n_layouts; ++i) P->lay[i] = layouts_h[i];
@@ -456,9 +466,6 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
              x.exec_noise != nullptr;
   }
   energy = energy || P->o.req_offset != nullptr || P->o.iter_offset != nullptr;  // outputs (E1-E3)
-  bool fast = L.itl_smem && kmax <= 8;
-  for (int i = 0; i < n_profiles; ++i)
-    fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0 && profiles_h[i].n_ptiles <= 1;
 #if VT_UTAB
   e = launch_utab(*P, st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate utab launch"); }

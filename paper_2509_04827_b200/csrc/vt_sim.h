@@ -22,7 +22,7 @@ constexpr int SIM_MIN_BLOCKS = VT_SIM_MIN_BLOCKS;  // 4: <= 128 registers, 16 wa
 #endif
 constexpr int SPW = VT_SPW;           // scenarios per warp (lane groups of 32 / SPW; N_P, N_D <= 8)
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
-size_t sim_smem_fixed();  // per-warp shared-memory block without the staged ITL table
+size_t sim_smem_fixed(bool fast);  // per-warp shared-memory block without the staged ITL table
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size
 #ifndef VT_NBMAX
 #define VT_NBMAX 1024
@@ -58,6 +58,7 @@ struct SimParams {
   size_t wheel_per_slot;       // max N_D * nb buckets
   uint32_t itl_smem;           // stage the ladder's ITL table in shared memory
   uint32_t smem_per_warp;
+  uint32_t sw_off;             // VT_SWHEEL: byte offset of the near wheel in the per-warp block
   uint64_t *timing;            // debug: [n][2] globaltimer ns at scenario start/end | smid<<56 (NULL: off)
   voltana_outputs o;           // optional per-request / per-instance outputs (variant kernel only)
   const double *utab;          // VT_UTAB: [MAX_PROFILES][2][SIM_UTAB] utilisation u = l / (l + u_half)

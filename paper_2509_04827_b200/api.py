@@ -374,6 +374,18 @@ class SimOutputs:
         return [rec[u, :min(int(cnt[u]), self.iter_cap)] for u in range(b - a)], cnt
 
 
+def simulate_ex(w: DeviceWorkload, outputs: SimOutputs | None = None, stream=None) -> np.ndarray:
+    """voltana_simulate_ex on a resident workload (optional per-request / per-instance outputs);
+    returns the records in the caller's scenario order."""
+    w.launch(stream, outputs=outputs)
+    return w.records()
+
+
+def series_to_samples(outputs: SimOutputs, profile_id: int = 0, stream=None) -> dict:
+    """voltana_series_to_samples: the iteration series of `outputs` as calibration samples."""
+    return outputs.samples(profile_id, stream)
+
+
 def simulate(traces, slos, layouts, grids, profiles, scen, device="cuda", stream=None) -> np.ndarray:
     """One-shot voltana_simulate from host arrays: upload, run, read back records."""
     w = DeviceWorkload(traces, slos, layouts, grids, profiles, scen, device=device)

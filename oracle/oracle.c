@@ -99,6 +99,20 @@ static double busy_power(const orc_profile *p, int phase, int lvl, uint64_t load
 /* energy = time x power: joules from watts and milliseconds */
 static double interval_energy(double power_w, double dur_ms) { return (power_w * dur_ms) / 1000.0; }
 
+/* ------------------------------------------------------------ ITL aggregation [E3] */
+
+static int cmp_double(const void *a, const void *b) {
+  double x = *(const double *)a, y = *(const double *)b;
+  return (x > y) - (x < y);
+}
+
+/* nearest-rank P99 of n gaps: the ceil(0.99 n)-th smallest ("itl_mode P99") [E3] */
+static double p99_nearest_rank(double *g, uint64_t n) {
+  qsort(g, (size_t)n, sizeof(double), cmp_double);
+  uint64_t rank = (99 * n + 99) / 100; /* ceil(0.99 n), exact in integers */
+  return g[rank - 1];
+}
+
 /* ------------------------------------------------------------ decision hash */
 
 static uint64_t splitmix64(uint64_t x) {
@@ -321,6 +335,7 @@ static int validate(const orc_scenario *s) {
   if (!(s->ctrl_interval_ms >= 0.0 && s->ctrl_interval_ms < 1e12)) return 0;
   if (!(s->freq_overhead_ms >= 0.0 && s->freq_overhead_ms < 1e9)) return 0;
   if (s->noise && (s->noise_len == 0 || (s->noise_len & (s->noise_len - 1)) != 0)) return 0;
+  if (s->itl_mode < 0 || s->itl_mode > 2) return 0;
   if (s->max_batch_tokens == 0 || s->kv_capacity == 0) return 0;
   if (s->max_batch_tokens > 0x7fffffffu || s->kv_capacity > 0x7fffffffu) return 0;
   if (!(s->slo_ttft > 0.0) || !(s->slo_itl > 0.0) || !(s->slo_scale > 0.0)) return 0;
@@ -361,6 +376,19 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
   uint32_t *xq_id = malloc((N ? N : 1) * sizeof(uint32_t)); /* KV-transfer FIFO [A18] */
   uint32_t *xq_d = malloc((N ? N : 1) * sizeof(uint32_t));
   uint64_t xq_head = 0, xq_tail = 0;
+  /* ITL Max / P99 [E3]: every request's token times (last token, running max, all gaps) */
+  double *last_tok = NULL, *maxgap = NULL, *gapbuf = NULL;
+  uint64_t *gap_off = NULL, *gap_n = NULL;
+  if (s->itl_mode != 0) {
+    last_tok = calloc(N ? N : 1, sizeof(double));
+    maxgap = calloc(N ? N : 1, sizeof(double));
+    if (s->itl_mode == 2) {
+      gap_off = calloc(N + 1, sizeof(uint64_t));
+      gap_n = calloc(N ? N : 1, sizeof(uint64_t));
+      for (uint64_t i = 0; i < N; ++i) gap_off[i + 1] = gap_off[i] + (out[i] > 1 ? out[i] - 1 : 0);
+      gapbuf = malloc((gap_off[N] ? gap_off[N] : 1) * sizeof(double));
+    }
+  }
   uint64_t *eff_n = malloc((size_t)ND * sizeof(uint64_t));
   uint64_t *eff_kv = malloc((size_t)ND * sizeof(uint64_t));
   for (int q = 0; q < NP; ++q) {
@@ -423,6 +451,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         n_ttft_ok += (uint64_t)ok;
         ttft_ok[i] = (uint8_t)ok;
         tfirst[i] = t;
+        if (last_tok) last_tok[i] = t; /* the first token [E3] */
         if (diag && diag->req_tfirst) diag->req_tfirst[i] = t;
         if (out[i] == 1) { /* first token came from prefill; nothing to decode [A8, A30] */
           n_itl_ok++;
@@ -469,12 +498,20 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       for (uint64_t r = 0; r < I->n_run; ++r) {
         run_entry e = I->run[r];
         e.rem -= 1;
+        if (last_tok) { /* this iteration produced one token for every running request [E3] */
+          double gap = t - last_tok[e.id];
+          last_tok[e.id] = t;
+          if (gap > maxgap[e.id]) maxgap[e.id] = gap;
+          if (gapbuf) gapbuf[gap_off[e.id] + gap_n[e.id]++] = gap;
+        }
         if (e.rem == 0) {
           uint32_t id = e.id;
           /* per-request ITL = mean inter-token latency [A30] */
           double itl = (t - tfirst[id]) / (double)(out[id] - 1);
           I->sum_itl += itl;
           int ok = itl <= s->slo_itl;
+          if (s->itl_mode == 1) ok = maxgap[id] <= s->slo_itl; /* ITL Max [E3] */
+          if (s->itl_mode == 2) ok = p99_nearest_rank(gapbuf + gap_off[id], gap_n[id]) <= s->slo_itl;
           n_itl_ok += (uint64_t)ok;
           n_both += (uint64_t)(ok && ttft_ok[id]);
           I->nreq -= 1;
@@ -686,6 +723,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
 
   for (int d = 0; d < ND; ++d) { free(D[d].run); free(D[d].admq); }
   free(P); free(D); free(tfirst); free(ttft_ok); free(xq_id); free(xq_d); free(eff_n); free(eff_kv);
+  free(last_tok); free(maxgap); free(gapbuf); free(gap_off); free(gap_n);
   return 0;
 }
 

@@ -56,6 +56,8 @@ typedef struct {
   double freq_overhead_ms;           /* blocking frequency-set delay on a level change (0 = non-blocking) [C3] */
   const double *noise;               /* [noise_len] execution-noise factors, NULL = none [D1, D2] */
   uint64_t noise_len;                /* power of two */
+  int32_t itl_mode;                  /* per-request ITL for attainment: 0 mean, 1 max, 2 P99 [E3] */
+  int32_t pad3_;
 } orc_scenario;
 
 /* 128-byte per-scenario result record. */

@@ -55,7 +55,7 @@ class OrcScenario(C.Structure):
                 ("kv_transfer_ms", C.c_double), ("delta_mhz", C.c_int32), ("ladder", vp),
                 ("K", C.c_int32), ("prof", P(OrcProfile)), ("hash_seed", C.c_uint64),
                 ("ctrl_mode", C.c_int32), ("ctrl_interval_ms", C.c_double), ("freq_overhead_ms", C.c_double),
-                ("noise", vp), ("noise_len", C.c_uint64)]
+                ("noise", vp), ("noise_len", C.c_uint64), ("itl_mode", C.c_int32), ("pad3_", C.c_int32)]
 
 
 class OrcDiag(C.Structure):
@@ -130,7 +130,7 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                      float(layout.kv_transfer_ms), int(layout.delta_mhz), _ptr(ladder), int(len(ladder)),
                      C.pointer(ph.s), int(hash_seed), int(getattr(layout, "ctrl_mode", 0)),
                      float(getattr(layout, "ctrl_interval_ms", 0.0)), float(getattr(layout, "freq_overhead_ms", 0.0)),
-                     _ptr(noise), 0 if noise is None else len(noise))
+                     _ptr(noise), 0 if noise is None else len(noise), int(getattr(layout, "itl_mode", 0)), 0)
     res = np.zeros(1, RESULT_DTYPE)
     dg = None
     keep = []

@@ -40,6 +40,7 @@ class Layout:
     ctrl_interval_ms: float = 0.0      # window control: 0 = per-iteration
     freq_overhead_ms: float = 0.0      # blocking frequency set on a change (~50 ms nvidia-smi, ~3 ms pyNVML)
     exec_noise: object = field(default=None, compare=False, repr=False)  # f64 factor table (noise.py), None = noiseless
+    itl_mode: int = 0                  # per-request ITL for attainment: 0 mean, 1 max, 2 P99
 
 
 @dataclass

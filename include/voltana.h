@@ -170,7 +170,9 @@ typedef struct {
   uint32_t kv_capacity;    /* decode KV tokens C (400000) [A20]                          */
   double kv_transfer_ms;   /* tau: 0, or >= 1e-3 [A18]                                    */
   int32_t ctrl_mode;       /* 0 EcoFreq lowest feasible, 1 energy argmin [B4] */
-  int32_t reserved;        /* 0                                                           */
+  int32_t itl_mode;        /* per-request ITL for the attainment counts: 0 mean
+                              (A30), 1 max inter-token gap, 2 nearest-rank P99 of the gaps;
+                              sum_itl_mean_ms stays the mean [E3]                         */
   double ctrl_interval_ms; /* window control: an instance decides at
                               an iteration START only when >= this has elapsed since its
                               previous decision (inclusive); 0 = every iteration [C1]      */

@@ -45,7 +45,7 @@ class Slo(C.Structure):
 class Layout(C.Structure):
     _fields_ = [("n_p", C.c_int32), ("n_d", C.c_int32), ("policy", C.c_int32), ("delta_mhz", C.c_int32),
                 ("max_batch_tokens", C.c_uint32), ("kv_capacity", C.c_uint32), ("kv_transfer_ms", C.c_double),
-                ("ctrl_mode", C.c_int32), ("reserved", C.c_int32), ("ctrl_interval_ms", C.c_double),
+                ("ctrl_mode", C.c_int32), ("itl_mode", C.c_int32), ("ctrl_interval_ms", C.c_double),
                 ("freq_overhead_ms", C.c_double), ("exec_noise", vp), ("noise_len", C.c_uint32),
                 ("reserved2", C.c_uint32)]
 

@@ -208,7 +208,8 @@ class DeviceWorkload:
                       else self._up(np.ascontiguousarray(x.exec_noise, np.float64), torch.float64) for x in layouts]
         self.layouts = (_lib.Layout * len(layouts))(*[
             _lib.Layout(int(x.n_p), int(x.n_d), int(x.policy), int(x.delta_mhz), int(x.max_batch_tokens),
-                        int(x.kv_capacity), float(x.kv_transfer_ms), int(getattr(x, "ctrl_mode", 0)), 0,
+                        int(x.kv_capacity), float(x.kv_transfer_ms), int(getattr(x, "ctrl_mode", 0)),
+                        int(getattr(x, "itl_mode", 0)),
                         float(getattr(x, "ctrl_interval_ms", 0.0)), float(getattr(x, "freq_overhead_ms", 0.0)),
                         None if nz is None else nz.data_ptr(), 0 if nz is None else int(nz.numel()), 0)
             for x, nz in zip(layouts, self.noise)])

@@ -149,6 +149,10 @@ struct WarpSmemT {
   const double *noise;             // execution-noise factor table or NULL [D1, D2]
   uint32_t noise_mask, np;         // np: N_P (decode instance d is noise instance N_P + d)
   uint64_t seed;                   // scenario hash seed (noise index)
+  double *re;                      // ITL modes (E3): this slot's rings [N_D][ring_r] of iteration end times
+  uint32_t *rc;                    //   ... and of cumulative counts of gaps above the ITL SLO
+  uint32_t itlm, rmask;            //   layout itl_mode, ring_r - 1
+  uint32_t dl_vc[VOLTANA_MAX_INSTANCES];  // decode lane: gaps above the ITL SLO so far
   uint64_t rq_base, it_base;       // outputs (E1-E3): request / iteration-slot base of the scenario
   uint32_t rq_on, it_on;
   // ---- variant-kernel per-instance controller state [C1-C3]
@@ -361,7 +365,20 @@ __device__ void itl_drain(Dec &D, const Lane &L, WS &W, int d, const voltana_out
       for (uint32_t hop = 0; hop < W.max_steps; ++hop) {
         const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
         ACC(sitl) = add(ACC(sitl), itl);
-        const bool ok = itl <= slo;
+        bool ok = itl <= slo;
+        if (EN && W.itlm) {
+          // ITL Max / P99 (E3): the request's gaps are e_a - t_first and the iteration gaps of
+          // (a, f], f = this iteration, a = f - (out - 2); count those above the SLO from the
+          // instance's rings and compare with the nearest-rank allowance (0 for Max)
+          static_assert(VT_ITL_FIFO == 1, "ITL modes read the completing iteration from D.cur");
+          const uint32_t n = (uint32_t)nd.out - 1u;
+          const uint32_t a = D.cur - (n - 1u);
+          const double ea = W.re[(size_t)d * (W.rmask + 1u) + (a & W.rmask)];
+          const uint32_t ca = W.rc[(size_t)d * (W.rmask + 1u) + (a & W.rmask)];
+          const uint32_t viol = (W.dl_vc[d] - ca) + (sub(ea, fabs(nd.tf)) > slo ? 1u : 0u);
+          const uint32_t allow = W.itlm == 1u ? 0u : n - (99u * n + 99u) / 100u;
+          ok = viol <= allow;
+        }
         ACC(n_itl_ok) += ok;
         ACC(n_both) += ok && nd.tf > 0.0;
         if (EN && W.rq_on) {  // per-request record (E1)
@@ -454,9 +471,11 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
   const uint32_t nbm = W.nb - 1u;
   for (;;) {
     double tnow;
+    bool cont = false;  // this START follows an END at the same time (the instance stays busy)
     if (D.busy) {
       if (!(D.end < t_lim)) return;
       tnow = D.end;
+      cont = true;
       // ---- O6 DecodeIterDone: +1 KV token per running request; this iteration's completions
       D.nkv += D.nreq;
       const uint4 b = D.bcur;
@@ -560,6 +579,12 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     }
     D.end = add(t0, dur);
     D.busy = true;
+    if (EN && W.itlm) {  // ITL modes (E3): gap e_i - e_{i-1} of this iteration, if continuous
+      W.dl_vc[d] += (cont && sub(D.end, tnow) > W.slo_itl) ? 1u : 0u;
+      const size_t ro = (size_t)d * (W.rmask + 1u) + (D.iters & W.rmask);
+      W.re[ro] = D.end;
+      W.rc[ro] = W.dl_vc[d];
+    }
     ACC(ebusy) = add(ACC(ebusy), mul(bpow(W, 1, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
     ACC(bms) = add(ACC(bms), dur);
     if (k == (int)W.K - 1) ACC(top) = add(ACC(top), dur);
@@ -776,7 +801,7 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
 }
 
 template <bool EN, bool F, class WS>
-__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WS &W) {
+__device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WS &W, uint32_t sid) {
   const int lane = glane();
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   // ---------------------------------------------------------------- ids and table rows
@@ -855,10 +880,15 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.noise_mask = LY.noise_len - 1u;
     W.seed = P.hash_seed[s];
     W.np = (uint32_t)NP;
+    W.itlm = EN ? (uint32_t)LY.itl_mode : 0u;
+    W.rmask = P.ring_r - 1u;
+    W.re = P.ring_e ? P.ring_e + (size_t)sid * P.ring_nd * P.ring_r : nullptr;
+    W.rc = P.ring_c ? P.ring_c + (size_t)sid * P.ring_nd * P.ring_r : nullptr;
     W.rq_on = rq_on; W.rq_base = rq_base;
     W.it_on = EN && P.o.iter_offset != nullptr; W.it_base = it_base;
   }
   if (EN && lane < NI) {
+    W.dl_vc[lane] = 0u;
     W.dl_last[lane] = -INF;
     W.dl_cur[lane] = (uint32_t)GR.k - 1u;  // the GPU starts at the top of the ladder [C2]
     W.dl_ndec[lane] = 0u;
@@ -1212,7 +1242,7 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
     if (s >= P.n) break;
     uint64_t t0 = 0;
     if (P.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    run_scenario<EN, F>(P, s, slot, wheels, W);
+    run_scenario<EN, F>(P, s, slot, wheels, W, sid);
     __syncwarp(gmask());
     if (P.timing && lane == 0) {
       uint64_t t1;

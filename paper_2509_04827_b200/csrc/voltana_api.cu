@@ -258,7 +258,8 @@ uint32_t wheel_buckets(uint32_t max_out) {
 
 struct SimLayout {
   size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
-  uint32_t n_slots, nb, itl_smem, sw_off;
+  uint32_t n_slots, nb, itl_smem, sw_off, ring_r = 0, ring_nd = 0;
+  size_t ring_e_off = 0, ring_c_off = 0;
 };
 
 int resident_warps(size_t smem_per_block) {
@@ -305,6 +306,18 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.slots_off = 256;
   L.wheels_off = align256(L.slots_off + (size_t)L.n_slots * L.slot);
   L.total = L.wheels_off + (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint4);
+  // ITL Max / P99 (E3): per decode instance, the end time and the running count of gaps above
+  // the SLO of its last ring_r iterations (ring_r >= max_out covers every request's window)
+  L.ring_r = 0;
+  for (int i = 0; i < n_layouts; ++i)
+    if (lays[i].itl_mode != 0) L.ring_r = 2;
+  if (L.ring_r) {
+    while (L.ring_r < tr->max_out) L.ring_r <<= 1;
+    L.ring_nd = (uint32_t)max_nd(lays, n_layouts);
+    L.ring_e_off = align256(L.total);
+    L.ring_c_off = align256(L.ring_e_off + (size_t)L.n_slots * L.ring_nd * L.ring_r * sizeof(double));
+    L.total = L.ring_c_off + (size_t)L.n_slots * L.ring_nd * L.ring_r * sizeof(uint32_t);
+  }
 #if VT_UTAB
   L.utab_off = align256(L.total);
   L.total = L.utab_off + (size_t)MAX_PROFILES * 2 * SIM_UTAB * sizeof(double);
@@ -379,6 +392,8 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     if (x.policy < 0 || x.policy > 2) return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].policy=%d", i, x.policy);
     if (x.ctrl_mode != 0 && x.ctrl_mode != 1)
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].ctrl_mode=%d", i, x.ctrl_mode);
+    if (x.itl_mode < 0 || x.itl_mode > 2)
+      return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].itl_mode=%d (0 mean, 1 max, 2 P99)", i, x.itl_mode);
     if (!(x.ctrl_interval_ms >= 0.0 && x.ctrl_interval_ms < 1e12))
       return fail(VOLTANA_E_CONFIG, "simulate: layouts[%d].ctrl_interval_ms must be in [0, 1e12)", i);
     if (!(x.freq_overhead_ms >= 0.0 && x.freq_overhead_ms < 1e9))
@@ -439,6 +454,12 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->slot_bytes = L.slot;
   P->node_bytes = L.node;
   P->wheels = (uint4 *)(ws + L.wheels_off);
+  if (L.ring_r) {
+    P->ring_e = (double *)(ws + L.ring_e_off);
+    P->ring_c = (uint32_t *)(ws + L.ring_c_off);
+    P->ring_r = L.ring_r;
+    P->ring_nd = L.ring_nd;
+  }
 #if VT_UTAB
   P->utab = (const double *)(ws + L.utab_off);
 #endif
@@ -463,7 +484,7 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   for (int i = 0; i < n_layouts; ++i) {
     const voltana_layout &x = layouts_h[i];
     energy = energy || x.policy == 2 || x.ctrl_mode != 0 || x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 ||
-             x.exec_noise != nullptr;
+             x.exec_noise != nullptr || x.itl_mode != 0;
   }
   energy = energy || P->o.req_offset != nullptr || P->o.iter_offset != nullptr;  // outputs (E1-E3)
 #if VT_UTAB

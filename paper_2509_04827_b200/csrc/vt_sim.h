@@ -62,6 +62,9 @@ struct SimParams {
   uint64_t *timing;            // debug: [n][2] globaltimer ns at scenario start/end | smid<<56 (NULL: off)
   voltana_outputs o;           // optional per-request / per-instance outputs (variant kernel only)
   const double *utab;          // VT_UTAB: [MAX_PROFILES][2][SIM_UTAB] utilisation u = l / (l + u_half)
+  double *ring_e;              // ITL modes (E3): [n_slots][max N_D][ring_r] iteration end times
+  uint32_t *ring_c;            //   ... and cumulative counts of gaps above the ITL SLO
+  uint32_t ring_r, ring_nd;    //   ring length (power of two >= max_out), instances per slot
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];

@@ -64,7 +64,7 @@ def test_random_scenarios(vt, orc, seed):
                   kv_transfer_ms=float(rng.choice([0.0, 0.0, 7.5])))
         if i >= 8:   # variants on half of the layouts
             kw.update(ctrl_mode=int(rng.integers(0, 2)), ctrl_interval_ms=float(rng.choice([0.0, 150.0, 2000.0])),
-                      freq_overhead_ms=float(rng.choice([0.0, 3.0, 50.0])),
+                      freq_overhead_ms=float(rng.choice([0.0, 3.0, 50.0])), itl_mode=int(rng.integers(0, 3)),
                       exec_noise=synth.exec_noise_table(float(rng.choice([0.0, 0.05, 0.2])), 256, seed=i)
                       if rng.random() < 0.5 else None)
         layouts.append(Layout(int(rng.integers(1, 9)), int(rng.integers(1, 9)), **kw))

@@ -115,6 +115,39 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
+def variant_kernels(vt, torch, w, dprof, dev, reps=3):
+    """K4 on the same C4 sweep with each §8(f) variant switched on for every scenario (the
+    variant instantiation): mean CUDA-event time of one launch and decisions/s. Context for
+    what the variants cost; the headline line above is the paper's policies."""
+    import dataclasses
+    import synth
+    variants = {
+        "paper_policies (default kernel)": {},
+        "energy_router+energy_ctrl": dict(policy=2, ctrl_mode=1),
+        "window_300ms+overhead_3ms": dict(ctrl_interval_ms=300.0, freq_overhead_ms=3.0),
+        "exec_noise_sigma_0.05": dict(exec_noise=synth.exec_noise_table(0.05, 4096)),
+        "itl_p99": dict(itl_mode=2),
+    }
+    out = {}
+    for name, kw in variants.items():
+        lays = [dataclasses.replace(x, **kw) for x in w.layouts]
+        wl = vt.DeviceWorkload(w.traces, w.slos, lays, w.grids, [dprof], w.scen, device=dev)
+        wl.launch()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            wl.launch()
+        b.record()
+        b.synchronize()
+        rec = wl.records()
+        steps = int((rec["steps_ctrl"] + rec["steps_route"]).sum())
+        ms = a.elapsed_time(b) / reps
+        out[name] = {"simulate_ms": ms, "decisions": steps, "decisions_per_s": steps / (ms / 1000.0)}
+        del wl
+    return out
+
+
 def workload_config():
     return {"workload": "C4: 4096 scenarios/GPU = 4 SLO x 8 Poisson rates x 128 seeds, 2P2D, 5-level ladder "
                         "[1005..1410] MHz, Delta=150, LLaMA-3.1-8B-shaped profile fitted from 2M samples, "
@@ -381,7 +414,9 @@ def run_ours(args):
            "fit_samples": n_samp, "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roof,
            "cpu_baseline": cpu,
            "streaming": (streaming_kernels(vt, torch, dev, peaks["hbm_gbs"])
-                         if not args.no_streaming and rank == 0 else None)}
+                         if not args.no_streaming and rank == 0 else None),
+           "variants": (variant_kernels(vt, torch, w, dprof, dev)
+                        if not args.no_streaming and rank == 0 else None)}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if world > 1:

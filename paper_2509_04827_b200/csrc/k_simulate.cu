@@ -348,7 +348,7 @@ __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
 
 // ITL accounting of deferred completion lists, in completion order (A30, A37); the head
 // nodes of up to four lists are loaded together.
-template <bool EN, bool F, class WS>
+template <int V, bool F, class WS>
 __device__ void itl_drain(Dec &D, const Lane &L, WS &W, int d, const voltana_outputs &O) {
   const double slo = W.slo_itl;
   for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
@@ -366,7 +366,7 @@ __device__ void itl_drain(Dec &D, const Lane &L, WS &W, int d, const voltana_out
         const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
         ACC(sitl) = add(ACC(sitl), itl);
         bool ok = itl <= slo;
-        if (EN && W.itlm) {
+        if ((V & 2) && W.itlm) {
           // ITL Max / P99 (E3): the request's gaps are e_a - t_first and the iteration gaps of
           // (a, f], f = this iteration, a = f - (out - 2); count those above the SLO from the
           // instance's rings and compare with the nearest-rank allowance (0 for Max)
@@ -381,7 +381,7 @@ __device__ void itl_drain(Dec &D, const Lane &L, WS &W, int d, const voltana_out
         }
         ACC(n_itl_ok) += ok;
         ACC(n_both) += ok && nd.tf > 0.0;
-        if (EN && W.rq_on) {  // per-request record (E1)
+        if ((V & 2) && W.rq_on) {  // per-request record (E1)
           O.req_tdone[W.rq_base + id] = td;
           O.req_itl[W.rq_base + id] = itl;
         }
@@ -464,7 +464,7 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
 }
 
 // Advance decode instance `d` through every event with time < t_lim (END, START).
-template <bool EN, bool F, class WS>  // EN: the variant kernel (energy scoring B1-B4, window control / overhead C1-C3)
+template <int V, bool F, class WS>  // V: variant bits, 1 energy scoring (B1-B4), 2 window/overhead/noise/ITL modes/outputs (C-E)
 __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, Err &E,
                             const voltana_outputs &O) {
   if (D.dead) return;
@@ -489,7 +489,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
 #endif
         L.fid[D.nfifo] = b.x - 1u;
         L.ft[D.nfifo] = tnow;
-        if (++D.nfifo == VT_ITL_FIFO) itl_drain<EN, F>(D, L, W, d, O);
+        if (++D.nfifo == VT_ITL_FIFO) itl_drain<V, F>(D, L, W, d, O);
       }
       D.busy = false;
       ACC(tlast) = tnow;
@@ -554,32 +554,32 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     double dur;
     int k;
     uint32_t fl = backlog ? 4u : 0u;
-    if (EN && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+    if ((V & 2) && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)W.dl_cur[d];
       dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv);
     } else {
       fl |= 1u;
       if (backlog) { k = (int)W.K - 1; dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
-      else if (EN && W.ctrl) k = energy_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
+      else if ((V & 1) && W.ctrl) k = energy_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
       else k = lowest_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);
       ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
-      if (EN) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
+      if ((V & 2)) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
     }
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
-    if (EN && W.noise) {  // [D1]
+    if ((V & 2) && W.noise) {  // [D1]
       const double e = noise_at(W, (uint64_t)W.np + d, D.iters);
       if (!(e > 0.0 && e <= 1e6)) { E.t = tnow; E.code = VOLTANA_ITEM_E_INPUT; D.dead = true; return; }
       dur = mul(dur, e);
     }
     double t0 = tnow;
-    if (EN) {  // blocking frequency set on a level change [C3]
+    if ((V & 2)) {  // blocking frequency set on a level change [C3]
       if (k != (int)W.dl_cur[d] && W.fs_ov > 0.0) { t0 = add(tnow, W.fs_ov); fl |= 2u; }
       W.dl_cur[d] = (uint32_t)k;
       log_iter(O, W, W.np + (uint32_t)d, D.iters, tnow, dur, D.nreq, D.nkv, k, fl);
     }
     D.end = add(t0, dur);
     D.busy = true;
-    if (EN && W.itlm) {  // ITL modes (E3): gap e_i - e_{i-1} of this iteration, if continuous
+    if ((V & 2) && W.itlm) {  // ITL modes (E3): gap e_i - e_{i-1} of this iteration, if continuous
       W.dl_vc[d] += (cont && sub(D.end, tnow) > W.slo_itl) ? 1u : 0u;
       const size_t ro = (size_t)d * (W.rmask + 1u) + (D.iters & W.rmask);
       W.re[ro] = D.end;
@@ -682,7 +682,7 @@ __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uin
 }
 
 // ------------------------------------------------------------------ phase A: prefill lane p
-template <bool EN, bool F, class WS>
+template <int V, bool F, class WS>
 __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double *arr, const uint32_t *inl,
                              const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0,
                              uint32_t *head_out) {
@@ -733,26 +733,26 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
     double dur;
     int k;
     uint32_t fl = backlog ? 4u : 0u;
-    if (EN && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+    if ((V & 2) && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)cur;
       dur = ttft_at<F>(W, k, nbt);
     } else {
       fl |= 1u;
       if (backlog) { k = (int)K - 1; dur = ttft_at<F>(W, k, nbt); }
-      else if (EN && W.ctrl) k = energy_ttft<F>(W, nbt, budget, &dur);  // B4
+      else if ((V & 1) && W.ctrl) k = energy_ttft<F>(W, nbt, budget, &dur);  // B4
       else k = lowest_ttft<F>(W, nbt, budget, &dur);
       h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
-      if (EN) { last = ts; ndec++; }
+      if ((V & 2)) { last = ts; ndec++; }
     }
     const uint32_t jit = iters++;
     if (!(dur > 0.0)) { errt = ts; errc = VOLTANA_ITEM_E_CONTRACT; break; }
-    if (EN && W.noise) {  // true time = prediction x lognormal factor [D1]
+    if ((V & 2) && W.noise) {  // true time = prediction x lognormal factor [D1]
       const double e = noise_at(W, p, jit);
       if (!(e > 0.0 && e <= 1e6)) { errt = ts; errc = VOLTANA_ITEM_E_INPUT; break; }
       dur = mul(dur, e);
     }
     double t0 = ts;
-    if (EN) {  // blocking frequency set on a level change [C3]
+    if ((V & 2)) {  // blocking frequency set on a level change [C3]
       if (k != (int)cur && W.fs_ov > 0.0) { t0 = add(ts, W.fs_ov); fl |= 2u; }
       cur = (uint32_t)k;
       log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
@@ -768,7 +768,7 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
       const bool ok = ttft <= slo_ttft;
       ttft_ok += ok;
       const uint32_t o = outl[i];
-      if (EN && W.rq_on) {  // per-request record (E1)
+      if ((V & 2) && W.rq_on) {  // per-request record (E1)
         P.o.req_tfirst[W.rq_base + i] = end;
         if (o == 1u) {
           P.o.req_tdone[W.rq_base + i] = end; P.o.req_itl[W.rq_base + i] = 0.0;
@@ -795,12 +795,12 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
   W.pa_ebusy[p] = ebusy; W.pa_bms[p] = bms; W.pa_top[p] = top; W.pa_sttft[p] = sttft; W.pa_tlast[p] = tlast;
   W.pa_errt[p] = errt; W.pa_errc[p] = errc; W.pa_h[p] = h; W.pa_iters[p] = iters; W.pa_ttft_ok[p] = ttft_ok;
   W.pa_itl_ok[p] = itl_ok; W.pa_both[p] = both;
-  if (EN) W.pa_ndec[p] = ndec;
-  if (EN && W.it_on) P.o.iter_count[W.it_base / P.o.iter_cap + p] = iters;
+  if ((V & 2)) W.pa_ndec[p] = ndec;
+  if ((V & 2) && W.it_on) P.o.iter_count[W.it_base / P.o.iter_cap + p] = iters;
   *head_out = head;
 }
 
-template <bool EN, bool F, class WS>
+template <int V, bool F, class WS>
 __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WS &W, uint32_t sid) {
   const int lane = glane();
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -848,7 +848,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const int NP = LY.n_p, ND = LY.n_d;
   uint64_t rq_base = 0, it_base = 0;
   bool rq_on = false;
-  if (EN && P.o.req_offset) {  // per-request range: empty (skip) or exactly the trace (E1)
+  if ((V & 2) && P.o.req_offset) {  // per-request range: empty (skip) or exactly the trace (E1)
     rq_base = P.o.req_offset[s];
     const uint64_t len = P.o.req_offset[s + 1] - rq_base;
     if (len != 0 && len != N64) {
@@ -857,7 +857,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
     rq_on = len != 0;
   }
-  if (EN && P.o.iter_offset) it_base = P.o.iter_offset[s];
+  if ((V & 2) && P.o.iter_offset) it_base = P.o.iter_offset[s];
 
   // ---------------------------------------------------------------- stage constants and tables
   const uint32_t K = (uint32_t)GR.k, T = (uint32_t)PR.n_tiles;
@@ -880,14 +880,14 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.noise_mask = LY.noise_len - 1u;
     W.seed = P.hash_seed[s];
     W.np = (uint32_t)NP;
-    W.itlm = EN ? (uint32_t)LY.itl_mode : 0u;
+    W.itlm = (V & 2) ? (uint32_t)LY.itl_mode : 0u;
     W.rmask = P.ring_r - 1u;
     W.re = P.ring_e ? P.ring_e + (size_t)sid * P.ring_nd * P.ring_r : nullptr;
     W.rc = P.ring_c ? P.ring_c + (size_t)sid * P.ring_nd * P.ring_r : nullptr;
     W.rq_on = rq_on; W.rq_base = rq_base;
-    W.it_on = EN && P.o.iter_offset != nullptr; W.it_base = it_base;
+    W.it_on = (V & 2) && P.o.iter_offset != nullptr; W.it_base = it_base;
   }
-  if (EN && lane < NI) {
+  if ((V & 2) && lane < NI) {
     W.dl_vc[lane] = 0u;
     W.dl_last[lane] = -INF;
     W.dl_cur[lane] = (uint32_t)GR.k - 1u;  // the GPU starts at the top of the ladder [C2]
@@ -928,7 +928,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
   // ================================================================ PHASE A: prefill lanes
   uint32_t p_head = NIL;
-  if (lane < NP) prefill_lane<EN, F>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
+  if (lane < NP) prefill_lane<V, F>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
   __syncwarp(gmask());
 #ifdef VT_PHASE_TIMING
   if (P.timing && glane() == 0) {  // experiment: phase-A end time replaces the start stamp
@@ -996,7 +996,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   int ka_last = 0;
   double c_en = 0.0, en_new = 0.0;                  // energy router: P*T of the cached state / successor
   const bool eco = LY.policy == 0 && ND > 1;
-  const bool ens = EN && LY.policy == 2 && ND > 1;
+  const bool ens = (V & 1) && LY.policy == 2 && ND > 1;
   const int32_t delta = LY.delta_mhz;
   int w = argmin_time(fabs(hn.tf), hd != NIL);  // next PrefillDone request in (t, p, id) order
   for (;;) {
@@ -1023,7 +1023,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #endif
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
-      dec_advance<EN, F>(D, lane, L, W, t, dE, P.o);
+      dec_advance<V, F>(D, lane, L, W, t, dE, P.o);
       t_adv = t;
     }
     // ---- O8 EcoRoute
@@ -1115,7 +1115,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       if (eco) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
       if (ens) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_en = en_new; }
       dec_push(D, L, i, tf_i, in_i, io >> 16, W.nb - 1u);
-      if (EN && W.rq_on) { P.o.req_decode[W.rq_base + i] = (uint8_t)dsel; P.o.req_case[W.rq_base + i] = (uint8_t)cse; }
+      if ((V & 2) && W.rq_on) { P.o.req_decode[W.rq_base + i] = (uint8_t)dsel; P.o.req_case[W.rq_base + i] = (uint8_t)cse; }
     }
 #if VT_PIPE_ARGMIN
     w = w_next;
@@ -1124,9 +1124,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #endif
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
-  dec_advance<EN, F>(D, lane, L, W, INF, dE, P.o);
-  if (lane < ND && !D.dead) itl_drain<EN, F>(D, L, W, lane, P.o);
-  if (EN && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
+  dec_advance<V, F>(D, lane, L, W, INF, dE, P.o);
+  if (lane < ND && !D.dead) itl_drain<V, F>(D, L, W, lane, P.o);
+  if ((V & 2) && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
   __syncwarp(gmask());
 
   // ================================================================ O9: record
@@ -1198,7 +1198,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     R.status = 0; R.n_requests = N;
     R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl_p + c_itl; R.n_both_ok = c_both_p + c_both; R.prefill_iters = c_pi;
     uint64_t sc = (uint64_t)c_pi + c_di;  // one decision per iteration ...
-    if (EN) {                            // ... unless window control skipped some [C1]
+    if ((V & 2)) {                            // ... unless window control skipped some [C1]
       sc = 0;
       for (int q = 0; q < NP; ++q) sc += W.pa_ndec[q];
       for (int d = 0; d < ND; ++d) sc += W.dl_ndec[d];
@@ -1211,9 +1211,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
 }
 
-// EN = false: the paper's EcoFreq/EcoRoute/RR only (the default kernel); EN = true also runs
-// the energy variants [B1-B4] (selected on the host when any layout asks for them).
-template <bool EN, bool F>
+// V = 0: the paper's EcoFreq/EcoRoute/RR only (the default kernel); V & 1 adds the energy-scored
+// router and controller [B1-B4]; V & 2 adds window control, blocking overhead, execution noise,
+// ITL modes and the optional outputs [C-E]. The host launches the smallest V that covers the
+// launch's layouts, so each variant pays only for its own registers.
+template <int V, bool F>
 __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(const __grid_constant__ SimParams P) {
   extern __shared__ __align__(16) char smem[];
   const int lane = glane();
@@ -1242,7 +1244,7 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
     if (s >= P.n) break;
     uint64_t t0 = 0;
     if (P.timing) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-    run_scenario<EN, F>(P, s, slot, wheels, W, sid);
+    run_scenario<V, F>(P, s, slot, wheels, W, sid);
     __syncwarp(gmask());
     if (P.timing && lane == 0) {
       uint64_t t1;
@@ -1278,19 +1280,36 @@ cudaError_t launch_utab(const SimParams &P, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-const void *sim_kernel_ptr(bool energy, bool fast) {
-  if (energy) return fast ? (const void *)simulate_kernel<true, true> : (const void *)simulate_kernel<true, false>;
-  return fast ? (const void *)simulate_kernel<false, true> : (const void *)simulate_kernel<false, false>;
+template <int V>
+static const void *kptr(bool fast) {
+  return fast ? (const void *)simulate_kernel<V, true> : (const void *)simulate_kernel<V, false>;
 }
 
-cudaError_t launch_sim(const SimParams &P, bool energy, bool fast, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(energy, fast), cudaFuncAttributeMaxDynamicSharedMemorySize,
+const void *sim_kernel_ptr(int v, bool fast) {
+  switch (v & 3) {
+    case 1: return kptr<1>(fast);
+    case 2: return kptr<2>(fast);
+    case 3: return kptr<3>(fast);
+    default: return kptr<0>(fast);
+  }
+}
+
+template <int V>
+static void launch_v(const SimParams &P, bool fast, int grid, size_t smem, cudaStream_t st) {
+  if (fast) simulate_kernel<V, true><<<grid, SIM_THREADS, smem, st>>>(P);
+  else simulate_kernel<V, false><<<grid, SIM_THREADS, smem, st>>>(P);
+}
+
+cudaError_t launch_sim(const SimParams &P, int v, bool fast, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(v, fast), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  if (energy && fast) simulate_kernel<true, true><<<grid, SIM_THREADS, smem, st>>>(P);
-  else if (energy) simulate_kernel<true, false><<<grid, SIM_THREADS, smem, st>>>(P);
-  else if (fast) simulate_kernel<false, true><<<grid, SIM_THREADS, smem, st>>>(P);
-  else simulate_kernel<false, false><<<grid, SIM_THREADS, smem, st>>>(P);
+  switch (v & 3) {
+    case 1: launch_v<1>(P, fast, grid, smem, st); break;
+    case 2: launch_v<2>(P, fast, grid, smem, st); break;
+    case 3: launch_v<3>(P, fast, grid, smem, st); break;
+    default: launch_v<0>(P, fast, grid, smem, st); break;
+  }
   return cudaGetLastError();
 }
 

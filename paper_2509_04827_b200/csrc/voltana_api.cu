@@ -270,9 +270,9 @@ int resident_warps(size_t smem_per_block) {
   if (smem_per_block != cached_smem) {
     int nb = 0;
     // both instantiations are built for the same bound (128 registers, 4 CTAs per SM)
-    cudaFuncSetAttribute(sim_kernel_ptr(false, false), cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sim_kernel_ptr(0, false), cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem_per_block);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(false, false), SIM_THREADS,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel_ptr(0, false), SIM_THREADS,
                                                       smem_per_block) !=
             cudaSuccess || nb < 1) {
       cudaGetLastError();
@@ -480,18 +480,18 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
   const int per_cta = (SIM_THREADS / 32) * SPW;
   const int grid = (int)((L.n_slots + per_cta - 1) / per_cta);
-  bool energy = false;  // any variant layout [B1-B4, C1-C3, D1-D2] selects that instantiation
+  int v = 0;  // variant bits of the instantiation: 1 energy scoring, 2 light variants / outputs
   for (int i = 0; i < n_layouts; ++i) {
     const voltana_layout &x = layouts_h[i];
-    energy = energy || x.policy == 2 || x.ctrl_mode != 0 || x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 ||
-             x.exec_noise != nullptr || x.itl_mode != 0;
+    if (x.policy == 2 || x.ctrl_mode != 0) v |= 1;
+    if (x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 || x.exec_noise != nullptr || x.itl_mode != 0) v |= 2;
   }
-  energy = energy || P->o.req_offset != nullptr || P->o.iter_offset != nullptr;  // outputs (E1-E3)
+  if (P->o.req_offset != nullptr || P->o.iter_offset != nullptr) v |= 2;  // outputs (E1-E2)
 #if VT_UTAB
   e = launch_utab(*P, st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate utab launch"); }
 #endif
-  e = launch_sim(*P, energy, fast, grid, L.smem, st);
+  e = launch_sim(*P, v, fast, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
   g_launches = 1 + VT_UTAB;

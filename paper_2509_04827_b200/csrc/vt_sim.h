@@ -72,11 +72,11 @@ struct SimParams {
   DevProfile prof[MAX_PROFILES];
 };
 
-// energy: the instantiation that also runs the variants [B1-B4, C1-C3, D1-D2, E1-E2];
+// v: variant bits (1 energy scoring B1-B4; 2 window/overhead/noise/ITL modes/outputs C-E);
 // fast: every ladder has K <= 8, every tile width is a power of two and the ITL tables are
 // staged in shared memory, so the general table paths are compiled out.
-const void *sim_kernel_ptr(bool energy, bool fast);
-cudaError_t launch_sim(const SimParams &P, bool energy, bool fast, int grid, size_t smem, cudaStream_t st);
+const void *sim_kernel_ptr(int v, bool fast);
+cudaError_t launch_sim(const SimParams &P, int v, bool fast, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_utab(const SimParams &P, cudaStream_t st);  // VT_UTAB: fill P.utab
 
 }  // namespace vt

@@ -152,6 +152,7 @@ struct WarpSmemT {
   double *re;                      // ITL modes (E3): this slot's rings [N_D][ring_r] of iteration end times
   uint32_t *rc;                    //   ... and of cumulative counts of gaps above the ITL SLO
   uint32_t itlm, rmask;            //   layout itl_mode, ring_r - 1
+  uint32_t wo;                     // window control or blocking overhead active (C1-C3)
   uint32_t dl_vc[VOLTANA_MAX_INSTANCES];  // decode lane: gaps above the ITL SLO so far
   uint64_t rq_base, it_base;       // outputs (E1-E3): request / iteration-slot base of the scenario
   uint32_t rq_on, it_on;
@@ -554,7 +555,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     double dur;
     int k;
     uint32_t fl = backlog ? 4u : 0u;
-    if ((V & 2) && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+    if ((V & 2) && W.wo && !(sub(tnow, W.dl_last[d]) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)W.dl_cur[d];
       dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv);
     } else {
@@ -563,7 +564,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       else if ((V & 1) && W.ctrl) k = energy_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
       else k = lowest_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);
       ACC(h) = fold(ACC(h), 2, (uint64_t)d, (uint64_t)k, 0);
-      if ((V & 2)) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
+      if ((V & 2) && W.wo) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
     }
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
     if ((V & 2) && W.noise) {  // [D1]
@@ -572,11 +573,11 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       dur = mul(dur, e);
     }
     double t0 = tnow;
-    if ((V & 2)) {  // blocking frequency set on a level change [C3]
+    if ((V & 2) && W.wo) {  // blocking frequency set on a level change [C3]
       if (k != (int)W.dl_cur[d] && W.fs_ov > 0.0) { t0 = add(tnow, W.fs_ov); fl |= 2u; }
       W.dl_cur[d] = (uint32_t)k;
-      log_iter(O, W, W.np + (uint32_t)d, D.iters, tnow, dur, D.nreq, D.nkv, k, fl);
     }
+    if ((V & 2)) log_iter(O, W, W.np + (uint32_t)d, D.iters, tnow, dur, D.nreq, D.nkv, k, fl);
     D.end = add(t0, dur);
     D.busy = true;
     if ((V & 2) && W.itlm) {  // ITL modes (E3): gap e_i - e_{i-1} of this iteration, if continuous
@@ -733,7 +734,7 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
     double dur;
     int k;
     uint32_t fl = backlog ? 4u : 0u;
-    if ((V & 2) && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+    if ((V & 2) && W.wo && !(sub(ts, last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
       k = (int)cur;
       dur = ttft_at<F>(W, k, nbt);
     } else {
@@ -742,7 +743,7 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
       else if ((V & 1) && W.ctrl) k = energy_ttft<F>(W, nbt, budget, &dur);  // B4
       else k = lowest_ttft<F>(W, nbt, budget, &dur);
       h = fold(h, 1, (uint64_t)p, (uint64_t)k, 0);
-      if ((V & 2)) { last = ts; ndec++; }
+      if ((V & 2) && W.wo) { last = ts; ndec++; }
     }
     const uint32_t jit = iters++;
     if (!(dur > 0.0)) { errt = ts; errc = VOLTANA_ITEM_E_CONTRACT; break; }
@@ -752,11 +753,11 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
       dur = mul(dur, e);
     }
     double t0 = ts;
-    if ((V & 2)) {  // blocking frequency set on a level change [C3]
+    if ((V & 2) && W.wo) {  // blocking frequency set on a level change [C3]
       if (k != (int)cur && W.fs_ov > 0.0) { t0 = add(ts, W.fs_ov); fl |= 2u; }
       cur = (uint32_t)k;
-      log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
     }
+    if ((V & 2)) log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
     const double end = add(t0, dur);
     ebusy = add(ebusy, mul(bpow(W, 0, W.dyn[k], nbt), dur));  // W*ms (A23)
     bms = add(bms, dur);
@@ -881,6 +882,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     W.seed = P.hash_seed[s];
     W.np = (uint32_t)NP;
     W.itlm = (V & 2) ? (uint32_t)LY.itl_mode : 0u;
+    W.wo = (V & 2) && (LY.ctrl_interval_ms > 0.0 || LY.freq_overhead_ms > 0.0) ? 1u : 0u;
     W.rmask = P.ring_r - 1u;
     W.re = P.ring_e ? P.ring_e + (size_t)sid * P.ring_nd * P.ring_r : nullptr;
     W.rc = P.ring_c ? P.ring_c + (size_t)sid * P.ring_nd * P.ring_r : nullptr;
@@ -1198,7 +1200,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     R.status = 0; R.n_requests = N;
     R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl_p + c_itl; R.n_both_ok = c_both_p + c_both; R.prefill_iters = c_pi;
     uint64_t sc = (uint64_t)c_pi + c_di;  // one decision per iteration ...
-    if ((V & 2)) {                            // ... unless window control skipped some [C1]
+    if ((V & 2) && W.wo) {                   // ... unless window control skipped some [C1]
       sc = 0;
       for (int q = 0; q < NP; ++q) sc += W.pa_ndec[q];
       for (int d = 0; d < ND; ++d) sc += W.dl_ndec[d];

@@ -293,7 +293,10 @@ def run_ours(args):
         launches = vt.last_launch_count()
         if ev:
             ev[1].record(stream)
+            vt.lib().voltana_set_split_event(ev[4].cuda_event)   # recorded between K4a and K4b
         wl.launch()
+        if ev:
+            vt.lib().voltana_set_split_event(None)
         launches += vt.last_launch_count()
         if ev:
             ev[2].record(stream)
@@ -316,7 +319,9 @@ def run_ours(args):
     torch.cuda.synchronize()
     clk = Clocks(dev.index)
     clk.start()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    for e in evs:
+        e[4].record(stream)   # creates the split event (torch creates events lazily)
     launches = 0
     for k in range(args.steps):
         flush.fill_(k & 0xFF)                           # L2 flush between timed steps (not timed)
@@ -328,6 +333,8 @@ def run_ours(args):
     t_step = [e[0].elapsed_time(e[3]) for e in evs]
     t_fit = [e[0].elapsed_time(e[1]) for e in evs]
     t_sim = [e[1].elapsed_time(e[2]) for e in evs]
+    t_pa = [e[1].elapsed_time(e[4]) for e in evs]      # setup + K4a prefill_kernel
+    t_dec = [e[4].elapsed_time(e[2]) for e in evs]     # K4b simulate_kernel
     t_gather = [e[2].elapsed_time(e[3]) for e in evs]
     dev_ms = float(sum(t_step))
     tot_steps = steps_per_pass * args.steps
@@ -379,8 +386,8 @@ def run_ours(args):
     nd = w.layouts[0].n_d
     pre = rec["prefill_iters"].astype(np.int64)
     dec = rec["steps_ctrl"].astype(np.int64) - pre
-    flops = int((pre * 2 * K + dec * 4 * K + rec["steps_route"].astype(np.int64) * 8 * nd * K).sum())
-    sim_s = statistics.mean(t_sim) / 1000.0
+    flops = int((dec * 4 * K + rec["steps_route"].astype(np.int64) * 8 * nd * K).sum())   # K4b's decisions
+    sim_s = statistics.mean(t_dec) / 1000.0
     achieved = flops / sim_s / 1e12
     sm_mhz = 1965.0
     peak = N_SM * FP64_LANES_PER_SM * sm_mhz * 1e6 / 1e12
@@ -394,10 +401,10 @@ def run_ours(args):
         ncu_k4 = json.load(open(tj)).get("simulate_kernel", {})
         traffic = ncu_k4.get("dram_bytes_per_launch")
     roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "vt::simulate_kernel",
-            "note": "algorithmic FP64 ops of the decision procedure (prefill ctrl 2K, decode ctrl 4K, route "
-                    "8*N_D*K per decision) / mean kernel time; peak = 148 SM x 64 FP64 lanes x 1965 MHz "
-                    "(non-FMA ops); the kernel is latency/issue-bound on the serial event loop",
+            "traffic": traffic, "kernel": "vt::simulate_kernel (K4b: routing + decode lanes)",
+            "note": "algorithmic FP64 ops of K4b's decisions (decode ctrl 4K, route 8*N_D*K per decision) / its "
+                    "mean duration (CUDA events on the launch stream around K4b); peak = 148 SM x 64 FP64 lanes "
+                    "x 1965 MHz (non-FMA ops); the kernel is latency/issue-bound on the serial event loop",
             "hbm_compulsory": {"bytes": comp_bytes, "gbs": comp_bytes / sim_s / 1e9,
                                "frac_of_measured_hbm": comp_bytes / sim_s / 1e9 / peaks["hbm_gbs"]},
             "issue": {"issue_active_pct": ncu_k4.get("issue_pct"), "occupancy_pct": ncu_k4.get("occupancy_pct"),
@@ -410,6 +417,7 @@ def run_ours(args):
            "config": dict(workload_config(), parallelism=f"scenario-sharded x{world}"),
            "decisions_per_step": tot_steps // args.steps,
            "kernel_ms": {"fit_profile": statistics.mean(t_fit), "simulate": statistics.mean(t_sim),
+                         "simulate_prefill_k4a": statistics.mean(t_pa), "simulate_decode_k4b": statistics.mean(t_dec),
                          "all_gather": statistics.mean(t_gather) if world > 1 else 0.0},
            "fit_samples": n_samp, "gpu_launches": launches, "clocks": clocks, "e2e": e2e, "roofline": roof,
            "cpu_baseline": cpu,

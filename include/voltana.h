@@ -305,6 +305,12 @@ int voltana_last_launch_count(void);
  * buf[2i+1] its duration in ns with the SM id in bits 56..63. NULL turns it off. */
 void voltana_debug_set_timing(uint64_t *buf);
 
+/* Profiling hook (this thread's next voltana_simulate calls): when ev != NULL (a cudaEvent_t
+ * created by the caller), it is recorded on the call's stream between the phase-A launch
+ * (prefill_kernel, K4a) and the decode launch (simulate_kernel, K4b), so the caller can time
+ * the two kernels with its own start/end events. NULL turns it off. */
+void voltana_set_split_event(void *ev);
+
 const char *voltana_status_string(voltana_status s);
 const char *voltana_last_error_detail(void); /* thread-local, names the argument        */
 

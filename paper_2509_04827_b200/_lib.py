@@ -87,7 +87,8 @@ assert RESULT_DTYPE.itemsize == 128
 
 EXPORTS = ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_fit_workspace_bytes",
            "voltana_simulate", "voltana_simulate_ex", "voltana_series_to_samples", "voltana_simulate_workspace_bytes", "voltana_status_string",
-           "voltana_last_error_detail", "voltana_last_launch_count", "voltana_debug_set_timing")
+           "voltana_last_error_detail", "voltana_last_launch_count", "voltana_debug_set_timing",
+           "voltana_set_split_event")
 
 _lib = None
 
@@ -124,6 +125,8 @@ def lib():
     L.voltana_last_launch_count.restype = C.c_int
     L.voltana_debug_set_timing.argtypes = [vp]
     L.voltana_debug_set_timing.restype = None
+    L.voltana_set_split_event.argtypes = [vp]
+    L.voltana_set_split_event.restype = None
     for name in ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_simulate",
                  "voltana_simulate_ex", "voltana_series_to_samples"):
         getattr(L, name).restype = C.c_int

@@ -126,9 +126,7 @@ struct WarpSmemT {
   uint32_t fid[NI][ITL_FIFO];
   double ft[NI][ITL_FIFO];
   // ---- phase-A results per prefill lane (read back for the record)
-  double pa_ebusy[NI], pa_bms[NI], pa_top[NI], pa_sttft[NI], pa_tlast[NI], pa_errt[NI];
-  uint64_t pa_h[NI];
-  uint32_t pa_iters[NI], pa_ttft_ok[NI], pa_itl_ok[NI], pa_both[NI], pa_errc[NI];
+  PaRes pa[NI];
 #if VT_DACC_SMEM
   // ---- decode-lane accumulators (VT_DACC_SMEM)
   double da_ebusy[NI], da_bms[NI], da_top[NI], da_sitl[NI], da_tlast[NI];
@@ -159,7 +157,6 @@ struct WarpSmemT {
   // ---- variant-kernel per-instance controller state [C1-C3]
   double dl_last[NI];              // decode lane: time of the last decision (-inf: none)
   uint32_t dl_cur[NI], dl_ndec[NI];  // decode lane: running level, decisions taken
-  uint32_t pa_ndec[NI];            // prefill lane: decisions taken
   // ---- staged ladder tables
   uint16_t lad[KC];
   int32_t mhz[KC];
@@ -683,10 +680,32 @@ __device__ __forceinline__ void write_status(const SimParams &P, uint32_t s, uin
 }
 
 // ------------------------------------------------------------------ phase A: prefill lane p
-template <int V, bool F, class WS>
+// K4a stream prefetch: each thread walks its own trace stream (32 independent streams per
+// warp), so without prefetching almost every step waits on some lane's DRAM miss. Bulk L2
+// prefetches run PA_PF_L2 entries ahead in PA_PF_CHUNK-entry chunks, L1 line prefetches
+// PA_PF_L1 entries ahead.
+#ifndef VT_PA_PF_L2
+#define VT_PA_PF_L2 1024
+#endif
+#ifndef VT_PA_PF_L1
+#define VT_PA_PF_L1 64
+#endif
+constexpr uint32_t PA_PF_CHUNK = 256;
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+// prefetch entries [from, from + cnt) of an array of `esz`-byte elements (16-B aligned bulk)
+__device__ __forceinline__ void prefetch_l2_range(const void *base, uint32_t from, uint32_t cnt, uint32_t esz) {
+  uintptr_t a = (uintptr_t)base + (uintptr_t)from * esz;
+  uintptr_t e = a + (uintptr_t)cnt * esz;
+  a &= ~(uintptr_t)15;
+  e &= ~(uintptr_t)15;
+  if (e > a) prefetch_l2_bulk((const void *)a, (uint32_t)(e - a));
+}
+
+template <int V, bool F, bool PFK, class WS>
 __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double *arr, const uint32_t *inl,
-                             const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0,
-                             uint32_t *head_out) {
+                             const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0, PaRes &R) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double ebusy = 0.0, bms = 0.0, top = 0.0, sttft = 0.0, tlast = 0.0, errt = INF;
   uint64_t h = h0;
@@ -699,7 +718,23 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
   uint32_t nxt = p, prev = NIL;
   Node pend;
   pend.tf = 0.0; pend.next = NIL; pend.in = 0; pend.out = 0;
+  uint32_t pf1 = p, pf2 = p;  // PFK: next entry to prefetch into L1 / L2
   while (nxt < N) {
+    if (PFK) {
+      while (pf2 < N && pf2 < nxt + (uint32_t)VT_PA_PF_L2) {
+        const uint32_t c = N - pf2 < PA_PF_CHUNK ? N - pf2 : PA_PF_CHUNK;
+        prefetch_l2_range(arr, pf2, c, 8u);
+        prefetch_l2_range(inl, pf2, c, 4u);
+        prefetch_l2_range(outl, pf2, c, 4u);
+        pf2 += PA_PF_CHUNK;
+      }
+      while (pf1 < N && pf1 < nxt + (uint32_t)VT_PA_PF_L1) {
+        prefetch_l1(arr + pf1);
+        prefetch_l1(inl + pf1);
+        prefetch_l1(outl + pf1);
+        pf1 += 16u;
+      }
+    }
 #if VT_PFA
     if (nxt + VT_PFA < N) {  // the trace stream ahead of the batch being formed
       prefetch_l1(arr + nxt + VT_PFA);
@@ -793,12 +828,252 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
     nxt = id;
   }
   if (prev != NIL) { pend.next = NIL; node[prev] = pend; }
-  W.pa_ebusy[p] = ebusy; W.pa_bms[p] = bms; W.pa_top[p] = top; W.pa_sttft[p] = sttft; W.pa_tlast[p] = tlast;
-  W.pa_errt[p] = errt; W.pa_errc[p] = errc; W.pa_h[p] = h; W.pa_iters[p] = iters; W.pa_ttft_ok[p] = ttft_ok;
-  W.pa_itl_ok[p] = itl_ok; W.pa_both[p] = both;
-  if ((V & 2)) W.pa_ndec[p] = ndec;
+  R.ebusy = ebusy; R.bms = bms; R.top = top; R.sttft = sttft; R.tlast = tlast; R.errt = errt; R.h = h;
+  R.iters = iters; R.ttft_ok = ttft_ok; R.itl_ok = itl_ok; R.both = both; R.errc = errc; R.ndec = ndec;
+  R.head = head; R.pad = 0;
   if ((V & 2) && W.it_on) P.o.iter_count[W.it_base / P.o.iter_cap + p] = iters;
-  *head_out = head;
+}
+
+// ------------------------------------------------------------------ phase A, warp-cooperative (K4a)
+// Prefill instance p of one scenario on a whole warp. The instance's decisions are a serial
+// chain over batches (O7 START_PREFILL): everything on that chain is computed redundantly by
+// all lanes, so control flow stays uniform. The lanes hold a window of the instance's next 32
+// queued requests (arrival, in, out, and the inclusive prefix sum of in):
+//  - batch formation at time ts from head lane h is one ballot: candidate j > h joins iff it
+//    and every candidate before it has arrived by ts and the tokens from h through j fit in B;
+//    the first failing lane ends the batch and says whether it is a backlog (A5, A6);
+//  - the per-request TTFT accounting of O5 runs once per window for all its batches: each lane
+//    holds its batch's end time, the report sum is added in FCFS order (A37), the counts are
+//    ballots, and each routed request links to the next routed one.
+// A batch longer than the window (> 32 requests) takes the general path (rounds of 32).
+
+struct PState {   // uniform state of one prefill instance (every lane holds the same values)
+  double ebusy, bms, top, sttft, tlast, errt, tfree, last;
+  uint64_t h;
+  uint32_t iters, ttft_ok, itl_ok, both, errc, head, cur, ndec, prev;
+  Node pend;      // node of request `prev` (last routed so far), written when its successor is known
+};
+
+// O7 decision for a batch of nbt tokens starting at ts, head arrival a0: EcoFreq,
+// duration, energy (A23). false: per-item error recorded in S.
+template <int V, bool F, class WS>
+__device__ __forceinline__ bool pa_decide(const SimParams &P, const WS &W, PState &S, uint32_t p, double ts,
+                                          double a0, uint32_t nbt, bool backlog, double &end) {
+  double budget = sub(W.tgt_ttft, sub(ts, a0));  // A4: SLO minus the oldest request's wait
+  budget = budget > 0.0 ? budget : 0.0;
+  const uint32_t K = W.K;
+  double dur;
+  int k;
+  uint32_t fl = backlog ? 4u : 0u;
+  if ((V & 2) && W.wo && !(sub(ts, S.last) >= W.ctrl_iv)) {  // window gating: keep the running level [C1]
+    k = (int)S.cur;
+    dur = ttft_at<F>(W, k, nbt);
+  } else {
+    fl |= 1u;
+    if (backlog) { k = (int)K - 1; dur = ttft_at<F>(W, k, nbt); }
+    else if ((V & 1) && W.ctrl) k = energy_ttft<F>(W, nbt, budget, &dur);  // B4
+    else k = lowest_ttft<F>(W, nbt, budget, &dur);
+    S.h = fold(S.h, 1, (uint64_t)p, (uint64_t)k, 0);
+    if ((V & 2) && W.wo) { S.last = ts; S.ndec++; }
+  }
+  const uint32_t jit = S.iters++;
+  if (!(dur > 0.0)) { S.errt = ts; S.errc = VOLTANA_ITEM_E_CONTRACT; return false; }
+  if ((V & 2) && W.noise) {  // true time = prediction x lognormal factor [D1]
+    const double e = noise_at(W, p, jit);
+    if (!(e > 0.0 && e <= 1e6)) { S.errt = ts; S.errc = VOLTANA_ITEM_E_INPUT; return false; }
+    dur = mul(dur, e);
+  }
+  double t0 = ts;
+  if ((V & 2) && W.wo) {  // blocking frequency set on a level change [C3]
+    if (k != (int)S.cur && W.fs_ov > 0.0) { t0 = add(ts, W.fs_ov); fl |= 2u; }
+    S.cur = (uint32_t)k;
+  }
+  if ((V & 2) && (threadIdx.x & 31u) == 0) log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
+  end = add(t0, dur);
+  S.ebusy = add(S.ebusy, mul(bpow(W, 0, W.dyn[k], nbt), dur));  // W*ms (A23)
+  S.bms = add(S.bms, dur);
+  if (k == (int)K - 1) S.top = add(S.top, dur);
+  S.tfree = end;
+  S.tlast = end;
+  return true;
+}
+
+// O5 for lanes [0, n): request base + lane*NP (arrival a, in x, out o) finished prefill at e.
+template <int V, class WS>
+__device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PState &S, Node *node, uint32_t base,
+                                           uint32_t NP, uint32_t n, double e, double a, uint32_t x, uint32_t o) {
+  if (n == 0u) return;
+  const uint32_t lane = threadIdx.x & 31u;
+  const bool valid = lane < n;
+  const uint32_t i = base + lane * NP;
+  const double ttft = valid ? sub(e, a) : 0.0;  // A26
+  const bool ok = valid && ttft <= W.slo_ttft;
+  for (uint32_t b = 0; b < n; b += 8u) {  // the report sum in FCFS order (A37)
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = __shfl_sync(FULL, ttft, (int)(b + u) & 31);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (b + u < n) S.sttft = add(S.sttft, v[u]);
+  }
+  S.ttft_ok += __popc(__ballot_sync(FULL, ok));
+  const bool one = valid && o == 1u;  // first token came from prefill: done (A8, A30)
+  S.itl_ok += __popc(__ballot_sync(FULL, one));
+  S.both += __popc(__ballot_sync(FULL, one && ok));
+  if ((V & 2) && W.rq_on && valid) {  // per-request record (E1)
+    P.o.req_tfirst[W.rq_base + i] = e;
+    if (o == 1u) {
+      P.o.req_tdone[W.rq_base + i] = e; P.o.req_itl[W.rq_base + i] = 0.0;
+      P.o.req_decode[W.rq_base + i] = 0xFF; P.o.req_case[W.rq_base + i] = 0xFF;
+    }
+  }
+  const unsigned rm = __ballot_sync(FULL, valid && o != 1u);  // routed requests, FCFS = lane order
+  if (rm == 0u) return;
+  const int f0 = ffs0(rm), ll = 31 - __clz(rm);
+  const uint32_t i_first = base + (uint32_t)f0 * NP;
+  if (S.prev != NIL) {
+    if (lane == 0) { S.pend.next = i_first; node[S.prev] = S.pend; }
+  } else {
+    S.head = i_first;
+  }
+  Node me;
+  me.tf = ok ? e : -e;
+  me.in = (uint16_t)x;
+  me.out = (uint16_t)o;
+  if (((rm >> lane) & 1u) && (int)lane != ll) {  // the next routed request is in this set
+    const unsigned above = rm & ~((2u << lane) - 1u);
+    me.next = base + (uint32_t)ffs0(above) * NP;
+    node[i] = me;
+  }
+  S.prev = base + (uint32_t)ll * NP;  // the last routed request: pending until its successor
+  S.pend.tf = __shfl_sync(FULL, me.tf, ll);
+  S.pend.in = (uint16_t)__shfl_sync(FULL, (uint32_t)me.in, ll);
+  S.pend.out = (uint16_t)__shfl_sync(FULL, (uint32_t)me.out, ll);
+  S.pend.next = NIL;
+}
+
+// General path for one batch starting at request nxt (any length): candidates in rounds of 32,
+// accounting in chunks of 32. Returns the next unbatched request, or NIL on an error.
+template <int V, bool F, class WS>
+__device__ uint32_t pa_batch_general(const SimParams &P, const WS &W, PState &S, Node *node, const double *arr,
+                                     const uint32_t *inl, const uint32_t *outl, uint32_t N, uint32_t p,
+                                     uint32_t NP, uint32_t nxt) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const uint32_t lane = threadIdx.x & 31u, B = W.B;
+  const double a0 = arr[nxt];
+  const double ts = S.tfree > a0 ? S.tfree : a0;
+  uint32_t nbt = inl[nxt], cnt = 1, id = nxt + NP;
+  bool backlog = false;
+  for (;;) {
+    const uint32_t j = id + lane * NP;
+    const bool in_tr = j < N && j >= id;
+    const double av = in_tr ? arr[j] : INF;  // past the trace end: "not arrived"
+    const uint32_t xv = in_tr ? inl[j] : 0u;
+    uint32_t ps = xv;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, ps, o);
+      if (lane >= (uint32_t)o) ps += y;
+    }
+    const bool arrived = av <= ts;
+    const unsigned m = __ballot_sync(FULL, arrived && !(nbt + ps > B));
+    const uint32_t f = m == FULL ? 32u : (uint32_t)ffs0(~m);
+    if (f > 0u) {
+      nbt += __shfl_sync(FULL, ps, (int)f - 1);
+      cnt += f;
+      id += f * NP;
+    }
+    if (f < 32u) {
+      backlog = __shfl_sync(FULL, arrived, (int)f);
+      break;
+    }
+  }
+  double end;
+  if (!pa_decide<V, F>(P, W, S, p, ts, a0, nbt, backlog, end)) return NIL;
+  for (uint32_t q0 = 0; q0 < cnt; q0 += 32u) {
+    const uint32_t nv = cnt - q0 < 32u ? cnt - q0 : 32u;
+    const uint32_t i = nxt + (q0 + lane) * NP;
+    double a = 0.0;
+    uint32_t x = 0u, o = 0u;
+    if (lane < nv) { a = arr[i]; x = inl[i]; o = outl[i]; }
+    pa_account<V>(P, W, S, node, nxt + q0 * NP, NP, nv, end, a, x, o);
+  }
+  return id;
+}
+
+template <int V, bool F, class WS>
+__device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double *arr, const uint32_t *inl,
+                             const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0, PaRes &R) {
+  const double INF = __longlong_as_double(0x7ff0000000000000ll);
+  const uint32_t lane = threadIdx.x & 31u, B = W.B;
+  PState S;
+  S.ebusy = S.bms = S.top = S.sttft = S.tlast = S.tfree = 0.0;
+  S.errt = INF;
+  S.last = -INF;             // [C1] time of the last decision
+  S.h = h0;
+  S.iters = S.ttft_ok = S.itl_ok = S.both = S.errc = S.ndec = 0;
+  S.cur = W.K - 1u;          // [C2] running level (starts at the top)
+  S.head = S.prev = NIL;
+  S.pend.tf = 0.0; S.pend.next = NIL; S.pend.in = 0; S.pend.out = 0;
+  uint32_t wbase = p;        // request of lane 0 in the window (the instance's next unbatched request)
+  uint32_t pf2 = p;          // next entry to prefetch into L2
+  while (wbase < N) {
+    if (lane == 0)
+      while (pf2 < N && pf2 < wbase + (uint32_t)VT_PA_PF_L2) {
+        const uint32_t c = N - pf2 < PA_PF_CHUNK ? N - pf2 : PA_PF_CHUNK;
+        prefetch_l2_range(arr, pf2, c, 8u);
+        prefetch_l2_range(inl, pf2, c, 4u);
+        prefetch_l2_range(outl, pf2, c, 4u);
+        pf2 += PA_PF_CHUNK;
+      }
+    const uint32_t rem = (N - wbase + NP - 1u) / NP;  // requests left on this instance
+    const uint32_t nwin = rem < 32u ? rem : 32u;
+    const uint32_t idx = wbase + lane * NP;
+    const bool v = lane < nwin;
+    const double a = v ? arr[idx] : INF;  // past the trace end: "not arrived"
+    const uint32_t x = v ? inl[idx] : 0u;
+    const uint32_t o = v ? outl[idx] : 0u;
+    uint32_t ps = x;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, ps, s);
+      if (lane >= (uint32_t)s) ps += y;
+    }
+    double e = 0.0;            // this lane's batch end, once its batch has started
+    uint32_t hl = 0;           // head lane of the next batch
+    bool err = false, general = false;
+    while (hl < nwin) {
+      const double a0 = __shfl_sync(FULL, a, (int)hl);
+      const double ts = S.tfree > a0 ? S.tfree : a0;  // START: instance idle and queue non-empty
+      const uint32_t psb = hl ? __shfl_sync(FULL, ps, (int)(hl - 1u)) : 0u;  // tokens before the head
+      const bool arrived = a <= ts;
+      const bool take = lane > hl && arrived && !(ps - psb > B);
+      const unsigned fails = __ballot_sync(FULL, lane > hl && !take);
+      if (fails == 0u) {       // a full window of arrivals that all fit: the batch may run on
+        general = hl == 0u;    // more than 32 requests: the general path; else re-window at the head
+        break;
+      }
+      const uint32_t f = (uint32_t)ffs0(fails);  // first candidate not taken
+      const bool backlog = __shfl_sync(FULL, arrived, (int)f);  // arrived but does not fit (A5)
+      const uint32_t nbt = __shfl_sync(FULL, ps, (int)(f - 1u)) - psb;
+      double end;
+      if (!pa_decide<V, F>(P, W, S, p, ts, a0, nbt, backlog, end)) { err = true; break; }
+      if (lane >= hl && lane < f) e = end;
+      hl = f;
+    }
+    pa_account<V>(P, W, S, node, wbase, NP, hl, e, a, x, o);  // O5 for the window's batches
+    wbase += hl * NP;
+    if (err) break;
+    if (general) {
+      wbase = pa_batch_general<V, F>(P, W, S, node, arr, inl, outl, N, p, NP, wbase);
+      if (wbase == NIL) break;
+    }
+  }
+  if (S.prev != NIL && lane == 0) { S.pend.next = NIL; node[S.prev] = S.pend; }
+  R.ebusy = S.ebusy; R.bms = S.bms; R.top = S.top; R.sttft = S.sttft; R.tlast = S.tlast; R.errt = S.errt;
+  R.h = S.h; R.iters = S.iters; R.ttft_ok = S.ttft_ok; R.itl_ok = S.itl_ok; R.both = S.both; R.errc = S.errc;
+  R.ndec = S.ndec; R.head = S.head; R.pad = 0;
+  if ((V & 2) && W.it_on && lane == 0) P.o.iter_count[W.it_base / P.o.iter_cap + p] = S.iters;
 }
 
 template <int V, bool F, class WS>
@@ -925,13 +1200,22 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     if (lane == 0) { W.mono_tt = mt; W.mono_it = mi; }
   }
   __syncwarp(gmask());
+#if VT_SPLIT_A
+  Node *node = (Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node));
+#else
   Node *node = (Node *)slot;
+#endif
   const uint64_t h0 = P.hash_seed[s];
 
   // ================================================================ PHASE A: prefill lanes
-  uint32_t p_head = NIL;
-  if (lane < NP) prefill_lane<V, F>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, &p_head);
+#if VT_SPLIT_A
+  // computed by K4a (prefill_kernel) before this launch: read back lane p's result
+  if (lane < NP) W.pa[lane] = P.pares[(size_t)s * NI + lane];
+#else
+  if (lane < NP) prefill_lane<V, F, false>(P, W, node, arr, inl, outl, N, (uint32_t)lane, (uint32_t)NP, h0, W.pa[lane]);
+#endif
   __syncwarp(gmask());
+  const uint32_t p_head = lane < NP ? W.pa[lane].head : NIL;
 #ifdef VT_PHASE_TIMING
   if (P.timing && glane() == 0) {  // experiment: phase-A end time replaces the start stamp
     uint64_t ta;
@@ -1133,14 +1417,14 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
   // ================================================================ O9: record
   // first error in (time, prefill before decode, instance) order = the oracle's stop point
-  const double pet = lane < NP ? W.pa_errt[lane] : INF;
+  const double pet = lane < NP ? W.pa[lane].errt : INF;
   const int wp = argmin_time(pet, lane < NP && pet < INF);
   const int wd = argmin_time(dE.t, lane < ND && dE.t < INF);
   if (wp >= 0 || wd >= 0) {
-    const double tp = wp >= 0 ? W.pa_errt[wp] : INF;
+    const double tp = wp >= 0 ? W.pa[wp].errt : INF;
     const double td = wd >= 0 ? gshfl(dE.t, wd) : INF;
     const uint32_t cd = gshfl(dE.code, wd >= 0 ? wd : 0);
-    write_status(P, s, N, (wp >= 0 && tp <= td) ? W.pa_errc[wp] : cd);
+    write_status(P, s, N, (wp >= 0 && tp <= td) ? W.pa[wp].errc : cd);
     if (lane < ND)  // leave the wheel clean for the next scenario of this warp
       for (uint32_t b = 0; b < P.nb; ++b) wst(wheels + (size_t)lane * P.nb + b, make_uint4(0u, 0u, 0u, 0u));
     return;
@@ -1152,7 +1436,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #define LACC(f) D.f
 #endif
   double tl = lane < ND ? LACC(tlast) : 0.0;
-  if (lane < NP) tl = tl > W.pa_tlast[lane] ? tl : W.pa_tlast[lane];
+  if (lane < NP) tl = tl > W.pa[lane].tlast ? tl : W.pa[lane].tlast;
   for (int o = GS / 2; o > 0; o >>= 1) {
     const double x = __shfl_xor_sync(gmask(), tl, o, GS);
     tl = x > tl ? x : tl;
@@ -1183,13 +1467,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     double sttft = 0.0, top = 0.0, epb = 0.0, epi = 0.0, bp = 0.0;
     uint32_t c_ttft = 0, c_itl_p = 0, c_both_p = 0, c_pi = 0;
     for (int q = 0; q < NP; ++q) {
-      hh = splitmix64(hh ^ W.pa_h[q]);
-      sttft = add(sttft, W.pa_sttft[q]);
-      top = add(top, W.pa_top[q]);
-      epb = add(epb, div(W.pa_ebusy[q], 1000.0));
-      epi = add(epi, energy_j(W.p_idle, sub(horizon, W.pa_bms[q])));
-      bp = add(bp, W.pa_bms[q]);
-      c_ttft += W.pa_ttft_ok[q]; c_itl_p += W.pa_itl_ok[q]; c_both_p += W.pa_both[q]; c_pi += W.pa_iters[q];
+      hh = splitmix64(hh ^ W.pa[q].h);
+      sttft = add(sttft, W.pa[q].sttft);
+      top = add(top, W.pa[q].top);
+      epb = add(epb, div(W.pa[q].ebusy, 1000.0));
+      epi = add(epi, energy_j(W.p_idle, sub(horizon, W.pa[q].bms)));
+      bp = add(bp, W.pa[q].bms);
+      c_ttft += W.pa[q].ttft_ok; c_itl_p += W.pa[q].itl_ok; c_both_p += W.pa[q].both; c_pi += W.pa[q].iters;
     }
 #pragma unroll
     for (int d = 0; d < NI; ++d)
@@ -1202,7 +1486,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     uint64_t sc = (uint64_t)c_pi + c_di;  // one decision per iteration ...
     if ((V & 2) && W.wo) {                   // ... unless window control skipped some [C1]
       sc = 0;
-      for (int q = 0; q < NP; ++q) sc += W.pa_ndec[q];
+      for (int q = 0; q < NP; ++q) sc += W.pa[q].ndec;
       for (int d = 0; d < ND; ++d) sc += W.dl_ndec[d];
     }
     R.steps_ctrl = sc; R.steps_route = steps_route; R.decision_hash = hh;
@@ -1263,17 +1547,134 @@ __global__ void __launch_bounds__(SIM_THREADS, SIM_MIN_BLOCKS) simulate_kernel(c
   }
 }
 
+// ------------------------------------------------------------------ K4a: phase A as its own launch
+// One thread per (scenario, prefill instance p): prefill instances never read decode state
+// (A6, A7), so every prefill timeline of every scenario is independent work.
+// The per-thread context names its members as the per-warp block does, so prefill_lane is
+// the same code in both arrangements; the ladder-resolved TTFT / prefill-power rows come
+// from P.rtab (filled by the setup launch), read through L1.
+struct PCtx {
+  double tgt_ttft, slo_ttft, p_idle, tdp, uh_p, uh_d, ctrl_iv, fs_ov;
+  const double *tt, *dyn, *a1g, *c1g, *ut, *noise;
+  const uint16_t *lad;
+  uint32_t B, K, W, kp, ptiles, pcut, mono_tt, ctrl, wo, noise_mask, rq_on, it_on;
+  uint64_t seed, rq_base, it_base;
+};
+
+template <int V, bool F>
+__global__ void __launch_bounds__(PA_THREADS, PA_MIN_BLOCKS) prefill_kernel(const __grid_constant__ SimParams P) {
+  const uint32_t total = P.n * P.np_max;
+  const uint32_t wpb = PA_WARP ? blockDim.x / 32u : blockDim.x;
+  const uint32_t x0 = blockIdx.x * wpb + (PA_WARP ? threadIdx.x / 32u : threadIdx.x);
+  for (uint32_t x = x0; x < total; x += gridDim.x * wpb) {
+    const uint32_t s = x / P.np_max, p = x - s * P.np_max;
+    if (!(P.trace_id[s] < P.n_traces && P.slo_id[s] < P.n_slos && P.layout_id[s] < P.n_layouts &&
+          P.grid_id[s] < P.n_grids && P.profile_id[s] < P.n_profiles))
+      continue;  // K4b writes E_INPUT
+    const voltana_layout &LY = P.lay[P.layout_id[s]];
+    const uint32_t NP = (uint32_t)LY.n_p;
+    if (p >= NP) continue;
+    const uint32_t tr = P.trace_id[s];
+    const uint64_t off = P.offset[tr];
+    const uint64_t N64 = P.offset[tr + 1] - off;
+    if (!(N64 <= P.max_requests)) continue;  // K4b writes E_INPUT (its other checks follow there)
+    const voltana_slo &SL = P.slo[P.slo_id[s]];
+    const uint32_t g = P.grid_id[s], pr = P.profile_id[s];
+    const voltana_grid &GR = P.grid[g];
+    const DevProfile &PR = P.prof[pr];
+    PCtx C;
+    C.rq_on = 0u; C.rq_base = 0; C.it_on = 0u; C.it_base = 0;
+    if ((V & 2) && P.o.req_offset) {
+      C.rq_base = P.o.req_offset[s];
+      const uint64_t len = P.o.req_offset[s + 1] - C.rq_base;
+      if (len != 0 && len != N64) continue;  // K4b writes E_INPUT
+      C.rq_on = len != 0;
+    }
+    if ((V & 2) && P.o.iter_offset) { C.it_on = 1u; C.it_base = P.o.iter_offset[s]; }
+    C.tgt_ttft = mul(SL.scale, SL.ttft_ms);  // A3
+    C.slo_ttft = SL.ttft_ms;
+    C.p_idle = PR.p_idle; C.tdp = PR.tdp; C.uh_p = PR.uh[0]; C.uh_d = PR.uh[1];
+    C.ctrl_iv = LY.ctrl_interval_ms; C.fs_ov = LY.freq_overhead_ms;
+    const double *rt = P.rtab + ((size_t)g * MAX_PROFILES + pr) * RT_STRIDE;
+    C.tt = rt; C.dyn = rt + 2 * VOLTANA_MAX_LEVELS;
+    C.a1g = PR.a1; C.c1g = PR.c1;
+    C.ut = VT_UTAB ? P.utab + (size_t)pr * 2 * SIM_UTAB : nullptr;
+    C.noise = LY.exec_noise; C.noise_mask = LY.noise_len - 1u;
+    C.lad = GR.level;
+    C.B = LY.max_batch_tokens; C.K = (uint32_t)GR.k; C.W = (uint32_t)PR.tile_w; C.kp = (uint32_t)PR.k;
+    C.ptiles = (uint32_t)PR.n_ptiles; C.pcut = PR.pcut;
+    C.ctrl = (uint32_t)LY.ctrl_mode;
+    C.wo = (V & 2) && (LY.ctrl_interval_ms > 0.0 || LY.freq_overhead_ms > 0.0) ? 1u : 0u;
+    C.seed = P.hash_seed[s];
+    {  // coefficient-monotone TTFT rows allow the exact binary search (A32); tiled TTFT: scan (F1)
+      bool mt = PR.n_ptiles <= 1;
+      for (uint32_t k = 0; mt && k + 1 < C.K; ++k)
+        mt = rt[2 * k + 2] <= rt[2 * k] && rt[2 * k + 3] <= rt[2 * k + 1];
+      C.mono_tt = mt;
+    }
+    Node *node = (Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node));
+    PaRes R;
+    if (PA_WARP) {
+      prefill_warp<V, F>(P, C, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p, NP,
+                         P.hash_seed[s], R);
+      if ((threadIdx.x & 31u) == 0) P.pares[(size_t)s * NI + p] = R;
+    } else {
+      prefill_lane<V, F, true>(P, C, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p,
+                               NP, P.hash_seed[s], R);
+      P.pares[(size_t)s * NI + p] = R;
+    }
+  }
+}
+
+template <int V>
+static void launch_pa_v(const SimParams &P, bool fast, int grid, cudaStream_t st) {
+  if (fast) prefill_kernel<V, true><<<grid, PA_THREADS, 0, st>>>(P);
+  else prefill_kernel<V, false><<<grid, PA_THREADS, 0, st>>>(P);
+}
+
+cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st) {
+  const uint64_t total = (uint64_t)P.n * P.np_max;
+  const uint64_t per_cta = PA_WARP ? PA_THREADS / 32 : PA_THREADS;
+  const int grid = (int)((total + per_cta - 1) / per_cta);
+  if (grid < 1) return cudaSuccess;
+  switch (v & 3) {
+    case 1: launch_pa_v<1>(P, fast, grid, st); break;
+    case 2: launch_pa_v<2>(P, fast, grid, st); break;
+    case 3: launch_pa_v<3>(P, fast, grid, st); break;
+    default: launch_pa_v<0>(P, fast, grid, st); break;
+  }
+  return cudaGetLastError();
+}
+
 size_t sim_smem_fixed(bool fast) {
   const size_t b = fast ? sizeof(WarpSmemT<8>) : sizeof(WarpSmemT<VOLTANA_MAX_LEVELS>);
   return (b - sizeof(double) + 15) & ~(size_t)15;
 }
 
 __global__ void utab_kernel(const __grid_constant__ SimParams P) {
-  const uint32_t total = P.n_profiles * 2u * SIM_UTAB;
-  for (uint32_t x = blockIdx.x * blockDim.x + threadIdx.x; x < total; x += gridDim.x * blockDim.x) {
-    const uint32_t pr = x / (2u * SIM_UTAB), ph = (x / SIM_UTAB) & 1u, l = x % SIM_UTAB;
-    const double uh = P.prof[pr].uh[ph];
-    ((double *)P.utab)[x] = div((double)l, add((double)l, uh));
+  const uint32_t stride = gridDim.x * blockDim.x, x0 = blockIdx.x * blockDim.x + threadIdx.x;
+  if (P.utab) {
+    const uint32_t total = P.n_profiles * 2u * SIM_UTAB;
+    for (uint32_t x = x0; x < total; x += stride) {
+      const uint32_t pr = x / (2u * SIM_UTAB), ph = (x / SIM_UTAB) & 1u, l = x % SIM_UTAB;
+      const double uh = P.prof[pr].uh[ph];
+      ((double *)P.utab)[x] = div((double)l, add((double)l, uh));
+    }
+  }
+  if (P.rtab) {  // VT_SPLIT_A: ladder-resolved prefill rows per (grid, profile): [K][a1, c1], DYN_prefill[K]
+    const uint32_t total = P.n_grids * P.n_profiles * VOLTANA_MAX_LEVELS;
+    for (uint32_t x = x0; x < total; x += stride) {
+      const uint32_t g = x / (P.n_profiles * VOLTANA_MAX_LEVELS), r = x % (P.n_profiles * VOLTANA_MAX_LEVELS);
+      const uint32_t pr = r / VOLTANA_MAX_LEVELS, k = r % VOLTANA_MAX_LEVELS;
+      if (k >= (uint32_t)P.grid[g].k) continue;
+      const DevProfile &PR = P.prof[pr];
+      const uint32_t lv = P.grid[g].level[k];
+      if (lv >= (uint32_t)PR.k) continue;  // grid not paired with this profile (host-validated when used)
+      double *rt = P.rtab + ((size_t)g * MAX_PROFILES + pr) * RT_STRIDE;
+      rt[2 * k] = PR.a1[lv];
+      rt[2 * k + 1] = PR.c1[lv];
+      rt[2 * VOLTANA_MAX_LEVELS + k] = PR.dyn[lv];
+    }
   }
 }
 

@@ -20,6 +20,7 @@ namespace {
 thread_local char g_detail[512] = "";
 thread_local int g_launches = 0;
 thread_local uint64_t *g_debug_timing = nullptr;
+thread_local void *g_split_event = nullptr;
 
 voltana_status fail(voltana_status s, const char *fmt, ...) {
   va_list ap;
@@ -103,6 +104,7 @@ const char *voltana_status_string(voltana_status s) {
 const char *voltana_last_error_detail(void) { return g_detail; }
 int voltana_last_launch_count(void) { return g_launches; }
 void voltana_debug_set_timing(uint64_t *buf) { g_debug_timing = buf; }
+void voltana_set_split_event(void *ev) { g_split_event = ev; }
 
 // ------------------------------------------------------------------ K2
 voltana_status voltana_control_step(const voltana_profile *prof_h, int phase, int mode, const uint16_t *ladder_h, int k,
@@ -260,6 +262,7 @@ struct SimLayout {
   size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
   uint32_t n_slots, nb, itl_smem, sw_off, ring_r = 0, ring_nd = 0;
   size_t ring_e_off = 0, ring_c_off = 0;
+  size_t nodes_off = 0, pares_off = 0, rtab_off = 0;  // VT_SPLIT_A
 };
 
 int resident_warps(size_t smem_per_block) {
@@ -297,7 +300,9 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.smem_per_warp += (size_t)max_nd(lays, n_layouts) * VT_SWHEEL * 16;
 #endif
   L.smem = L.smem_per_warp * (SIM_THREADS / 32) * SPW;  // per-scenario block x scenarios per CTA
-  L.node = align256((size_t)tr->max_requests * 16);
+  // VT_SPLIT_A: request nodes live per scenario (K4a writes them before K4b runs), so the
+  // per-warp slot keeps only the far-list array
+  L.node = VT_SPLIT_A ? 0 : align256((size_t)tr->max_requests * 16);
   L.slot = L.node + align256((size_t)tr->max_requests * 4);
   L.slot = L.slot > 256 ? L.slot : 256;
   L.wheel_per_slot = (size_t)max_nd(lays, n_layouts) * L.nb;
@@ -321,6 +326,14 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
 #if VT_UTAB
   L.utab_off = align256(L.total);
   L.total = L.utab_off + (size_t)MAX_PROFILES * 2 * SIM_UTAB * sizeof(double);
+#endif
+#if VT_SPLIT_A
+  L.nodes_off = align256(L.total);
+  L.total = L.nodes_off + align256((size_t)(n < 1 ? 1 : n) * tr->max_requests * 16);
+  L.pares_off = L.total;
+  L.total = L.pares_off + align256((size_t)(n < 1 ? 1 : n) * VOLTANA_MAX_INSTANCES * sizeof(PaRes));
+  L.rtab_off = L.total;
+  L.total = L.rtab_off + (size_t)MAX_GRIDS * MAX_PROFILES * RT_STRIDE * sizeof(double);
 #endif
   return L;
 }
@@ -463,6 +476,16 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
 #if VT_UTAB
   P->utab = (const double *)(ws + L.utab_off);
 #endif
+#if VT_SPLIT_A
+  P->nodes = ws + L.nodes_off;
+  P->pares = (PaRes *)(ws + L.pares_off);
+  P->rtab = (double *)(ws + L.rtab_off);
+  P->np_max = 1;
+  for (int i = 0; i < n_layouts; ++i) P->np_max = (uint32_t)layouts_h[i].n_p > P->np_max ? layouts_h[i].n_p : P->np_max;
+#ifdef VT_PA_SPREAD
+  P->np_max = P->np_max < VT_PA_SPREAD ? VT_PA_SPREAD : P->np_max;  // experiment: threads per scenario in K4a
+#endif
+#endif
   P->wheel_per_slot = L.wheel_per_slot;
   P->itl_smem = L.itl_smem;
   P->smem_per_warp = (uint32_t)L.smem_per_warp;
@@ -487,14 +510,22 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     if (x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 || x.exec_noise != nullptr || x.itl_mode != 0) v |= 2;
   }
   if (P->o.req_offset != nullptr || P->o.iter_offset != nullptr) v |= 2;  // outputs (E1-E2)
-#if VT_UTAB
-  e = launch_utab(*P, st);
-  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate utab launch"); }
+#if VT_UTAB || VT_SPLIT_A
+  e = launch_utab(*P, st);  // setup: utilisation table and ladder-resolved prefill rows
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate setup launch"); }
 #endif
+#if VT_SPLIT_A
+  e = launch_prefill(*P, v, fast, st);  // K4a: every prefill timeline of every scenario
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate prefill launch"); }
+#endif
+  if (g_split_event) {
+    e = cudaEventRecord((cudaEvent_t)g_split_event, st);
+    if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate split event"); }
+  }
   e = launch_sim(*P, v, fast, grid, L.smem, st);
   delete P;
   if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
-  g_launches = 1 + VT_UTAB;
+  g_launches = 1 + ((VT_UTAB || VT_SPLIT_A) ? 1 : 0) + (VT_SPLIT_A ? 1 : 0);
   return ok();
 }
 

@@ -33,6 +33,26 @@ constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in s
 constexpr uint32_t SIM_UTAB = 8192;         // loads with a tabulated utilisation (VT_UTAB)
 constexpr uint32_t SIM_WHEEL_MAX = VT_NBMAX; // decode wheel buckets (L2-resident); longer requests use the far list
 
+#ifndef VT_SPLIT_A
+#define VT_SPLIT_A 1  // phase A (prefill lanes) as its own launch (K4a) ahead of the decode kernel
+#endif
+#ifndef VT_PA_WARP
+#define VT_PA_WARP 1  // K4a: one warp per (scenario, prefill instance) (0: one thread each)
+#endif
+constexpr bool PA_WARP = VT_PA_WARP;
+constexpr int PA_THREADS = VT_PA_WARP ? 128 : 32;
+#ifndef VT_PA_MIN_BLOCKS
+#define VT_PA_MIN_BLOCKS 6
+#endif
+constexpr int PA_MIN_BLOCKS = VT_PA_WARP ? VT_PA_MIN_BLOCKS : 1;
+constexpr int RT_STRIDE = 3 * VOLTANA_MAX_LEVELS;  // resolved ladder row: [K][a1, c1] then prefill DYN [K]
+
+struct PaRes {     // phase-A result of one prefill instance (K4a -> K4b; the record's prefill part)
+  double ebusy, bms, top, sttft, tlast, errt;  // W*ms, ms, ms, ms, last event, first error time (+inf none)
+  uint64_t h;                                  // decision-hash chain (A36)
+  uint32_t iters, ttft_ok, itl_ok, both, errc, ndec, head, pad;  // head: first routed request (NIL none)
+};
+
 struct SimParams {
   // traces (device)
   const double *arrival;
@@ -65,6 +85,10 @@ struct SimParams {
   double *ring_e;              // ITL modes (E3): [n_slots][max N_D][ring_r] iteration end times
   uint32_t *ring_c;            //   ... and cumulative counts of gaps above the ITL SLO
   uint32_t ring_r, ring_nd;    //   ring length (power of two >= max_out), instances per slot
+  char *nodes;                 // VT_SPLIT_A: [n][max_requests] 16-B request nodes (scenario in kernel order)
+  PaRes *pares;                // VT_SPLIT_A: [n][VOLTANA_MAX_INSTANCES] phase-A results
+  double *rtab;                // VT_SPLIT_A: [MAX_GRIDS][MAX_PROFILES][RT_STRIDE] ladder-resolved prefill tables
+  uint32_t np_max;             // VT_SPLIT_A: max N_P over the launch's layouts (K4a threads per scenario)
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];
@@ -78,5 +102,6 @@ struct SimParams {
 const void *sim_kernel_ptr(int v, bool fast);
 cudaError_t launch_sim(const SimParams &P, int v, bool fast, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_utab(const SimParams &P, cudaStream_t st);  // VT_UTAB: fill P.utab
+cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st);  // K4a (VT_SPLIT_A)
 
 }  // namespace vt

@@ -1,0 +1,6 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+for so in "" variants/lib_pamb4.so variants/lib_pamb6.so; do
+  VOLTANA_SO=$so timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/pa2.csv python tools/prof_sim.py --reps 1 > /dev/null 2>&1
+  echo "== $so"; grep -v "^==" gpurun_out/pa2.csv | awk -F'","' '{print $5, $NF}' | tail -3
+done
+timeout 300 python tools/prof_sim.py --reps 3

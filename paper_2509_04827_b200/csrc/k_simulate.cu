@@ -70,6 +70,9 @@
 #ifndef VT_PFA
 #define VT_PFA 0       // prefill lanes: prefetch the trace this many requests ahead (0 = off)
 #endif
+#ifndef VT_EDEFER
+#define VT_EDEFER 1    // decode busy energy: utilisation/DYN loads issued at START, accumulated at END
+#endif
 #ifndef VT_ITL_SMEM_ONLY
 #define VT_ITL_SMEM_ONLY 0  // experiment: assume the ITL table is staged (no global fallback)
 #endif
@@ -311,6 +314,9 @@ struct Dec {               // decode instance d, owned by lane d
   uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both, nfifo, far_h, far_hfin;
   bool busy, dead;
   double end, ebusy, bms, top, sitl, tlast;
+#if VT_EDEFER
+  double e_u, e_dyn, e_dur;  // running iteration's utilisation, DYN entry and duration (energy added at END)
+#endif
   uint64_t h;
   uint4 bcur;              // bucket of the running iteration, read at its START (final by then)
 #if VT_QCACHE
@@ -491,6 +497,12 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       }
       D.busy = false;
       ACC(tlast) = tnow;
+#if VT_EDEFER
+      {  // busy energy of the iteration that just ended, in iteration order (W*ms, A23)
+        const double w = add(W.p_idle, mul(D.e_u, D.e_dyn));
+        ACC(ebusy) = add(ACC(ebusy), mul(w < W.tdp ? w : W.tdp, D.e_dur));
+      }
+#endif
     } else {
       // idle: the next START happens when the head of the admission queue becomes available
       if (D.qh == NIL) return;
@@ -583,7 +595,15 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       W.re[ro] = D.end;
       W.rc[ro] = W.dl_vc[d];
     }
+#if VT_EDEFER
+    // the table loads are consumed at this iteration's END (off the in-order path of the START)
+    D.e_u = D.nreq < SIM_UTAB && VT_UTAB ? __ldg(W.ut + SIM_UTAB + D.nreq)
+                                          : div((double)D.nreq, add((double)D.nreq, W.uh_d));
+    D.e_dyn = W.dyn[W.K + k];
+    D.e_dur = dur;
+#else
     ACC(ebusy) = add(ACC(ebusy), mul(bpow(W, 1, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
+#endif
     ACC(bms) = add(ACC(bms), dur);
     if (k == (int)W.K - 1) ACC(top) = add(ACC(top), dur);
     D.cur = D.iters;
@@ -847,6 +867,22 @@ __device__ void prefill_lane(const SimParams &P, WS &W, Node *node, const double
 //    ballots, and each routed request links to the next routed one.
 // A batch longer than the window (> 32 requests) takes the general path (rounds of 32).
 
+// K4a lane groups: G lanes per prefill instance (32 / G instances per warp); every collective
+// is masked to the group, lane indices and window positions are group-relative.
+template <int G> struct Grp {
+  uint32_t gl, base;
+  unsigned m;
+  __device__ __forceinline__ Grp() {
+    gl = threadIdx.x & (G - 1);
+    base = (threadIdx.x & 31u) & ~(uint32_t)(G - 1);
+    m = G == 32 ? 0xffffffffu : (((1u << G) - 1u) << base);
+  }
+  __device__ __forceinline__ unsigned ballot(bool p) const { return __ballot_sync(m, p) >> base; }
+  template <class T> __device__ __forceinline__ T shfl(T v, int src) const { return __shfl_sync(m, v, src, G); }
+  template <class T> __device__ __forceinline__ T shfl_up(T v, int d) const { return __shfl_up_sync(m, v, d, G); }
+  static constexpr unsigned all = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
+};
+
 struct PState {   // uniform state of one prefill instance (every lane holds the same values)
   double ebusy, bms, top, sttft, tlast, errt, tfree, last;
   uint64_t h;
@@ -856,7 +892,7 @@ struct PState {   // uniform state of one prefill instance (every lane holds the
 
 // O7 decision for a batch of nbt tokens starting at ts, head arrival a0: EcoFreq,
 // duration, energy (A23). false: per-item error recorded in S.
-template <int V, bool F, class WS>
+template <int V, bool F, int G, class WS>
 __device__ __forceinline__ bool pa_decide(const SimParams &P, const WS &W, PState &S, uint32_t p, double ts,
                                           double a0, uint32_t nbt, bool backlog, double &end) {
   double budget = sub(W.tgt_ttft, sub(ts, a0));  // A4: SLO minus the oldest request's wait
@@ -888,7 +924,7 @@ __device__ __forceinline__ bool pa_decide(const SimParams &P, const WS &W, PStat
     if (k != (int)S.cur && W.fs_ov > 0.0) { t0 = add(ts, W.fs_ov); fl |= 2u; }
     S.cur = (uint32_t)k;
   }
-  if ((V & 2) && (threadIdx.x & 31u) == 0) log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
+  if ((V & 2) && (threadIdx.x & (G - 1)) == 0) log_iter(P.o, W, p, jit, ts, dur, nbt, 0u, k, fl);
   end = add(t0, dur);
   S.ebusy = add(S.ebusy, mul(bpow(W, 0, W.dyn[k], nbt), dur));  // W*ms (A23)
   S.bms = add(S.bms, dur);
@@ -899,11 +935,12 @@ __device__ __forceinline__ bool pa_decide(const SimParams &P, const WS &W, PStat
 }
 
 // O5 for lanes [0, n): request base + lane*NP (arrival a, in x, out o) finished prefill at e.
-template <int V, class WS>
+template <int V, int G, class WS>
 __device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PState &S, Node *node, uint32_t base,
                                            uint32_t NP, uint32_t n, double e, double a, uint32_t x, uint32_t o) {
   if (n == 0u) return;
-  const uint32_t lane = threadIdx.x & 31u;
+  const Grp<G> g;
+  const uint32_t lane = g.gl;
   const bool valid = lane < n;
   const uint32_t i = base + lane * NP;
   const double ttft = valid ? sub(e, a) : 0.0;  // A26
@@ -911,15 +948,15 @@ __device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PSta
   for (uint32_t b = 0; b < n; b += 8u) {  // the report sum in FCFS order (A37)
     double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = __shfl_sync(FULL, ttft, (int)(b + u) & 31);
+    for (int u = 0; u < 8; ++u) v[u] = g.shfl(ttft, (int)(b + u) & (G - 1));
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (b + u < n) S.sttft = add(S.sttft, v[u]);
   }
-  S.ttft_ok += __popc(__ballot_sync(FULL, ok));
+  S.ttft_ok += __popc(g.ballot(ok));
   const bool one = valid && o == 1u;  // first token came from prefill: done (A8, A30)
-  S.itl_ok += __popc(__ballot_sync(FULL, one));
-  S.both += __popc(__ballot_sync(FULL, one && ok));
+  S.itl_ok += __popc(g.ballot(one));
+  S.both += __popc(g.ballot(one && ok));
   if ((V & 2) && W.rq_on && valid) {  // per-request record (E1)
     P.o.req_tfirst[W.rq_base + i] = e;
     if (o == 1u) {
@@ -927,7 +964,7 @@ __device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PSta
       P.o.req_decode[W.rq_base + i] = 0xFF; P.o.req_case[W.rq_base + i] = 0xFF;
     }
   }
-  const unsigned rm = __ballot_sync(FULL, valid && o != 1u);  // routed requests, FCFS = lane order
+  const unsigned rm = g.ballot(valid && o != 1u);  // routed requests, FCFS = lane order
   if (rm == 0u) return;
   const int f0 = ffs0(rm), ll = 31 - __clz(rm);
   const uint32_t i_first = base + (uint32_t)f0 * NP;
@@ -946,20 +983,21 @@ __device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PSta
     node[i] = me;
   }
   S.prev = base + (uint32_t)ll * NP;  // the last routed request: pending until its successor
-  S.pend.tf = __shfl_sync(FULL, me.tf, ll);
-  S.pend.in = (uint16_t)__shfl_sync(FULL, (uint32_t)me.in, ll);
-  S.pend.out = (uint16_t)__shfl_sync(FULL, (uint32_t)me.out, ll);
+  S.pend.tf = g.shfl(me.tf, ll);
+  S.pend.in = (uint16_t)g.shfl((uint32_t)me.in, ll);
+  S.pend.out = (uint16_t)g.shfl((uint32_t)me.out, ll);
   S.pend.next = NIL;
 }
 
 // General path for one batch starting at request nxt (any length): candidates in rounds of 32,
 // accounting in chunks of 32. Returns the next unbatched request, or NIL on an error.
-template <int V, bool F, class WS>
+template <int V, bool F, int G, class WS>
 __device__ uint32_t pa_batch_general(const SimParams &P, const WS &W, PState &S, Node *node, const double *arr,
                                      const uint32_t *inl, const uint32_t *outl, uint32_t N, uint32_t p,
                                      uint32_t NP, uint32_t nxt) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
-  const uint32_t lane = threadIdx.x & 31u, B = W.B;
+  const Grp<G> g;
+  const uint32_t lane = g.gl, B = W.B;
   const double a0 = arr[nxt];
   const double ts = S.tfree > a0 ? S.tfree : a0;
   uint32_t nbt = inl[nxt], cnt = 1, id = nxt + NP;
@@ -971,41 +1009,42 @@ __device__ uint32_t pa_batch_general(const SimParams &P, const WS &W, PState &S,
     const uint32_t xv = in_tr ? inl[j] : 0u;
     uint32_t ps = xv;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, ps, o);
+    for (int o = 1; o < G; o <<= 1) {
+      const uint32_t y = g.shfl_up(ps, o);
       if (lane >= (uint32_t)o) ps += y;
     }
     const bool arrived = av <= ts;
-    const unsigned m = __ballot_sync(FULL, arrived && !(nbt + ps > B));
-    const uint32_t f = m == FULL ? 32u : (uint32_t)ffs0(~m);
+    const unsigned m = g.ballot(arrived && !(nbt + ps > B));
+    const uint32_t f = m == Grp<G>::all ? (uint32_t)G : (uint32_t)ffs0(~m);
     if (f > 0u) {
-      nbt += __shfl_sync(FULL, ps, (int)f - 1);
+      nbt += g.shfl(ps, (int)f - 1);
       cnt += f;
       id += f * NP;
     }
-    if (f < 32u) {
-      backlog = __shfl_sync(FULL, arrived, (int)f);
+    if (f < (uint32_t)G) {
+      backlog = g.shfl(arrived, (int)f);
       break;
     }
   }
   double end;
-  if (!pa_decide<V, F>(P, W, S, p, ts, a0, nbt, backlog, end)) return NIL;
-  for (uint32_t q0 = 0; q0 < cnt; q0 += 32u) {
-    const uint32_t nv = cnt - q0 < 32u ? cnt - q0 : 32u;
+  if (!pa_decide<V, F, G>(P, W, S, p, ts, a0, nbt, backlog, end)) return NIL;
+  for (uint32_t q0 = 0; q0 < cnt; q0 += (uint32_t)G) {
+    const uint32_t nv = cnt - q0 < (uint32_t)G ? cnt - q0 : (uint32_t)G;
     const uint32_t i = nxt + (q0 + lane) * NP;
     double a = 0.0;
     uint32_t x = 0u, o = 0u;
     if (lane < nv) { a = arr[i]; x = inl[i]; o = outl[i]; }
-    pa_account<V>(P, W, S, node, nxt + q0 * NP, NP, nv, end, a, x, o);
+    pa_account<V, G>(P, W, S, node, nxt + q0 * NP, NP, nv, end, a, x, o);
   }
   return id;
 }
 
-template <int V, bool F, class WS>
+template <int V, bool F, int G, class WS>
 __device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double *arr, const uint32_t *inl,
                              const uint32_t *outl, uint32_t N, uint32_t p, uint32_t NP, uint64_t h0, PaRes &R) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
-  const uint32_t lane = threadIdx.x & 31u, B = W.B;
+  const Grp<G> g;
+  const uint32_t lane = g.gl, B = W.B;
   PState S;
   S.ebusy = S.bms = S.top = S.sttft = S.tlast = S.tfree = 0.0;
   S.errt = INF;
@@ -1027,7 +1066,7 @@ __device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double
         pf2 += PA_PF_CHUNK;
       }
     const uint32_t rem = (N - wbase + NP - 1u) / NP;  // requests left on this instance
-    const uint32_t nwin = rem < 32u ? rem : 32u;
+    const uint32_t nwin = rem < (uint32_t)G ? rem : (uint32_t)G;
     const uint32_t idx = wbase + lane * NP;
     const bool v = lane < nwin;
     const double a = v ? arr[idx] : INF;  // past the trace end: "not arrived"
@@ -1035,37 +1074,37 @@ __device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double
     const uint32_t o = v ? outl[idx] : 0u;
     uint32_t ps = x;
 #pragma unroll
-    for (int s = 1; s < 32; s <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, ps, s);
+    for (int s = 1; s < G; s <<= 1) {
+      const uint32_t y = g.shfl_up(ps, s);
       if (lane >= (uint32_t)s) ps += y;
     }
     double e = 0.0;            // this lane's batch end, once its batch has started
     uint32_t hl = 0;           // head lane of the next batch
     bool err = false, general = false;
     while (hl < nwin) {
-      const double a0 = __shfl_sync(FULL, a, (int)hl);
+      const double a0 = g.shfl(a, (int)hl);
       const double ts = S.tfree > a0 ? S.tfree : a0;  // START: instance idle and queue non-empty
-      const uint32_t psb = hl ? __shfl_sync(FULL, ps, (int)(hl - 1u)) : 0u;  // tokens before the head
+      const uint32_t psb = hl ? g.shfl(ps, (int)(hl - 1u)) : 0u;  // tokens before the head
       const bool arrived = a <= ts;
       const bool take = lane > hl && arrived && !(ps - psb > B);
-      const unsigned fails = __ballot_sync(FULL, lane > hl && !take);
+      const unsigned fails = g.ballot(lane > hl && !take);
       if (fails == 0u) {       // a full window of arrivals that all fit: the batch may run on
         general = hl == 0u;    // more than 32 requests: the general path; else re-window at the head
         break;
       }
       const uint32_t f = (uint32_t)ffs0(fails);  // first candidate not taken
-      const bool backlog = __shfl_sync(FULL, arrived, (int)f);  // arrived but does not fit (A5)
-      const uint32_t nbt = __shfl_sync(FULL, ps, (int)(f - 1u)) - psb;
+      const bool backlog = g.shfl(arrived, (int)f);  // arrived but does not fit (A5)
+      const uint32_t nbt = g.shfl(ps, (int)(f - 1u)) - psb;
       double end;
-      if (!pa_decide<V, F>(P, W, S, p, ts, a0, nbt, backlog, end)) { err = true; break; }
+      if (!pa_decide<V, F, G>(P, W, S, p, ts, a0, nbt, backlog, end)) { err = true; break; }
       if (lane >= hl && lane < f) e = end;
       hl = f;
     }
-    pa_account<V>(P, W, S, node, wbase, NP, hl, e, a, x, o);  // O5 for the window's batches
+    pa_account<V, G>(P, W, S, node, wbase, NP, hl, e, a, x, o);  // O5 for the window's batches
     wbase += hl * NP;
     if (err) break;
     if (general) {
-      wbase = pa_batch_general<V, F>(P, W, S, node, arr, inl, outl, N, p, NP, wbase);
+      wbase = pa_batch_general<V, F, G>(P, W, S, node, arr, inl, outl, N, p, NP, wbase);
       if (wbase == NIL) break;
     }
   }
@@ -1245,6 +1284,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   D.busy = false;
   D.dead = !(lane < ND);
   D.end = 0.0;
+#if VT_EDEFER
+  D.e_u = D.e_dyn = D.e_dur = 0.0;
+#endif
   {
     const int d = lane < ND ? lane : 0;
     if (lane < ND || !VT_DACC_SMEM) {
@@ -1564,8 +1606,8 @@ struct PCtx {
 template <int V, bool F>
 __global__ void __launch_bounds__(PA_THREADS, PA_MIN_BLOCKS) prefill_kernel(const __grid_constant__ SimParams P) {
   const uint32_t total = P.n * P.np_max;
-  const uint32_t wpb = PA_WARP ? blockDim.x / 32u : blockDim.x;
-  const uint32_t x0 = blockIdx.x * wpb + (PA_WARP ? threadIdx.x / 32u : threadIdx.x);
+  const uint32_t wpb = PA_WARP ? blockDim.x / PA_G : blockDim.x;
+  const uint32_t x0 = blockIdx.x * wpb + (PA_WARP ? threadIdx.x / PA_G : threadIdx.x);
   for (uint32_t x = x0; x < total; x += gridDim.x * wpb) {
     const uint32_t s = x / P.np_max, p = x - s * P.np_max;
     if (!(P.trace_id[s] < P.n_traces && P.slo_id[s] < P.n_slos && P.layout_id[s] < P.n_layouts &&
@@ -1614,10 +1656,22 @@ __global__ void __launch_bounds__(PA_THREADS, PA_MIN_BLOCKS) prefill_kernel(cons
     }
     Node *node = (Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node));
     PaRes R;
+#ifdef VT_PA_TIMING
+    uint64_t tq0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
+#endif
     if (PA_WARP) {
-      prefill_warp<V, F>(P, C, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p, NP,
+      prefill_warp<V, F, PA_G>(P, C, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p, NP,
                          P.hash_seed[s], R);
-      if ((threadIdx.x & 31u) == 0) P.pares[(size_t)s * NI + p] = R;
+      if ((threadIdx.x & (PA_G - 1)) == 0) P.pares[(size_t)s * NI + p] = R;
+#ifdef VT_PA_TIMING
+      if (P.timing && (threadIdx.x & (PA_G - 1)) == 0) {  // experiment: [x][2] chain start, duration
+        uint64_t tq1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq1));
+        P.timing[2 * (size_t)P.n + 2 * x] = tq0;   // after K4b's [n][2]
+        P.timing[2 * (size_t)P.n + 2 * x + 1] = tq1 - tq0;
+      }
+#endif
     } else {
       prefill_lane<V, F, true>(P, C, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p,
                                NP, P.hash_seed[s], R);
@@ -1634,7 +1688,7 @@ static void launch_pa_v(const SimParams &P, bool fast, int grid, cudaStream_t st
 
 cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st) {
   const uint64_t total = (uint64_t)P.n * P.np_max;
-  const uint64_t per_cta = PA_WARP ? PA_THREADS / 32 : PA_THREADS;
+  const uint64_t per_cta = PA_WARP ? PA_THREADS / PA_G : PA_THREADS;
   const int grid = (int)((total + per_cta - 1) / per_cta);
   if (grid < 1) return cudaSuccess;
   switch (v & 3) {

@@ -40,6 +40,10 @@ constexpr uint32_t SIM_WHEEL_MAX = VT_NBMAX; // decode wheel buckets (L2-residen
 #define VT_PA_WARP 1  // K4a: one warp per (scenario, prefill instance) (0: one thread each)
 #endif
 constexpr bool PA_WARP = VT_PA_WARP;
+#ifndef VT_PA_G
+#define VT_PA_G 32    // K4a: lanes per prefill instance (a power of two <= 32): 32 / G instances per warp
+#endif
+constexpr int PA_G = VT_PA_G;
 constexpr int PA_THREADS = VT_PA_WARP ? 128 : 32;
 #ifndef VT_PA_MIN_BLOCKS
 #define VT_PA_MIN_BLOCKS 6

@@ -70,8 +70,11 @@
 #ifndef VT_PFA
 #define VT_PFA 0       // prefill lanes: prefetch the trace this many requests ahead (0 = off)
 #endif
+#ifndef VT_NODE_PF_L2
+#define VT_NODE_PF_L2 0  // K4b: bulk L2 prefetch of the node array this many requests ahead (1024/4096: no gain)
+#endif
 #ifndef VT_EDEFER
-#define VT_EDEFER 1    // decode busy energy: utilisation/DYN loads issued at START, accumulated at END
+#define VT_EDEFER 0    // decode busy energy: table loads issued at START, added at END (measured: no gain)
 #endif
 #ifndef VT_ITL_SMEM_ONLY
 #define VT_ITL_SMEM_ONLY 0  // experiment: assume the ITL table is staged (no global fallback)
@@ -153,6 +156,7 @@ struct WarpSmemT {
   double *re;                      // ITL modes (E3): this slot's rings [N_D][ring_r] of iteration end times
   uint32_t *rc;                    //   ... and of cumulative counts of gaps above the ITL SLO
   uint32_t itlm, rmask;            //   layout itl_mode, ring_r - 1
+  uint32_t clog_m;                 // VT_DEFER_ITL: log slots handed out (chunks of CLOG_CHUNK)
   uint32_t wo;                     // window control or blocking overhead active (C1-C3)
   uint32_t dl_vc[VOLTANA_MAX_INSTANCES];  // decode lane: gaps above the ITL SLO so far
   uint64_t rq_base, it_base;       // outputs (E1-E3): request / iteration-slot base of the scenario
@@ -319,6 +323,10 @@ struct Dec {               // decode instance d, owned by lane d
 #endif
   uint64_t h;
   uint4 bcur;              // bucket of the running iteration, read at its START (final by then)
+#if VT_DEFER_ITL
+  uint32_t lpos, lend;     // this lane's chunk [lpos, lend) of the scenario's completion log
+  bool lneed;              // the chunk is full: dec_advance stopped before an END
+#endif
 #if VT_QCACHE
   Node qhn;                // register copy of the admission-queue head node
 #endif
@@ -340,6 +348,7 @@ struct Lane {              // per-lane pointers
   uint4 *wheel;            // this lane's decode instance: [NB] buckets
   uint32_t *fid;
   double *ft;
+  CEnt *clog;              // VT_DEFER_ITL: the scenario's completion log
 };
 
 __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
@@ -354,6 +363,10 @@ __device__ __forceinline__ Node queue_head(const Dec &D, const Lane &L) {
 // nodes of up to four lists are loaded together.
 template <int V, bool F, class WS>
 __device__ void itl_drain(Dec &D, const Lane &L, WS &W, int d, const voltana_outputs &O) {
+#ifdef VT_ITL_SKIP
+  D.nfifo = 0;  // experiment only (wrong records): the cost of the ITL walk
+  return;
+#endif
   const double slo = W.slo_itl;
   for (uint32_t e0 = 0; e0 < D.nfifo; e0 += 4) {
     Node h4[4];
@@ -478,6 +491,9 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     bool cont = false;  // this START follows an END at the same time (the instance stays busy)
     if (D.busy) {
       if (!(D.end < t_lim)) return;
+#if VT_DEFER_ITL
+      if (!(V & 2) && D.lpos == D.lend) { D.lneed = true; return; }  // a new chunk first (dec_advance_all)
+#endif
       tnow = D.end;
       cont = true;
       // ---- O6 DecodeIterDone: +1 KV token per running request; this iteration's completions
@@ -491,9 +507,18 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
 #else
         wst(L.wheel + (D.cur & nbm), make_uint4(0u, 0u, 0u, 0u));
 #endif
-        L.fid[D.nfifo] = b.x - 1u;
-        L.ft[D.nfifo] = tnow;
-        if (++D.nfifo == VT_ITL_FIFO) itl_drain<V, F>(D, L, W, d, O);
+#if VT_DEFER_ITL
+        if (!(V & 2)) {  // log (td, list head, instance); K4c does the ITL accounting (A30, A37)
+          CEnt ce;
+          ce.td = tnow; ce.head = b.x - 1u; ce.d = (uint32_t)d;
+          L.clog[D.lpos++] = ce;
+        } else
+#endif
+        {
+          L.fid[D.nfifo] = b.x - 1u;
+          L.ft[D.nfifo] = tnow;
+          if (++D.nfifo == VT_ITL_FIFO) itl_drain<V, F>(D, L, W, d, O);
+        }
       }
       D.busy = false;
       ACC(tlast) = tnow;
@@ -631,6 +656,34 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     }
 #endif
   }
+}
+
+// dec_advance for every lane of the warp (converged call site). VT_DEFER_ITL: a lane whose log
+// chunk is full stops before its next END; the warp then hands out new chunks in lane order
+// (one ballot, no atomics: shared-memory atomics inside the divergent advance cost 75 % of K4b)
+// and those lanes continue.
+template <int V, bool F, class WS>
+__device__ __forceinline__ void dec_advance_all(Dec &D, int d, const Lane &L, WS &W, double t_lim, Err &E,
+                                                const voltana_outputs &O) {
+  dec_advance<V, F>(D, d, L, W, t_lim, E, O);
+#if VT_DEFER_ITL
+  if (!(V & 2)) {
+    for (;;) {
+      const unsigned nm = gballot(D.lneed);
+      if (nm == 0u) break;
+      const uint32_t top = W.clog_m;
+      if (D.lneed) {
+        D.lpos = top + CLOG_CHUNK * (uint32_t)__popc(nm & ((1u << glane()) - 1u));
+        D.lend = D.lpos + CLOG_CHUNK;
+        D.lneed = false;
+        dec_advance<V, F>(D, d, L, W, t_lim, E, O);
+      }
+      __syncwarp(gmask());
+      if (glane() == 0) W.clog_m = top + CLOG_CHUNK * (uint32_t)__popc(nm);
+      __syncwarp(gmask());
+    }
+  }
+#endif
 }
 
 // Append request i (routed at its first-token time) to instance d's admission queue.
@@ -1276,6 +1329,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   L.wheel = wheels + (size_t)dl * P.nb;
   L.fid = W.fid[dl];
   L.ft = W.ft[dl];
+#if VT_DEFER_ITL
+  L.clog = P.clog + (size_t)s * P.clog_stride;
+  if (lane == 0) W.clog_m = (uint32_t)ND * CLOG_CHUNK;  // the first chunk of every decode lane
+  __syncwarp(gmask());
+#endif
   Dec D;
   D.nreq = D.nkv = D.pn = D.pkv = D.iters = D.cur = 0;
   D.qh = D.qt = NIL;
@@ -1284,6 +1342,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   D.busy = false;
   D.dead = !(lane < ND);
   D.end = 0.0;
+#if VT_DEFER_ITL
+  D.lpos = (uint32_t)lane * CLOG_CHUNK;  // first chunks: one per lane, allocated in lane order
+  D.lend = D.lpos + CLOG_CHUNK;
+  D.lneed = false;
+#endif
 #if VT_EDEFER
   D.e_u = D.e_dyn = D.e_dur = 0.0;
 #endif
@@ -1309,6 +1372,12 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
   // stream head of prefill lane p (head node hn and, loaded one step ahead, its successor nn)
   uint32_t hd = lane < NP ? p_head : NIL;
+#if VT_SPLIT_A && VT_NODE_PF_L2
+  uint32_t npf = 0;  // nodes [0, npf) of the scenario already prefetched into L2 (shared by the streams)
+  if (lane < NP)
+    for (; npf < (uint32_t)VT_NODE_PF_L2 && npf < N; npf += 256u)
+      prefetch_l2_range(node, npf, N - npf < 256u ? N - npf : 256u, 16u);
+#endif
   Node hn, nn;
   hn.tf = 0.0; hn.next = NIL; hn.in = 0; hn.out = 0;
   nn = hn;
@@ -1344,6 +1413,13 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         prefetch_l1(node + hn.next + 8u);  // the stream's next line (ids advance by N_P)
 #endif
       }
+#if VT_SPLIT_A && VT_NODE_PF_L2
+      // K4a wrote the node array long before (DRAM): keep the stream's next nodes coming into L2
+      if (hd != NIL && hd + (uint32_t)VT_NODE_PF_L2 > npf && npf < N) {
+        prefetch_l2_range(node, npf, N - npf < 256u ? N - npf : 256u, 16u);
+        npf += 256u;
+      }
+#endif
     }
 #if VT_PIPE_ARGMIN
     // the next request depends only on the stream heads: its selection overlaps this route
@@ -1351,7 +1427,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #endif
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
-      dec_advance<V, F>(D, lane, L, W, t, dE, P.o);
+      dec_advance_all<V, F>(D, lane, L, W, t, dE, P.o);
       t_adv = t;
     }
     // ---- O8 EcoRoute
@@ -1452,8 +1528,16 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #endif
   }
   // drain: every decode instance runs to completion, then its deferred ITL accounting
-  dec_advance<V, F>(D, lane, L, W, INF, dE, P.o);
+  dec_advance_all<V, F>(D, lane, L, W, INF, dE, P.o);
   if (lane < ND && !D.dead) itl_drain<V, F>(D, L, W, lane, P.o);
+#if VT_DEFER_ITL
+  if (!(V & 2)) {
+    if (lane < ND)  // the unused rest of this lane's chunk: empty entries
+      for (uint32_t q = D.lpos; q < D.lend; ++q) { CEnt ce; ce.td = 0.0; ce.head = NIL; ce.d = 0u; L.clog[q] = ce; }
+    __syncwarp(gmask());
+    if (lane == 0) P.clog_n[s] = W.clog_m;
+  }
+#endif
   if ((V & 2) && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
   __syncwarp(gmask());
 
@@ -1697,6 +1781,91 @@ cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st
     case 3: launch_pa_v<3>(P, fast, grid, st); break;
     default: launch_pa_v<0>(P, fast, grid, st); break;
   }
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K4c: deferred ITL accounting
+// The per-request mean-ITL accounting of O6 (A30) for the paper's-policy kernels, taken off
+// K4b's in-order path: K4b logs every iteration end with completions (end time, head of the
+// completion list, instance) in its own order; here one warp per scenario walks the lists.
+// Lanes gather 32 log entries at a time (each walks its list, up to 4 values in registers),
+// then the values are added to their instance's running sum one by one in log order, so each
+// instance's sum is the oracle's sequential sum in completion order (A37); the counts are
+// order-free. The record's decode ITL fields are completed here (K4b wrote the prefill part).
+__global__ void __launch_bounds__(128) itl_kernel(const __grid_constant__ SimParams P) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < P.n; s += nw) {
+    voltana_result *R = P.out + s;
+    if (R->status != 0u) continue;
+    const uint32_t m = P.clog_n[s];
+    const CEnt *E = P.clog + (size_t)s * P.clog_stride;
+    const Node *node = (const Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node));
+    const double slo = P.slo[P.slo_id[s]].itl_ms;
+    double sd = 0.0;                // lane d: instance d's running sum
+    uint32_t c_ok = 0, c_both = 0;  // this lane's counts
+    for (uint32_t c0 = 0; c0 < m; c0 += 32u) {
+      const bool v = c0 + lane < m;
+      CEnt e;
+      e.td = 0.0; e.head = NIL; e.d = 0u;
+      if (v) e = E[c0 + lane];
+      double x[4];
+      uint32_t cnt = 0, id = e.head;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        x[j] = 0.0;
+        if (id != NIL) {
+          const Node nd = node[id];
+          x[j] = div(sub(e.td, fabs(nd.tf)), (double)(nd.out - 1u));
+          const bool ok = x[j] <= slo;
+          c_ok += ok;
+          c_both += ok && nd.tf > 0.0;
+          cnt++;
+          id = nd.next;
+        }
+      }
+      const uint32_t nv = m - c0 < 32u ? m - c0 : 32u;
+      for (uint32_t l = 0; l < nv; ++l) {  // log order
+        const uint32_t dl = __shfl_sync(FULL, e.d, (int)l), cl = __shfl_sync(FULL, cnt, (int)l);
+        double y[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) y[j] = __shfl_sync(FULL, x[j], (int)l);
+        if (lane == dl) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if ((uint32_t)j < cl) sd = add(sd, y[j]);
+        }
+        uint32_t r = __shfl_sync(FULL, id, (int)l);
+        if (r != NIL) {  // a list longer than 4: the rest of it, walked here in order (rare)
+          const double td = __shfl_sync(FULL, e.td, (int)l);
+          for (uint32_t hop = 0; r != NIL && hop < P.max_requests; ++hop) {
+            const Node nd = node[r];
+            const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
+            if (lane == dl) sd = add(sd, itl);
+            const bool ok = itl <= slo;
+            if (lane == 0) { c_ok += ok; c_both += ok && nd.tf > 0.0; }
+            r = nd.next;
+          }
+        }
+      }
+    }
+    c_ok = __reduce_add_sync(FULL, c_ok);
+    c_both = __reduce_add_sync(FULL, c_both);
+    const int ND = P.lay[P.layout_id[s]].n_d;
+    double sitl = 0.0;  // decode instances in instance order (A37)
+    for (int d = 0; d < ND; ++d) sitl = add(sitl, __shfl_sync(FULL, sd, d));
+    if (lane == 0) {
+      R->n_itl_ok += c_ok;
+      R->n_both_ok += c_both;
+      R->sum_itl_mean_ms = sitl;
+    }
+  }
+}
+
+cudaError_t launch_itl(const SimParams &P, cudaStream_t st) {
+  int grid = (int)((P.n + 3u) / 4u);
+  grid = grid < 1 ? 1 : grid;
+  itl_kernel<<<grid, 128, 0, st>>>(P);
   return cudaGetLastError();
 }
 

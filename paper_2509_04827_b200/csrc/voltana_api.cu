@@ -258,11 +258,16 @@ uint32_t wheel_buckets(uint32_t max_out) {
   return nb;
 }
 
+size_t tr_stride_clog(const voltana_traces *tr) {
+  return (size_t)tr->max_requests + 2 * VOLTANA_MAX_INSTANCES * CLOG_CHUNK;
+}
+
 struct SimLayout {
   size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
   uint32_t n_slots, nb, itl_smem, sw_off, ring_r = 0, ring_nd = 0;
   size_t ring_e_off = 0, ring_c_off = 0;
   size_t nodes_off = 0, pares_off = 0, rtab_off = 0;  // VT_SPLIT_A
+  size_t clog_off = 0, clog_n_off = 0;                 // VT_DEFER_ITL
 };
 
 int resident_warps(size_t smem_per_block) {
@@ -334,6 +339,14 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.total = L.pares_off + align256((size_t)(n < 1 ? 1 : n) * VOLTANA_MAX_INSTANCES * sizeof(PaRes));
   L.rtab_off = L.total;
   L.total = L.rtab_off + (size_t)MAX_GRIDS * MAX_PROFILES * RT_STRIDE * sizeof(double);
+#if VT_DEFER_ITL
+  // completion log: at most one entry per routed request of the scenario
+  L.clog_off = align256(L.total);
+  L.total = L.clog_off + align256((size_t)(n < 1 ? 1 : n) * (tr->max_requests + 2 * VOLTANA_MAX_INSTANCES * CLOG_CHUNK) *
+                                   sizeof(CEnt));
+  L.clog_n_off = L.total;
+  L.total = L.clog_n_off + align256((size_t)(n < 1 ? 1 : n) * sizeof(uint32_t));
+#endif
 #endif
   return L;
 }
@@ -480,6 +493,11 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->nodes = ws + L.nodes_off;
   P->pares = (PaRes *)(ws + L.pares_off);
   P->rtab = (double *)(ws + L.rtab_off);
+#if VT_DEFER_ITL
+  P->clog = (CEnt *)(ws + L.clog_off);
+  P->clog_n = (uint32_t *)(ws + L.clog_n_off);
+  P->clog_stride = tr_stride_clog(traces_h);
+#endif
   P->np_max = 1;
   for (int i = 0; i < n_layouts; ++i) P->np_max = (uint32_t)layouts_h[i].n_p > P->np_max ? layouts_h[i].n_p : P->np_max;
 #ifdef VT_PA_SPREAD
@@ -523,9 +541,17 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate split event"); }
   }
   e = launch_sim(*P, v, fast, grid, L.smem, st);
+  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate launch"); }
+  int k4c = 0;
+#if VT_SPLIT_A && VT_DEFER_ITL
+  if (!(v & 2)) {  // K4c: the decode ITL accounting the paper's-policy kernels deferred
+    e = launch_itl(*P, st);
+    k4c = 1;
+  }
+#endif
   delete P;
-  if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
-  g_launches = 1 + ((VT_UTAB || VT_SPLIT_A) ? 1 : 0) + (VT_SPLIT_A ? 1 : 0);
+  if (e != cudaSuccess) return cuda_fail(e, "simulate itl launch");
+  g_launches = 1 + ((VT_UTAB || VT_SPLIT_A) ? 1 : 0) + (VT_SPLIT_A ? 1 : 0) + k4c;
   return ok();
 }
 

@@ -57,6 +57,16 @@ struct PaRes {     // phase-A result of one prefill instance (K4a -> K4b; the re
   uint32_t iters, ttft_ok, itl_ok, both, errc, ndec, head, pad;  // head: first routed request (NIL none)
 };
 
+#ifndef VT_DEFER_ITL
+#define VT_DEFER_ITL 1  // paper's-policy kernels: per-request ITL accounting in a post-pass (K4c)
+#endif
+constexpr uint32_t CLOG_CHUNK = 32;  // completion-log slots handed to a decode lane at a time
+struct CEnt {      // K4b -> K4c: one decode iteration end with completions (16 B)
+  double td;       // the iteration's end time
+  uint32_t head;   // first request of its completion list (admission order, linked by node.next)
+  uint32_t d;      // decode instance
+};
+
 struct SimParams {
   // traces (device)
   const double *arrival;
@@ -93,6 +103,9 @@ struct SimParams {
   PaRes *pares;                // VT_SPLIT_A: [n][VOLTANA_MAX_INSTANCES] phase-A results
   double *rtab;                // VT_SPLIT_A: [MAX_GRIDS][MAX_PROFILES][RT_STRIDE] ladder-resolved prefill tables
   uint32_t np_max;             // VT_SPLIT_A: max N_P over the launch's layouts (K4a threads per scenario)
+  CEnt *clog;                  // VT_DEFER_ITL: [n][max_requests] completion log per scenario (log order)
+  uint32_t *clog_n;            // VT_DEFER_ITL: [n] log slots used by each scenario (empty ones: head NIL)
+  size_t clog_stride;          // VT_DEFER_ITL: log slots per scenario (max_requests + 2 * 8 * CLOG_CHUNK)
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];
@@ -107,5 +120,6 @@ const void *sim_kernel_ptr(int v, bool fast);
 cudaError_t launch_sim(const SimParams &P, int v, bool fast, int grid, size_t smem, cudaStream_t st);
 cudaError_t launch_utab(const SimParams &P, cudaStream_t st);  // VT_UTAB: fill P.utab
 cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st);  // K4a (VT_SPLIT_A)
+cudaError_t launch_itl(const SimParams &P, cudaStream_t st);  // K4c (VT_DEFER_ITL)
 
 }  // namespace vt

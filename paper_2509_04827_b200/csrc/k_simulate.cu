@@ -1792,8 +1792,17 @@ cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st
 // then the values are added to their instance's running sum one by one in log order, so each
 // instance's sum is the oracle's sequential sum in completion order (A37); the counts are
 // order-free. The record's decode ITL fields are completed here (K4b wrote the prefill part).
+constexpr int ITL_U = 2;  // K4c: log entries gathered per lane per round (independent walks in flight)
+__device__ __forceinline__ double itl_marker(uint32_t slot) {  // "list continues": NaN with the slot
+  return __longlong_as_double((long long)(0xFFF8000000000000ull | slot));
+}
 __global__ void __launch_bounds__(128) itl_kernel(const __grid_constant__ SimParams P) {
-  const uint32_t lane = threadIdx.x & 31u;
+  constexpr uint32_t RN = 32u * ITL_U;  // entries per round
+  __shared__ double s_v[4][RN][4];      // per warp: gathered ITL values (<= 4 per entry)
+  __shared__ double s_seq[4][RN * 5];   // the round's values regrouped: instance by instance, log order
+  __shared__ double s_td[4][RN];
+  __shared__ uint32_t s_id[4][RN];      // where a list longer than 4 continues
+  const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < P.n; s += nw) {
     voltana_result *R = P.out + s;
@@ -1802,56 +1811,108 @@ __global__ void __launch_bounds__(128) itl_kernel(const __grid_constant__ SimPar
     const CEnt *E = P.clog + (size_t)s * P.clog_stride;
     const Node *node = (const Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node));
     const double slo = P.slo[P.slo_id[s]].itl_ms;
+    const int ND = P.lay[P.layout_id[s]].n_d;
     double sd = 0.0;                // lane d: instance d's running sum
     uint32_t c_ok = 0, c_both = 0;  // this lane's counts
-    for (uint32_t c0 = 0; c0 < m; c0 += 32u) {
-      const bool v = c0 + lane < m;
-      CEnt e;
-      e.td = 0.0; e.head = NIL; e.d = 0u;
-      if (v) e = E[c0 + lane];
-      double x[4];
-      uint32_t cnt = 0, id = e.head;
+    for (uint32_t c0 = 0; c0 < m; c0 += RN) {
+      double td[ITL_U];
+      uint32_t id[ITL_U], cnt[ITL_U], dd[ITL_U];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        x[j] = 0.0;
-        if (id != NIL) {
-          const Node nd = node[id];
-          x[j] = div(sub(e.td, fabs(nd.tf)), (double)(nd.out - 1u));
-          const bool ok = x[j] <= slo;
-          c_ok += ok;
-          c_both += ok && nd.tf > 0.0;
-          cnt++;
-          id = nd.next;
-        }
+      for (int u = 0; u < ITL_U; ++u) {
+        const uint32_t q = c0 + (uint32_t)u * 32u + lane;
+        CEnt e;
+        e.td = 0.0; e.head = NIL; e.d = 0u;
+        if (q < m) e = E[q];
+        td[u] = e.td; id[u] = e.head; dd[u] = e.d; cnt[u] = 0u;
       }
-      const uint32_t nv = m - c0 < 32u ? m - c0 : 32u;
-      for (uint32_t l = 0; l < nv; ++l) {  // log order
-        const uint32_t dl = __shfl_sync(FULL, e.d, (int)l), cl = __shfl_sync(FULL, cnt, (int)l);
-        double y[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) y[j] = __shfl_sync(FULL, x[j], (int)l);
-        if (lane == dl) {
+      for (int jj = 0; jj < 4; ++jj) {  // step jj of every walk: ITL_U independent loads in flight
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if ((uint32_t)j < cl) sd = add(sd, y[j]);
-        }
-        uint32_t r = __shfl_sync(FULL, id, (int)l);
-        if (r != NIL) {  // a list longer than 4: the rest of it, walked here in order (rare)
-          const double td = __shfl_sync(FULL, e.td, (int)l);
-          for (uint32_t hop = 0; r != NIL && hop < P.max_requests; ++hop) {
-            const Node nd = node[r];
-            const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
-            if (lane == dl) sd = add(sd, itl);
-            const bool ok = itl <= slo;
-            if (lane == 0) { c_ok += ok; c_both += ok && nd.tf > 0.0; }
-            r = nd.next;
+        for (int u = 0; u < ITL_U; ++u) {
+          if (id[u] != NIL) {
+            const Node nd = node[id[u]];
+            const double x = div(sub(td[u], fabs(nd.tf)), (double)(nd.out - 1u));
+            const bool ok = x <= slo;
+            c_ok += ok;
+            c_both += ok && nd.tf > 0.0;
+            s_v[wib][u * 32 + lane][jj] = x;
+            cnt[u]++;
+            id[u] = nd.next;
           }
         }
       }
+      // regroup: the values of instance d, in log order, go to s_seq[base_d ...] (exclusive scans)
+      uint32_t pos[ITL_U], tot[NI];
+#pragma unroll
+      for (int d = 0; d < NI; ++d) tot[d] = 0u;
+#pragma unroll
+      for (int u = 0; u < ITL_U; ++u) {
+        const uint32_t cp = cnt[u] + (id[u] != NIL ? 1u : 0u);  // values + a continuation marker
+        pos[u] = 0u;
+#pragma unroll
+        for (int d = 0; d < NI; ++d) {
+          if (d >= ND) break;
+          const uint32_t c = dd[u] == (uint32_t)d ? cp : 0u;
+          uint32_t incl = c;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+          }
+          if (dd[u] == (uint32_t)d) pos[u] = tot[d] + incl - c;
+          tot[d] += __shfl_sync(FULL, incl, 31);
+        }
+      }
+      uint32_t base = 0u, my_base = 0u, my_tot = 0u;  // lane d: its sequence [my_base, my_base + my_tot)
+#pragma unroll
+      for (int d = 0; d < NI; ++d) {
+        if (d >= ND) break;
+        if (lane == (uint32_t)d) { my_base = base; my_tot = tot[d]; }
+        base += tot[d];
+      }
+#pragma unroll
+      for (int u = 0; u < ITL_U; ++u) {
+        uint32_t b = 0u;
+#pragma unroll
+        for (int d = 0; d < NI; ++d) {
+          if (d >= ND) break;
+          const uint32_t bd = __shfl_sync(FULL, my_base, d);
+          if (dd[u] == (uint32_t)d) b = bd;
+        }
+        double *o = &s_seq[wib][b + pos[u]];
+        for (uint32_t jj = 0; jj < cnt[u]; ++jj) o[jj] = s_v[wib][u * 32 + lane][jj];
+        if (id[u] != NIL) {
+          o[cnt[u]] = itl_marker((uint32_t)u * 32u + lane);
+          s_td[wib][u * 32 + lane] = td[u];
+          s_id[wib][u * 32 + lane] = id[u];
+        }
+      }
+      __syncwarp();
+      if (lane < (uint32_t)ND) {  // instance `lane` adds its values in log order (A37)
+        for (uint32_t q = 0; q < my_tot; ++q) {
+          const double v = s_seq[wib][my_base + q];
+          if (v == v) {
+            sd = add(sd, v);
+          } else {  // a list longer than 4: its rest, in order (rare)
+            const uint32_t slot = (uint32_t)(__double_as_longlong(v) & 0xFFFFu);
+            const double t = s_td[wib][slot];
+            uint32_t r = s_id[wib][slot];
+            for (uint32_t hop = 0; r != NIL && hop < P.max_requests; ++hop) {
+              const Node nd = node[r];
+              const double itl = div(sub(t, fabs(nd.tf)), (double)(nd.out - 1u));
+              sd = add(sd, itl);
+              const bool ok = itl <= slo;
+              c_ok += ok;
+              c_both += ok && nd.tf > 0.0;
+              r = nd.next;
+            }
+          }
+        }
+      }
+      __syncwarp();
     }
     c_ok = __reduce_add_sync(FULL, c_ok);
     c_both = __reduce_add_sync(FULL, c_both);
-    const int ND = P.lay[P.layout_id[s]].n_d;
     double sitl = 0.0;  // decode instances in instance order (A37)
     for (int d = 0; d < ND; ++d) sitl = add(sitl, __shfl_sync(FULL, sd, d));
     if (lane == 0) {

@@ -1168,6 +1168,124 @@ __device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double
   if ((V & 2) && W.it_on && lane == 0) P.o.iter_count[W.it_base / P.o.iter_cap + p] = S.iters;
 }
 
+// ------------------------------------------------------------------ deferred ITL accounting (K4c)
+__device__ __forceinline__ double itl_marker(uint32_t slot) {  // "list continues": NaN with the slot
+  return __longlong_as_double((long long)(0xFFF8000000000000ull | slot));
+}
+// The ITL accounting of one scenario's completion log E[0, m) on the calling warp (all 32
+// lanes): c_ok / c_both summed over the warp, sitl = the decode instances' sums in instance
+// order, each the sequential sum in completion order (A30, A37).
+template <int U>
+__device__ void itl_scenario(const SimParams &P, uint32_t m, int ND, double slo, const CEnt *E, const Node *node,
+                             ItlScratch<U> &S, uint32_t &c_ok_out, uint32_t &c_both_out, double &sitl_out) {
+  constexpr uint32_t RN = 32u * U;  // entries per round
+  const uint32_t lane = threadIdx.x & 31u;
+  double sd = 0.0;                // lane d: instance d's running sum
+  uint32_t c_ok = 0, c_both = 0;  // this lane's counts
+  for (uint32_t c0 = 0; c0 < m; c0 += RN) {
+    double td[U];
+    uint32_t id[U], cnt[U], dd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t q = c0 + (uint32_t)u * 32u + lane;
+      CEnt e;
+      e.td = 0.0; e.head = NIL; e.d = 0u;
+      if (q < m) e = E[q];
+      td[u] = e.td; id[u] = e.head; dd[u] = e.d; cnt[u] = 0u;
+    }
+#pragma unroll
+    for (uint32_t jj = 0; jj < ITL_CAP; ++jj) {  // step jj of every walk: U independent loads in flight
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (id[u] != NIL) {
+          const Node nd = node[id[u]];
+          const double x = div(sub(td[u], fabs(nd.tf)), (double)(nd.out - 1u));
+          const bool ok = x <= slo;
+          c_ok += ok;
+          c_both += ok && nd.tf > 0.0;
+          S.v[u * 32 + lane][jj] = x;
+          cnt[u]++;
+          id[u] = nd.next;
+        }
+      }
+    }
+    // regroup: the values of instance d, in log order, go to seq[base_d ...] (exclusive scans)
+    uint32_t pos[U], tot[NI];
+#pragma unroll
+    for (int d = 0; d < NI; ++d) tot[d] = 0u;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint32_t cp = cnt[u] + (id[u] != NIL ? 1u : 0u);  // values + a continuation marker
+      pos[u] = 0u;
+#pragma unroll
+      for (int d = 0; d < NI; ++d) {
+        if (d >= ND) break;
+        const uint32_t c = dd[u] == (uint32_t)d ? cp : 0u;
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= (uint32_t)o) incl += y;
+        }
+        if (dd[u] == (uint32_t)d) pos[u] = tot[d] + incl - c;
+        tot[d] += __shfl_sync(FULL, incl, 31);
+      }
+    }
+    uint32_t base = 0u, my_base = 0u, my_tot = 0u;  // lane d: its sequence [my_base, my_base + my_tot)
+#pragma unroll
+    for (int d = 0; d < NI; ++d) {
+      if (d >= ND) break;
+      if (lane == (uint32_t)d) { my_base = base; my_tot = tot[d]; }
+      base += tot[d];
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      uint32_t b = 0u;
+#pragma unroll
+      for (int d = 0; d < NI; ++d) {
+        if (d >= ND) break;
+        const uint32_t bd = __shfl_sync(FULL, my_base, d);
+        if (dd[u] == (uint32_t)d) b = bd;
+      }
+      double *o = &S.seq[b + pos[u]];
+      for (uint32_t jj = 0; jj < cnt[u]; ++jj) o[jj] = S.v[u * 32 + lane][jj];
+      if (id[u] != NIL) {
+        o[cnt[u]] = itl_marker((uint32_t)u * 32u + lane);
+        S.td[u * 32 + lane] = td[u];
+        S.id[u * 32 + lane] = id[u];
+      }
+    }
+    __syncwarp();
+    if (lane < (uint32_t)ND) {  // instance `lane` adds its values in log order (A37)
+      for (uint32_t q = 0; q < my_tot; ++q) {
+        const double v = S.seq[my_base + q];
+        if (v == v) {
+          sd = add(sd, v);
+        } else {  // a list longer than ITL_CAP: its rest, in order
+          const uint32_t slot = (uint32_t)(__double_as_longlong(v) & 0xFFFFu);
+          const double t = S.td[slot];
+          uint32_t r = S.id[slot];
+          for (uint32_t hop = 0; r != NIL && hop < P.max_requests; ++hop) {
+            const Node nd = node[r];
+            const double itl = div(sub(t, fabs(nd.tf)), (double)(nd.out - 1u));
+            sd = add(sd, itl);
+            const bool ok = itl <= slo;
+            c_ok += ok;
+            c_both += ok && nd.tf > 0.0;
+            r = nd.next;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  c_ok_out = __reduce_add_sync(FULL, c_ok);
+  c_both_out = __reduce_add_sync(FULL, c_both);
+  double sitl = 0.0;  // decode instances in instance order (A37)
+  for (int d = 0; d < ND; ++d) sitl = add(sitl, __shfl_sync(FULL, sd, d));
+  sitl_out = sitl;
+}
+
 template <int V, bool F, class WS>
 __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *wheels, WS &W, uint32_t sid) {
   const int lane = glane();
@@ -1531,11 +1649,19 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   dec_advance_all<V, F>(D, lane, L, W, INF, dE, P.o);
   if (lane < ND && !D.dead) itl_drain<V, F>(D, L, W, lane, P.o);
 #if VT_DEFER_ITL
+  uint32_t k_ok = 0u, k_both = 0u;  // the decode ITL accounting of the completion log (in-warp K4c)
+  double k_sitl = 0.0;
   if (!(V & 2)) {
     if (lane < ND)  // the unused rest of this lane's chunk: empty entries
       for (uint32_t q = D.lpos; q < D.lend; ++q) { CEnt ce; ce.td = 0.0; ce.head = NIL; ce.d = 0u; L.clog[q] = ce; }
     __syncwarp(gmask());
+#if VT_ITL_INWARP
+    // the scenario's log and nodes are still warm in L2: all 32 lanes gather, then sum in order
+    itl_scenario<ITL_UW>(P, W.clog_m, ND, W.slo_itl, L.clog, node, *(ItlScratch<ITL_UW> *)((char *)&W + P.ks_off), k_ok,
+                    k_both, k_sitl);
+#else
     if (lane == 0) P.clog_n[s] = W.clog_m;
+#endif
   }
 #endif
   if ((V & 2) && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
@@ -1584,8 +1710,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       bd = add(bd, b);
     }
   }
-  const uint32_t c_itl = __reduce_add_sync(gmask(), lane < ND ? LACC(n_itl_ok) : 0u);
-  const uint32_t c_both = __reduce_add_sync(gmask(), lane < ND ? LACC(n_both) : 0u);
+  uint32_t c_itl = __reduce_add_sync(gmask(), lane < ND ? LACC(n_itl_ok) : 0u);
+  uint32_t c_both = __reduce_add_sync(gmask(), lane < ND ? LACC(n_both) : 0u);
+#if VT_DEFER_ITL && VT_ITL_INWARP
+  if (!(V & 2)) { c_itl += k_ok; c_both += k_both; sitl = k_sitl; }
+#endif
   const uint32_t c_di = __reduce_add_sync(gmask(), lane < ND ? D.iters : 0u);
   if (lane == 0) {
     voltana_result R = voltana_result{};
@@ -1792,129 +1921,21 @@ cudaError_t launch_prefill(const SimParams &P, int v, bool fast, cudaStream_t st
 // then the values are added to their instance's running sum one by one in log order, so each
 // instance's sum is the oracle's sequential sum in completion order (A37); the counts are
 // order-free. The record's decode ITL fields are completed here (K4b wrote the prefill part).
-constexpr int ITL_U = 2;  // K4c: log entries gathered per lane per round (independent walks in flight)
-__device__ __forceinline__ double itl_marker(uint32_t slot) {  // "list continues": NaN with the slot
-  return __longlong_as_double((long long)(0xFFF8000000000000ull | slot));
-}
+// K4c as its own launch (VT_ITL_INWARP = 0): one warp per scenario after K4b.
+constexpr int ITL_U = 2;
 __global__ void __launch_bounds__(128) itl_kernel(const __grid_constant__ SimParams P) {
-  constexpr uint32_t RN = 32u * ITL_U;  // entries per round
-  __shared__ double s_v[4][RN][4];      // per warp: gathered ITL values (<= 4 per entry)
-  __shared__ double s_seq[4][RN * 5];   // the round's values regrouped: instance by instance, log order
-  __shared__ double s_td[4][RN];
-  __shared__ uint32_t s_id[4][RN];      // where a list longer than 4 continues
+  __shared__ ItlScratch<ITL_U> scr[4];
   const uint32_t lane = threadIdx.x & 31u, wib = threadIdx.x >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < P.n; s += nw) {
     voltana_result *R = P.out + s;
     if (R->status != 0u) continue;
-    const uint32_t m = P.clog_n[s];
-    const CEnt *E = P.clog + (size_t)s * P.clog_stride;
-    const Node *node = (const Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node));
-    const double slo = P.slo[P.slo_id[s]].itl_ms;
-    const int ND = P.lay[P.layout_id[s]].n_d;
-    double sd = 0.0;                // lane d: instance d's running sum
-    uint32_t c_ok = 0, c_both = 0;  // this lane's counts
-    for (uint32_t c0 = 0; c0 < m; c0 += RN) {
-      double td[ITL_U];
-      uint32_t id[ITL_U], cnt[ITL_U], dd[ITL_U];
-#pragma unroll
-      for (int u = 0; u < ITL_U; ++u) {
-        const uint32_t q = c0 + (uint32_t)u * 32u + lane;
-        CEnt e;
-        e.td = 0.0; e.head = NIL; e.d = 0u;
-        if (q < m) e = E[q];
-        td[u] = e.td; id[u] = e.head; dd[u] = e.d; cnt[u] = 0u;
-      }
-#pragma unroll
-      for (int jj = 0; jj < 4; ++jj) {  // step jj of every walk: ITL_U independent loads in flight
-#pragma unroll
-        for (int u = 0; u < ITL_U; ++u) {
-          if (id[u] != NIL) {
-            const Node nd = node[id[u]];
-            const double x = div(sub(td[u], fabs(nd.tf)), (double)(nd.out - 1u));
-            const bool ok = x <= slo;
-            c_ok += ok;
-            c_both += ok && nd.tf > 0.0;
-            s_v[wib][u * 32 + lane][jj] = x;
-            cnt[u]++;
-            id[u] = nd.next;
-          }
-        }
-      }
-      // regroup: the values of instance d, in log order, go to s_seq[base_d ...] (exclusive scans)
-      uint32_t pos[ITL_U], tot[NI];
-#pragma unroll
-      for (int d = 0; d < NI; ++d) tot[d] = 0u;
-#pragma unroll
-      for (int u = 0; u < ITL_U; ++u) {
-        const uint32_t cp = cnt[u] + (id[u] != NIL ? 1u : 0u);  // values + a continuation marker
-        pos[u] = 0u;
-#pragma unroll
-        for (int d = 0; d < NI; ++d) {
-          if (d >= ND) break;
-          const uint32_t c = dd[u] == (uint32_t)d ? cp : 0u;
-          uint32_t incl = c;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= (uint32_t)o) incl += y;
-          }
-          if (dd[u] == (uint32_t)d) pos[u] = tot[d] + incl - c;
-          tot[d] += __shfl_sync(FULL, incl, 31);
-        }
-      }
-      uint32_t base = 0u, my_base = 0u, my_tot = 0u;  // lane d: its sequence [my_base, my_base + my_tot)
-#pragma unroll
-      for (int d = 0; d < NI; ++d) {
-        if (d >= ND) break;
-        if (lane == (uint32_t)d) { my_base = base; my_tot = tot[d]; }
-        base += tot[d];
-      }
-#pragma unroll
-      for (int u = 0; u < ITL_U; ++u) {
-        uint32_t b = 0u;
-#pragma unroll
-        for (int d = 0; d < NI; ++d) {
-          if (d >= ND) break;
-          const uint32_t bd = __shfl_sync(FULL, my_base, d);
-          if (dd[u] == (uint32_t)d) b = bd;
-        }
-        double *o = &s_seq[wib][b + pos[u]];
-        for (uint32_t jj = 0; jj < cnt[u]; ++jj) o[jj] = s_v[wib][u * 32 + lane][jj];
-        if (id[u] != NIL) {
-          o[cnt[u]] = itl_marker((uint32_t)u * 32u + lane);
-          s_td[wib][u * 32 + lane] = td[u];
-          s_id[wib][u * 32 + lane] = id[u];
-        }
-      }
-      __syncwarp();
-      if (lane < (uint32_t)ND) {  // instance `lane` adds its values in log order (A37)
-        for (uint32_t q = 0; q < my_tot; ++q) {
-          const double v = s_seq[wib][my_base + q];
-          if (v == v) {
-            sd = add(sd, v);
-          } else {  // a list longer than 4: its rest, in order (rare)
-            const uint32_t slot = (uint32_t)(__double_as_longlong(v) & 0xFFFFu);
-            const double t = s_td[wib][slot];
-            uint32_t r = s_id[wib][slot];
-            for (uint32_t hop = 0; r != NIL && hop < P.max_requests; ++hop) {
-              const Node nd = node[r];
-              const double itl = div(sub(t, fabs(nd.tf)), (double)(nd.out - 1u));
-              sd = add(sd, itl);
-              const bool ok = itl <= slo;
-              c_ok += ok;
-              c_both += ok && nd.tf > 0.0;
-              r = nd.next;
-            }
-          }
-        }
-      }
-      __syncwarp();
-    }
-    c_ok = __reduce_add_sync(FULL, c_ok);
-    c_both = __reduce_add_sync(FULL, c_both);
-    double sitl = 0.0;  // decode instances in instance order (A37)
-    for (int d = 0; d < ND; ++d) sitl = add(sitl, __shfl_sync(FULL, sd, d));
+    uint32_t c_ok, c_both;
+    double sitl;
+    itl_scenario<ITL_U>(P, P.clog_n[s], P.lay[P.layout_id[s]].n_d, P.slo[P.slo_id[s]].itl_ms,
+                        P.clog + (size_t)s * P.clog_stride,
+                        (const Node *)(P.nodes + (size_t)s * P.max_requests * sizeof(Node)), scr[wib], c_ok, c_both,
+                        sitl);
     if (lane == 0) {
       R->n_itl_ok += c_ok;
       R->n_both_ok += c_both;

@@ -264,7 +264,7 @@ size_t tr_stride_clog(const voltana_traces *tr) {
 
 struct SimLayout {
   size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
-  uint32_t n_slots, nb, itl_smem, sw_off, ring_r = 0, ring_nd = 0;
+  uint32_t n_slots, nb, itl_smem, sw_off, ring_r = 0, ring_nd = 0, ks_off = 0;
   size_t ring_e_off = 0, ring_c_off = 0;
   size_t nodes_off = 0, pares_off = 0, rtab_off = 0;  // VT_SPLIT_A
   size_t clog_off = 0, clog_n_off = 0;                 // VT_DEFER_ITL
@@ -301,6 +301,10 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
   L.smem_per_warp = (sim_smem_fixed(fast) + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
   L.sw_off = (uint32_t)L.smem_per_warp;
+#if VT_SPLIT_A && VT_DEFER_ITL && VT_ITL_INWARP
+  L.ks_off = (uint32_t)L.smem_per_warp;  // in-warp ITL pass scratch
+  L.smem_per_warp += ITL_SCRATCH;
+#endif
 #ifdef VT_SWHEEL
   L.smem_per_warp += (size_t)max_nd(lays, n_layouts) * VT_SWHEEL * 16;
 #endif
@@ -497,6 +501,7 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->clog = (CEnt *)(ws + L.clog_off);
   P->clog_n = (uint32_t *)(ws + L.clog_n_off);
   P->clog_stride = tr_stride_clog(traces_h);
+  P->ks_off = L.ks_off;
 #endif
   P->np_max = 1;
   for (int i = 0; i < n_layouts; ++i) P->np_max = (uint32_t)layouts_h[i].n_p > P->np_max ? layouts_h[i].n_p : P->np_max;
@@ -543,7 +548,7 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   e = launch_sim(*P, v, fast, grid, L.smem, st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate launch"); }
   int k4c = 0;
-#if VT_SPLIT_A && VT_DEFER_ITL
+#if VT_SPLIT_A && VT_DEFER_ITL && !VT_ITL_INWARP
   if (!(v & 2)) {  // K4c: the decode ITL accounting the paper's-policy kernels deferred
     e = launch_itl(*P, st);
     k4c = 1;

@@ -58,8 +58,26 @@ struct PaRes {     // phase-A result of one prefill instance (K4a -> K4b; the re
 };
 
 #ifndef VT_DEFER_ITL
-#define VT_DEFER_ITL 1  // paper's-policy kernels: per-request ITL accounting in a post-pass (K4c)
+#define VT_DEFER_ITL VT_SPLIT_A  // paper's-policy kernels: per-request ITL accounting deferred (K4c; needs the split)
 #endif
+#ifndef VT_ITL_INWARP
+#define VT_ITL_INWARP 1  // the deferred ITL pass runs in K4b's warp right after its scenario (else K4c launch)
+#endif
+#ifndef VT_ITL_CAP
+#define VT_ITL_CAP 4     // ITL pass: values of one list gathered by its lane (the rest: walked in order)
+#endif
+#ifndef VT_ITL_UW
+#define VT_ITL_UW 1      // in-warp ITL pass: log entries per lane per round
+#endif
+constexpr uint32_t ITL_CAP = VT_ITL_CAP;
+constexpr int ITL_UW = VT_ITL_UW;
+template <int U> struct ItlScratch {  // per-warp scratch of the ITL pass (shared memory)
+  double v[32 * U][ITL_CAP];          // gathered values of a round's entries
+  double seq[32 * U * (ITL_CAP + 1)]; // the round's values regrouped instance by instance, log order
+  double td[32 * U];
+  uint32_t id[32 * U];                // where a list longer than ITL_CAP continues
+};
+constexpr uint32_t ITL_SCRATCH = (uint32_t)((sizeof(ItlScratch<ITL_UW>) + 15) & ~(size_t)15);
 constexpr uint32_t CLOG_CHUNK = 32;  // completion-log slots handed to a decode lane at a time
 struct CEnt {      // K4b -> K4c: one decode iteration end with completions (16 B)
   double td;       // the iteration's end time
@@ -106,6 +124,7 @@ struct SimParams {
   CEnt *clog;                  // VT_DEFER_ITL: [n][max_requests] completion log per scenario (log order)
   uint32_t *clog_n;            // VT_DEFER_ITL: [n] log slots used by each scenario (empty ones: head NIL)
   size_t clog_stride;          // VT_DEFER_ITL: log slots per scenario (max_requests + 2 * 8 * CLOG_CHUNK)
+  uint32_t ks_off;             // VT_ITL_INWARP: byte offset of the ITL scratch in the per-warp block
   // host tables copied into the kernel parameter bank
   voltana_slo slo[MAX_SLOS];
   voltana_layout lay[MAX_LAYOUTS];

@@ -154,6 +154,12 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level,
  * profiles[n_profiles] (<= 8). Device: traces, scenario table, out[n] records.
  * Scenarios are claimed in array order by persistent warps: put expensive scenarios
  * first for load balance (the Python layer does LPT ordering).
+ * Enqueues three kernels on `stream`: a setup launch (utilisation and ladder tables), the
+ * prefill timelines of every scenario (K4a, one warp per prefill instance), then routing +
+ * decode (K4b, one warp per scenario; the per-request ITL accounting runs in the same warp
+ * after each scenario for the paper's-policy kernels).
+ * Workspace (voltana_simulate_workspace_bytes) grows as n x max_requests x 32 B: per scenario
+ * a 16-B node per request (K4a -> K4b) and a 16-B completion-log slot per request.
  * Errors: INVALID_ARG, LADDER, COVERAGE, CONFIG, WORKSPACE, CUDA. Per-scenario problems
  * go to out[i].status (then only status and n_requests are set).                        */
 typedef struct {

@@ -1815,6 +1815,27 @@ struct PCtx {
   uint32_t B, K, W, kp, ptiles, pcut, mono_tt, ctrl, wo, noise_mask, rq_on, it_on;
   uint64_t seed, rq_base, it_base;
 };
+// The same context in shared memory, one per lane group (VT_PA_SMEM): the fields are uniform
+// over the group, so they cost no registers, and the ladder rows are read with LDS.
+struct PCtxS {
+  double tgt_ttft, slo_ttft, p_idle, tdp, uh_p, uh_d, ctrl_iv, fs_ov;
+  const double *a1g, *c1g, *ut, *noise;
+  const uint16_t *lad;
+  uint32_t B, K, W, kp, ptiles, pcut, mono_tt, ctrl, wo, noise_mask, rq_on, it_on;
+  uint64_t seed, rq_base, it_base;
+  double tt[2 * VOLTANA_MAX_LEVELS];  // [K][a1, c1]
+  double dyn[VOLTANA_MAX_LEVELS];     // prefill DYN
+};
+__device__ __forceinline__ void pctx_scalars(PCtxS &S, const PCtx &C) {
+  S.tgt_ttft = C.tgt_ttft; S.slo_ttft = C.slo_ttft; S.p_idle = C.p_idle; S.tdp = C.tdp; S.uh_p = C.uh_p;
+  S.uh_d = C.uh_d; S.ctrl_iv = C.ctrl_iv; S.fs_ov = C.fs_ov; S.a1g = C.a1g; S.c1g = C.c1g; S.ut = C.ut;
+  S.noise = C.noise; S.lad = C.lad; S.B = C.B; S.K = C.K; S.W = C.W; S.kp = C.kp; S.ptiles = C.ptiles;
+  S.pcut = C.pcut; S.mono_tt = C.mono_tt; S.ctrl = C.ctrl; S.wo = C.wo; S.noise_mask = C.noise_mask;
+  S.rq_on = C.rq_on; S.it_on = C.it_on; S.seed = C.seed; S.rq_base = C.rq_base; S.it_base = C.it_base;
+}
+#ifndef VT_PA_SMEM
+#define VT_PA_SMEM 1
+#endif
 
 template <int V, bool F>
 __global__ void __launch_bounds__(PA_THREADS, PA_MIN_BLOCKS) prefill_kernel(const __grid_constant__ SimParams P) {
@@ -1874,8 +1895,24 @@ __global__ void __launch_bounds__(PA_THREADS, PA_MIN_BLOCKS) prefill_kernel(cons
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tq0));
 #endif
     if (PA_WARP) {
+#if VT_PA_SMEM
+      __shared__ PCtxS cs[PA_THREADS / PA_G];
+      PCtxS &S = cs[threadIdx.x / PA_G];
+      const Grp<PA_G> g;
+      if (g.gl == 0) pctx_scalars(S, C);
+      for (uint32_t k = g.gl; k < C.K; k += PA_G) {
+        S.tt[2 * k] = C.tt[2 * k];
+        S.tt[2 * k + 1] = C.tt[2 * k + 1];
+        S.dyn[k] = C.dyn[k];
+      }
+      __syncwarp(g.m);
+      prefill_warp<V, F, PA_G>(P, S, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p, NP,
+                               P.hash_seed[s], R);
+      __syncwarp(g.m);  // the next item of this group rewrites S
+#else
       prefill_warp<V, F, PA_G>(P, C, node, P.arrival + off, P.in_len + off, P.out_len + off, (uint32_t)N64, p, NP,
-                         P.hash_seed[s], R);
+                               P.hash_seed[s], R);
+#endif
       if ((threadIdx.x & (PA_G - 1)) == 0) P.pares[(size_t)s * NI + p] = R;
 #ifdef VT_PA_TIMING
       if (P.timing && (threadIdx.x & (PA_G - 1)) == 0) {  // experiment: [x][2] chain start, duration

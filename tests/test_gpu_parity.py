@@ -274,3 +274,25 @@ def test_simulate_deterministic_and_order_independent(vt, orc):
     wd.launch()
     b = wd.records()
     assert a.tobytes() == b.tobytes()
+
+
+def test_simulate_prefill_windows_and_completion_log(vt, orc):
+    """The split kernel's own paths: K4a's 32-request windows (batches that end inside a window,
+    batches re-windowed at their head, batches of more than 32 requests on the general path,
+    equal arrival times) and K4b's completion log (many completions per iteration: lists far
+    longer than the 4 values a lane gathers; more log chunks than one per lane; an instance that
+    gets nearly all the load)."""
+    p = synth.make_profile("L8")
+    lad5 = [0, 6, 13, 20, 27]
+    rng = np.random.default_rng(7)
+    # bursts of 1..90 simultaneous short requests: batches of every length around 32 and 64
+    sizes = rng.integers(1, 91, 120)
+    arr = np.repeat(np.cumsum(rng.uniform(50.0, 400.0, len(sizes))), sizes)
+    n = len(arr)
+    inl = rng.integers(1, 40, n)
+    outl = np.full(n, 60)                     # everything admitted together finishes together
+    outl[::17] = rng.integers(2, 400, len(outl[::17]))
+    for lay in (Layout(1, 1), Layout(2, 2), Layout(3, 2, max_batch_tokens=300), Layout(1, 2, policy=1)):
+        _one(vt, orc, arr, inl, outl, float(arr[-1]) + 1000.0, p, Slo(600, 60), lay, lad5)
+    # Delta = 0 with a 2-level ladder: EcoRoute keeps choosing one instance (skewed completion logs)
+    _one(vt, orc, arr, inl, outl, float(arr[-1]) + 1000.0, p, Slo(600, 60), Layout(1, 2, delta_mhz=0), [0, 27])

@@ -70,6 +70,12 @@
 #ifndef VT_PFA
 #define VT_PFA 0       // prefill lanes: prefetch the trace this many requests ahead (0 = off)
 #endif
+#ifndef VT_SCAN_ILP
+#define VT_SCAN_ILP 0  // K4b fast tables: all K evaluations issued together (heaviest alone -4 %, full sweep +24 %: off)
+#endif
+#ifndef VT_NODE_PF_L1
+#define VT_NODE_PF_L1 8  // K4b: L1 prefetch of the prefill stream this many request ids ahead
+#endif
 #ifndef VT_NODE_PF_L2
 #define VT_NODE_PF_L2 0  // K4b: bulk L2 prefetch of the node array this many requests ahead (1024/4096: no gain)
 #endif
@@ -203,11 +209,45 @@ __device__ __forceinline__ double ttft_at(const WS &W, int k, uint32_t nbt) {
 // Lowest ladder index whose prediction meets `target` (A1), else K-1 (A2);
 // *pred = the prediction there. Ascending scan with early exit, or an exact binary search
 // when the tables are coefficient-monotone in f (A32).
+// All KK levels evaluated independently (no early-exit chain: the evaluations overlap), then
+// the lowest feasible one selected from the top down — the same values as the ascending scan.
+template <int KK, class WS>
+__device__ __forceinline__ int lowest_itl_ilp(const WS &W, uint32_t j, double dn, double dkv, double target,
+                                              double *pred) {
+  double p[KK];
+#pragma unroll
+  for (int k = 0; k < KK; ++k) {
+    const double *r = W.it + 3 * ((size_t)j * KK + k);
+    p[k] = add(add(mul(r[0], dn), mul(r[1], dkv)), r[2]);
+  }
+  int kk = KK - 1;
+  double pp = p[KK - 1];
+#pragma unroll
+  for (int k = KK - 2; k >= 0; --k)
+    if (p[k] <= target) { kk = k; pp = p[k]; }
+  *pred = pp;
+  return kk;
+}
+
 template <bool F, class WS>
 __device__ int lowest_itl(const WS &W, uint32_t n, uint32_t kv, double target, double *pred) {
   const uint32_t j = tile_j<F>(W, n);
   const int K = (int)W.K;
   const double dn = (double)n, dkv = (double)kv;
+#if VT_SCAN_ILP
+  if (F) {
+    switch (K) {
+      case 1: return lowest_itl_ilp<1>(W, j, dn, dkv, target, pred);
+      case 2: return lowest_itl_ilp<2>(W, j, dn, dkv, target, pred);
+      case 3: return lowest_itl_ilp<3>(W, j, dn, dkv, target, pred);
+      case 4: return lowest_itl_ilp<4>(W, j, dn, dkv, target, pred);
+      case 5: return lowest_itl_ilp<5>(W, j, dn, dkv, target, pred);
+      case 6: return lowest_itl_ilp<6>(W, j, dn, dkv, target, pred);
+      case 7: return lowest_itl_ilp<7>(W, j, dn, dkv, target, pred);
+      default: return lowest_itl_ilp<8>(W, j, dn, dkv, target, pred);
+    }
+  }
+#endif
   if (!F && W.mono_it && K > 8) {
     int lo = 0, hi = K;
     while (lo < hi) {
@@ -1528,7 +1568,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       if (hd != NIL && hn.next != NIL) {
         nn = node[hn.next];
 #if VT_PF >= 1
-        prefetch_l1(node + hn.next + 8u);  // the stream's next line (ids advance by N_P)
+        prefetch_l1(node + hn.next + (uint32_t)VT_NODE_PF_L1);  // the stream's next line (ids advance by N_P)
 #endif
       }
 #if VT_SPLIT_A && VT_NODE_PF_L2

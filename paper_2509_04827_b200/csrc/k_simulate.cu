@@ -70,6 +70,10 @@
 #ifndef VT_PFA
 #define VT_PFA 0       // prefill lanes: prefetch the trace this many requests ahead (0 = off)
 #endif
+#ifndef VT_ADM_DEFER
+#define VT_ADM_DEFER 0  // K4b: wheel appends applied at the next START, line prefetched now (measured +5 %: off)
+#endif
+constexpr uint32_t ADM_PQ = 8;  // pending appends per decode lane (shared memory)
 #ifndef VT_SCAN_ILP
 #define VT_SCAN_ILP 0  // K4b fast tables: all K evaluations issued together (heaviest alone -4 %, full sweep +24 %: off)
 #endif
@@ -163,6 +167,9 @@ struct WarpSmemT {
   uint32_t *rc;                    //   ... and of cumulative counts of gaps above the ITL SLO
   uint32_t itlm, rmask;            //   layout itl_mode, ring_r - 1
   uint32_t clog_m;                 // VT_DEFER_ITL: log slots handed out (chunks of CLOG_CHUNK)
+#if VT_ADM_DEFER
+  uint32_t pq_i[NI][ADM_PQ], pq_fin[NI][ADM_PQ], pq_io[NI][ADM_PQ];  // decode lane: pending wheel appends
+#endif
   uint32_t wo;                     // window control or blocking overhead active (C1-C3)
   uint32_t dl_vc[VOLTANA_MAX_INSTANCES];  // decode lane: gaps above the ITL SLO so far
   uint64_t rq_base, it_base;       // outputs (E1-E3): request / iteration-slot base of the scenario
@@ -357,6 +364,9 @@ struct Err {               // first error of one lane in its own event order
 struct Dec {               // decode instance d, owned by lane d
   uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both, nfifo, far_h, far_hfin;
   bool busy, dead;
+#if VT_ADM_DEFER
+  uint32_t npq;            // pending wheel appends (admitted at the last START, applied at the next)
+#endif
   double end, ebusy, bms, top, sitl, tlast;
 #if VT_EDEFER
   double e_u, e_dyn, e_dur;  // running iteration's utilisation, DYN entry and duration (energy added at END)
@@ -598,6 +608,12 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       D.far_hfin = fn.next != NIL ? L.farfin[fn.next] : NIL;
       bucket_append(D, L, nbm, i, fin, (uint32_t)fn.in + fn.out, lfin, lb);
     }
+#if VT_ADM_DEFER && !VT_SWHEEL
+    // the previous START's admissions join their buckets now, in admission order (their lines
+    // were prefetched then; none of them finishes before this iteration ends)
+    for (uint32_t q = 0; q < D.npq; ++q) bucket_append(D, L, nbm, W.pq_i[d][q], W.pq_fin[d][q], W.pq_io[d][q], lfin, lb);
+    D.npq = 0u;
+#endif
     // FCFS admission while KV fits (A20)
     const double tau = W.tau;
     const uint32_t kvcap = W.kvcap;
@@ -613,8 +629,24 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       else D.qhn = L.node[D.qh];
 #endif
       const uint32_t fin = D.iters + (uint32_t)hn.out - 2u;  // its last iteration
-      if ((uint32_t)hn.out - 2u < W.nb) bucket_append(D, L, nbm, i, fin, (uint32_t)hn.in + hn.out, lfin, lb);
-      else far_insert(D, L, W.max_steps, i, fin);
+      const uint32_t o2 = (uint32_t)hn.out - 2u;
+      if (o2 < W.nb) {
+#if VT_ADM_DEFER && !VT_SWHEEL
+        if (o2 != 0u) {  // finishes after this iteration: append at the next START
+          if (D.npq == ADM_PQ) {  // full: apply the pending ones first (admission order)
+            for (uint32_t q = 0; q < ADM_PQ; ++q)
+              bucket_append(D, L, nbm, W.pq_i[d][q], W.pq_fin[d][q], W.pq_io[d][q], lfin, lb);
+            D.npq = 0u;
+          }
+          W.pq_i[d][D.npq] = i; W.pq_fin[d][D.npq] = fin; W.pq_io[d][D.npq] = (uint32_t)hn.in + hn.out;
+          D.npq += 1u;
+          prefetch_l1(L.wheel + (fin & nbm));
+        } else
+#endif
+        bucket_append(D, L, nbm, i, fin, (uint32_t)hn.in + hn.out, lfin, lb);
+      } else {
+        far_insert(D, L, W.max_steps, i, fin);
+      }
       D.nreq += 1u;
       D.nkv += need;
       D.pn -= 1u;
@@ -1500,6 +1532,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   D.busy = false;
   D.dead = !(lane < ND);
   D.end = 0.0;
+#if VT_ADM_DEFER
+  D.npq = 0u;
+#endif
 #if VT_DEFER_ITL
   D.lpos = (uint32_t)lane * CLOG_CHUNK;  // first chunks: one per lane, allocated in lane order
   D.lend = D.lpos + CLOG_CHUNK;

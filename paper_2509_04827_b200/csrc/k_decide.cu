@@ -11,6 +11,9 @@
 #include "vt_decide.h"
 #include "vt_device.cuh"
 
+#ifndef VT_DECIDE_ILP
+#define VT_DECIDE_ILP 1      // K2/K3 with K <= 8: branch-free level evaluation
+#endif
 #ifndef VT_ROUTE_LOCKSTEP
 #define VT_ROUTE_LOCKSTEP 0  // K3: the 2*N_D what-if scans of an item advance in lockstep over the levels
 #endif
@@ -66,7 +69,23 @@ __device__ void stage_tables(const DevProfile &PR, const LadderParam &LP, bool n
   __syncthreads();
 }
 
+template <int KK>
+__device__ __forceinline__ int scan_ttft_ilp(const double *tt, uint32_t nbt, double budget);
+
 __device__ __forceinline__ int scan_ttft(const double *tt, int K, uint32_t nbt, double budget) {
+#if VT_DECIDE_ILP
+  switch (K) {
+    case 1: return 0;
+    case 2: return scan_ttft_ilp<2>(tt, nbt, budget);
+    case 3: return scan_ttft_ilp<3>(tt, nbt, budget);
+    case 4: return scan_ttft_ilp<4>(tt, nbt, budget);
+    case 5: return scan_ttft_ilp<5>(tt, nbt, budget);
+    case 6: return scan_ttft_ilp<6>(tt, nbt, budget);
+    case 7: return scan_ttft_ilp<7>(tt, nbt, budget);
+    case 8: return scan_ttft_ilp<8>(tt, nbt, budget);
+    default: break;
+  }
+#endif
   for (int k = 0; k < K; ++k)
     if (ttft_pred(tt[2 * k], tt[2 * k + 1], nbt) <= budget) return k;
   return K - 1;
@@ -90,10 +109,43 @@ __device__ __forceinline__ uint32_t itl_tile(const DevProfile &PR, uint64_t n, i
   return j > (uint64_t)(PR.n_tiles - 1) ? (uint32_t)(PR.n_tiles - 1) : (uint32_t)j;
 }
 
+// K <= 8: levels 0..K-2 evaluated without branches (independent, predicated selects from the
+// top down = the lowest feasible level), else K-1 — the ascending scan's answer (A2).
+// The threads of a warp no longer wait for the longest early-exit chain among them.
+template <int KK>
+__device__ __forceinline__ int scan_itl_ilp(const double *row, double dn, double dkv, double target) {
+  int kk = KK - 1;
+#pragma unroll
+  for (int k = KK - 2; k >= 0; --k)
+    if (itl_eval(row, k, dn, dkv) <= target) kk = k;
+  return kk;
+}
+template <int KK>
+__device__ __forceinline__ int scan_ttft_ilp(const double *tt, uint32_t nbt, double budget) {
+  int kk = KK - 1;
+#pragma unroll
+  for (int k = KK - 2; k >= 0; --k)
+    if (ttft_pred(tt[2 * k], tt[2 * k + 1], nbt) <= budget) kk = k;
+  return kk;
+}
+
 __device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, int K, uint64_t n,
                                         uint64_t kv, double target, int wshift) {
   const double *row = itl_row(it, PR, K, n, wshift);
   const double dn = (double)n, dkv = (double)kv;
+#if VT_DECIDE_ILP
+  switch (K) {
+    case 1: return 0;
+    case 2: return scan_itl_ilp<2>(row, dn, dkv, target);
+    case 3: return scan_itl_ilp<3>(row, dn, dkv, target);
+    case 4: return scan_itl_ilp<4>(row, dn, dkv, target);
+    case 5: return scan_itl_ilp<5>(row, dn, dkv, target);
+    case 6: return scan_itl_ilp<6>(row, dn, dkv, target);
+    case 7: return scan_itl_ilp<7>(row, dn, dkv, target);
+    case 8: return scan_itl_ilp<8>(row, dn, dkv, target);
+    default: break;
+  }
+#endif
   for (int k = 0; k < K; ++k)
     if (itl_eval(row, k, dn, dkv) <= target) return k;
   return K - 1;

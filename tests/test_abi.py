@@ -121,3 +121,20 @@ def test_product_has_no_cpu_fallback():
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "oracle.h" not in src and "liboracle" not in src, f
                 assert "import synth" not in src and "from synth" not in src, f
+
+
+def test_simulate_workspace_grows_with_requests(vt):
+    """The split K4 keeps, per scenario, a 16-B request node (K4a -> K4b) and a 16-B
+    completion-log slot per request: the workspace bound grows by >= 32 B per (scenario,
+    request) of max_requests (voltana.h, voltana_simulate)."""
+    L = vt.lib()
+    lib = vt._lib
+    lays = (lib.Layout * 1)(lib.Layout(2, 2, 0, 150, 8192, 400000, 0.0))
+
+    def ws(n, mr):
+        tr = lib.Traces(1, 1, 1, 1, 1, 1, mr, 100, 0)
+        return int(L.voltana_simulate_workspace_bytes(C.byref(tr), lays, 1, n))
+
+    assert ws(100, 2000) - ws(100, 1000) >= 100 * 1000 * 32
+    assert ws(200, 1000) - ws(100, 1000) >= 100 * 1000 * 32
+    assert ws(4096, 45412) >= 4096 * 45412 * 32

@@ -11,6 +11,10 @@
 #include "vt_decide.h"
 #include "vt_device.cuh"
 
+#ifndef VT_ITS4
+#define VT_ITS4 0            // K2/K3 ITL rows padded to 4 doubles, a2+b2 in one LDS.128 (measured: K2 66 -> 51 %, K3 30 -> 29 %: off)
+#endif
+constexpr int ITS = VT_ITS4 ? 4 : 3;
 #ifndef VT_DECIDE_ILP
 #define VT_DECIDE_ILP 1      // K2/K3 with K <= 8: branch-free level evaluation
 #endif
@@ -32,10 +36,10 @@ struct SmemTables {
 __device__ __forceinline__ int tt_len(int K, const DevProfile &PR) { return 2 * PR.n_ptiles * K; }
 __device__ __forceinline__ double *itl_smem(double *sm, int K, const DevProfile &PR) { return sm + tt_len(K, PR); }
 __device__ __forceinline__ double *dyn_smem(double *sm, int K, const DevProfile &PR) {
-  return sm + tt_len(K, PR) + 3 * PR.n_tiles * K;
+  return sm + tt_len(K, PR) + ITS * PR.n_tiles * K;
 }
 __device__ __forceinline__ int *mhz_smem(double *sm, int K, const DevProfile &PR) {
-  return (int *)(sm + tt_len(K, PR) + 3 * PR.n_tiles * K + K);
+  return (int *)(sm + tt_len(K, PR) + ITS * PR.n_tiles * K + K);
 }
 // TTFT row {a1, c1}[K] of the batch's prefill tile
 __device__ __forceinline__ const double *tt_row(const double *sm, int K, const DevProfile &PR, uint32_t nbt) {
@@ -63,7 +67,8 @@ __device__ void stage_tables(const DevProfile &PR, const LadderParam &LP, bool n
     for (int x = threadIdx.x; x < T * K; x += blockDim.x) {
       int j = x / K, k = x - j * K;
       size_t o = (size_t)j * PR.k + LP.level[k];
-      it[3 * x] = PR.a2[o]; it[3 * x + 1] = PR.b2[o]; it[3 * x + 2] = PR.c2[o];
+      it[ITS * x] = PR.a2[o]; it[ITS * x + 1] = PR.b2[o]; it[ITS * x + 2] = PR.c2[o];
+      if (ITS == 4) it[ITS * x + 3] = 0.0;
     }
   }
   __syncthreads();
@@ -97,11 +102,16 @@ __device__ __forceinline__ const double *itl_row(const double *it, const DevProf
                                                  int wshift) {
   uint64_t j = wshift >= 0 ? (n - 1u) >> wshift : (n - 1u) / (uint64_t)PR.tile_w;
   if (j > (uint64_t)(PR.n_tiles - 1)) j = (uint64_t)(PR.n_tiles - 1);
-  return it + 3 * (size_t)j * K;
+  return it + ITS * (size_t)j * K;
 }
 
 __device__ __forceinline__ double itl_eval(const double *row, int k, double dn, double dkv) {
+#if VT_ITS4
+  const double2 ab = *reinterpret_cast<const double2 *>(row + 4 * k);  // one LDS.128 for a2, b2
+  return add(add(mul(ab.x, dn), mul(ab.y, dkv)), row[4 * k + 2]);
+#else
   return add(add(mul(row[3 * k], dn), mul(row[3 * k + 1], dkv)), row[3 * k + 2]);
+#endif
 }
 
 __device__ __forceinline__ uint32_t itl_tile(const DevProfile &PR, uint64_t n, int wshift) {
@@ -330,7 +340,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
     const uint64_t nn = (uint64_t)n[d < NI ? d : 0] + (q & 1), kk = (uint64_t)kv[d < NI ? d : 0] + ((q & 1) ? in + 1u : 0u);
     lv[q] = (q & 1) == 0 && nn == 0 ? 0 : K - 1;
     dn[q] = d >= ND || ((q & 1) == 0 && nn == 0);
-    row[q] = dn[q] ? 0 : 3 * K * (int)itl_tile(P.prof, nn, wshift);
+    row[q] = dn[q] ? 0 : ITS * K * (int)itl_tile(P.prof, nn, wshift);
     xn[q] = (double)nn; xk[q] = (double)kk;
   }
   for (int k = 0; k < K - 1; ++k) {
@@ -338,7 +348,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
 #pragma unroll
     for (int q = 0; q < 2 * NI; ++q) {
       if (dn[q]) continue;
-      const double *r = it + row[q] + 3 * k;
+      const double *r = it + row[q] + ITS * k;
       if (add(add(mul(r[0], xn[q]), mul(r[1], xk[q])), r[2]) <= tgt) { lv[q] = k; dn[q] = true; }
       all = all && dn[q];
     }
@@ -444,7 +454,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
 
 size_t decide_smem_bytes(int k, int n_tiles, int n_ptiles) {
   const int tp = n_ptiles < 1 ? 1 : n_ptiles;
-  return (size_t)(2 * tp * k + 3 * n_tiles * k + k) * sizeof(double) + (size_t)k * sizeof(int);
+  return (size_t)(2 * tp * k + ITS * n_tiles * k + k) * sizeof(double) + (size_t)k * sizeof(int);
 }
 
 cudaError_t launch_control(const ControlParams &P, int phase, int grid, size_t smem, cudaStream_t st) {

@@ -25,7 +25,7 @@ constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
 size_t sim_smem_fixed(bool fast);  // per-warp shared-memory block without the staged ITL table
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size
 #ifndef VT_NBMAX
-#define VT_NBMAX 1024
+#define VT_NBMAX 2048
 #endif
 #ifndef VT_UTAB
 #define VT_UTAB 1  // utilisation table for busy power (one 1-MB setup launch; measured -0.5 %)

@@ -1,5 +1,4 @@
-for so in "" variants/lib_nb2k.so "" variants/lib_nb2k.so; do
+for so in "" variants/lib_nb4k.so "" variants/lib_nb4k.so; do
 VOLTANA_SO=$so timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/v.csv python tools/prof_sim.py --reps 3 > /dev/null 2>&1
 echo "== $so"; grep -v "^==" gpurun_out/v.csv | awk -F'","' '{print $5, $NF}' | grep simulate_kernel | tr '\n' ' '; echo
 done
-VOLTANA_SO=variants/lib_nb2k.so timeout 900 python -m pytest tests -m gpu -x -q -k "simulate" 2>&1 | tail -1

@@ -1008,6 +1008,17 @@ template <int G> struct Grp {
   static constexpr unsigned all = G == 32 ? 0xffffffffu : ((1u << G) - 1u);
 };
 
+// Window element access: from the group's shared copy (PCtxS) or by shuffle (register context).
+struct PCtxS;
+struct PCtx;
+template <int G> __device__ __forceinline__ void win_put(PCtx &, uint32_t, double, uint32_t) {}
+template <int G> __device__ __forceinline__ double win_a(const PCtx &, const Grp<G> &g, double a, uint32_t i) {
+  return g.shfl(a, (int)i);
+}
+template <int G> __device__ __forceinline__ uint32_t win_ps(const PCtx &, const Grp<G> &g, uint32_t ps, uint32_t i) {
+  return g.shfl(ps, (int)i);
+}
+
 struct PState {   // uniform state of one prefill instance (every lane holds the same values)
   double ebusy, bms, top, sttft, tlast, errt, tfree, last;
   uint64_t h;
@@ -1203,13 +1214,16 @@ __device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double
       const uint32_t y = g.shfl_up(ps, s);
       if (lane >= (uint32_t)s) ps += y;
     }
+    __syncwarp(g.m);           // the previous window's reads are done
+    win_put<G>(W, lane, a, ps);
+    __syncwarp(g.m);
     double e = 0.0;            // this lane's batch end, once its batch has started
     uint32_t hl = 0;           // head lane of the next batch
     bool err = false, general = false;
     while (hl < nwin) {
-      const double a0 = g.shfl(a, (int)hl);
+      const double a0 = win_a<G>(W, g, a, hl);
       const double ts = S.tfree > a0 ? S.tfree : a0;  // START: instance idle and queue non-empty
-      const uint32_t psb = hl ? g.shfl(ps, (int)(hl - 1u)) : 0u;  // tokens before the head
+      const uint32_t psb = hl ? win_ps<G>(W, g, ps, hl - 1u) : 0u;  // tokens before the head
       const bool arrived = a <= ts;
       const bool take = lane > hl && arrived && !(ps - psb > B);
       const unsigned fails = g.ballot(lane > hl && !take);
@@ -1218,8 +1232,8 @@ __device__ void prefill_warp(const SimParams &P, WS &W, Node *node, const double
         break;
       }
       const uint32_t f = (uint32_t)ffs0(fails);  // first candidate not taken
-      const bool backlog = g.shfl(arrived, (int)f);  // arrived but does not fit (A5)
-      const uint32_t nbt = g.shfl(ps, (int)(f - 1u)) - psb;
+      const bool backlog = win_a<G>(W, g, a, f) <= ts;  // arrived but does not fit (A5)
+      const uint32_t nbt = win_ps<G>(W, g, ps, f - 1u) - psb;
       double end;
       if (!pa_decide<V, F, G>(P, W, S, p, ts, a0, nbt, backlog, end)) { err = true; break; }
       if (lane >= hl && lane < f) e = end;
@@ -1900,7 +1914,19 @@ struct PCtxS {
   uint64_t seed, rq_base, it_base;
   double tt[2 * VOLTANA_MAX_LEVELS];  // [K][a1, c1]
   double dyn[VOLTANA_MAX_LEVELS];     // prefill DYN
+  double wa[32];                      // the window's arrivals and inclusive token prefix sums
+  uint32_t wps[32];
 };
+template <int G> __device__ __forceinline__ void win_put(PCtxS &W, uint32_t lane, double a, uint32_t ps) {
+  W.wa[lane] = a;
+  W.wps[lane] = ps;
+}
+template <int G> __device__ __forceinline__ double win_a(const PCtxS &W, const Grp<G> &, double, uint32_t i) {
+  return W.wa[i];
+}
+template <int G> __device__ __forceinline__ uint32_t win_ps(const PCtxS &W, const Grp<G> &, uint32_t, uint32_t i) {
+  return W.wps[i];
+}
 __device__ __forceinline__ void pctx_scalars(PCtxS &S, const PCtx &C) {
   S.tgt_ttft = C.tgt_ttft; S.slo_ttft = C.slo_ttft; S.p_idle = C.p_idle; S.tdp = C.tdp; S.uh_p = C.uh_p;
   S.uh_d = C.uh_d; S.ctrl_iv = C.ctrl_iv; S.fs_ov = C.fs_ov; S.a1g = C.a1g; S.c1g = C.c1g; S.ut = C.ut;

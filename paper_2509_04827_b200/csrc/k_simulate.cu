@@ -1018,6 +1018,10 @@ template <int G> __device__ __forceinline__ double win_a(const PCtx &, const Grp
 template <int G> __device__ __forceinline__ uint32_t win_ps(const PCtx &, const Grp<G> &g, uint32_t ps, uint32_t i) {
   return g.shfl(ps, (int)i);
 }
+template <int G> __device__ __forceinline__ void win_tput(PCtx &, uint32_t, double) {}
+template <int G> __device__ __forceinline__ double win_t(const PCtx &, const Grp<G> &g, double t, uint32_t i) {
+  return g.shfl(t, (int)i);
+}
 
 struct PState {   // uniform state of one prefill instance (every lane holds the same values)
   double ebusy, bms, top, sttft, tlast, errt, tfree, last;
@@ -1072,7 +1076,7 @@ __device__ __forceinline__ bool pa_decide(const SimParams &P, const WS &W, PStat
 
 // O5 for lanes [0, n): request base + lane*NP (arrival a, in x, out o) finished prefill at e.
 template <int V, int G, class WS>
-__device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PState &S, Node *node, uint32_t base,
+__device__ __forceinline__ void pa_account(const SimParams &P, WS &W, PState &S, Node *node, uint32_t base,
                                            uint32_t NP, uint32_t n, double e, double a, uint32_t x, uint32_t o) {
   if (n == 0u) return;
   const Grp<G> g;
@@ -1081,10 +1085,13 @@ __device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PSta
   const uint32_t i = base + lane * NP;
   const double ttft = valid ? sub(e, a) : 0.0;  // A26
   const bool ok = valid && ttft <= W.slo_ttft;
+  __syncwarp(g.m);
+  win_tput<G>(W, lane, ttft);
+  __syncwarp(g.m);
   for (uint32_t b = 0; b < n; b += 8u) {  // the report sum in FCFS order (A37)
     double v[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = g.shfl(ttft, (int)(b + u) & (G - 1));
+    for (int u = 0; u < 8; ++u) v[u] = win_t<G>(W, g, ttft, (b + u) & (G - 1));
 #pragma unroll
     for (int u = 0; u < 8; ++u)
       if (b + u < n) S.sttft = add(S.sttft, v[u]);
@@ -1128,7 +1135,7 @@ __device__ __forceinline__ void pa_account(const SimParams &P, const WS &W, PSta
 // General path for one batch starting at request nxt (any length): candidates in rounds of 32,
 // accounting in chunks of 32. Returns the next unbatched request, or NIL on an error.
 template <int V, bool F, int G, class WS>
-__device__ uint32_t pa_batch_general(const SimParams &P, const WS &W, PState &S, Node *node, const double *arr,
+__device__ uint32_t pa_batch_general(const SimParams &P, WS &W, PState &S, Node *node, const double *arr,
                                      const uint32_t *inl, const uint32_t *outl, uint32_t N, uint32_t p,
                                      uint32_t NP, uint32_t nxt) {
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
@@ -1916,6 +1923,7 @@ struct PCtxS {
   double dyn[VOLTANA_MAX_LEVELS];     // prefill DYN
   double wa[32];                      // the window's arrivals and inclusive token prefix sums
   uint32_t wps[32];
+  double wt[32];                      // the TTFTs being added to the report sum (O5, A37)
 };
 template <int G> __device__ __forceinline__ void win_put(PCtxS &W, uint32_t lane, double a, uint32_t ps) {
   W.wa[lane] = a;
@@ -1926,6 +1934,10 @@ template <int G> __device__ __forceinline__ double win_a(const PCtxS &W, const G
 }
 template <int G> __device__ __forceinline__ uint32_t win_ps(const PCtxS &W, const Grp<G> &, uint32_t, uint32_t i) {
   return W.wps[i];
+}
+template <int G> __device__ __forceinline__ void win_tput(PCtxS &W, uint32_t lane, double t) { W.wt[lane] = t; }
+template <int G> __device__ __forceinline__ double win_t(const PCtxS &W, const Grp<G> &, double, uint32_t i) {
+  return W.wt[i];
 }
 __device__ __forceinline__ void pctx_scalars(PCtxS &S, const PCtx &C) {
   S.tgt_ttft = C.tgt_ttft; S.slo_ttft = C.slo_ttft; S.p_idle = C.p_idle; S.tdp = C.tdp; S.uh_p = C.uh_p;

@@ -1610,6 +1610,14 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const bool ens = (V & 1) && LY.policy == 2 && ND > 1;
   const int32_t delta = LY.delta_mhz;
   int w = argmin_time(fabs(hn.tf), hd != NIL);  // next PrefillDone request in (t, p, id) order
+#ifdef VT_LAT_PROBE
+  // experiment: clock64 cycles per phase of the route loop, summed over the scenario
+  // [0] select + stream advance, [1] decode advance, [2] EcoRoute + push, [3] drain + ITL pass
+  long long lp_acc[4] = {0, 0, 0, 0}, lp_t = clock64();
+#define LP_MARK(q) do { const long long _n = clock64(); lp_acc[q] += _n - lp_t; lp_t = _n; } while (0)
+#else
+#define LP_MARK(q) do { } while (0)
+#endif
   for (;;) {
     if (w < 0) break;
     if (steps_route > N) { dE.t = 0.0; dE.code = VOLTANA_ITEM_E_INTERNAL; break; }  // watchdog
@@ -1640,10 +1648,12 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     const int w_next = argmin_time(fabs(hn.tf), hd != NIL);
 #endif
     // decode instances catch up to t: events strictly before t (PrefillDone drains first)
+    LP_MARK(0);
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
       dec_advance_all<V, F>(D, lane, L, W, t, dE, P.o);
       t_adv = t;
     }
+    LP_MARK(1);
     // ---- O8 EcoRoute
     int dsel, cse;
     if (ens) {  // ---- energy-scored router [B1-B3]
@@ -1728,6 +1738,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       if (__popc(inset) >= 2) cursor = wrap_nd((uint32_t)dsel + 1u, (uint32_t)ND);
     }
     steps_route++;
+    LP_MARK(2);
     h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
     if (lane == dsel) {
       if (eco) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
@@ -1763,6 +1774,11 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   if ((V & 2) && W.it_on && lane < ND) P.o.iter_count[W.it_base / P.o.iter_cap + NP + lane] = D.iters;
   __syncwarp(gmask());
 
+#ifdef VT_LAT_PROBE
+  LP_MARK(3);
+  if (P.timing && lane == 0)
+    for (int q = 0; q < 4; ++q) P.timing[2 * (size_t)P.n + 4 * (size_t)s + q] = (uint64_t)lp_acc[q];
+#endif
   // ================================================================ O9: record
   // first error in (time, prefill before decode, instance) order = the oracle's stop point
   const double pet = lane < NP ? W.pa[lane].errt : INF;

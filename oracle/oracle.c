@@ -439,6 +439,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
       uint32_t i = xq_id[xq_head], d = xq_d[xq_head];
       xq_head++;
       D[d].admq[D[d].q_tail++] = i;
+      if (diag && diag->req_tqueue) diag->req_tqueue[i] = t;
     }
 
     for (int q = 0; q < NP; ++q) { /* O5: PrefillDone(q) */
@@ -481,6 +482,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
         D[d].pend_kv += (uint64_t)in[i] + 1;
         if (tau == 0.0) {
           D[d].admq[D[d].q_tail++] = (uint32_t)i;
+          if (diag && diag->req_tqueue) diag->req_tqueue[i] = t;
         } else {
           xq_id[xq_tail] = (uint32_t)i;
           xq_d[xq_tail] = (uint32_t)d;
@@ -605,6 +607,7 @@ int oracle_simulate(const orc_scenario *s, orc_result *res, orc_diag *diag) {
           I->cap_run *= 2;
           I->run = realloc(I->run, I->cap_run * sizeof(run_entry));
         }
+        if (diag && diag->req_tadmit) diag->req_tadmit[hd] = t;
         I->run[I->n_run].id = hd;
         I->run[I->n_run].rem = out[hd] - 1;
         I->n_run++;

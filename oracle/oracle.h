@@ -96,6 +96,8 @@ typedef struct {
   uint32_t *iter_load;     /* [iter_cap] N_bt (prefill) / N_req (decode)     */
   uint32_t *iter_kv;       /* [iter_cap] N_kv (decode), 0 (prefill)          */
   uint8_t *iter_flags;     /* [iter_cap] bit0 decision, bit1 overhead, bit2 backlog */
+  double *req_tadmit;      /* [n] time the request joined its decode running set (NaN: never) */
+  double *req_tqueue;      /* [n] time it joined its decode admission queue (NaN: never)       */
 } orc_diag;
 
 /* status codes (result.status / per-item status) */

@@ -64,7 +64,8 @@ class OrcDiag(C.Structure):
                 ("max_nreq", vp), ("boundary", C.c_uint32), ("force_decode", vp), ("force_level", vp),
                 ("n_force_level", C.c_uint64), ("tokens", vp), ("kv_peak", vp), ("iter_cap", C.c_uint64),
                 ("iter_n", C.c_uint64), ("iter_inst", vp), ("iter_level", vp), ("iter_dur", vp),
-                ("iter_target", vp), ("iter_start", vp), ("iter_load", vp), ("iter_kv", vp), ("iter_flags", vp)]
+                ("iter_target", vp), ("iter_start", vp), ("iter_load", vp), ("iter_kv", vp), ("iter_flags", vp),
+                ("req_tadmit", vp), ("req_tqueue", vp)]
 
 
 def lib():
@@ -144,7 +145,8 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                  iter_level=np.zeros(max(iter_cap, 1), np.uint16), iter_dur=np.zeros(max(iter_cap, 1)),
                  iter_target=np.zeros(max(iter_cap, 1)), iter_start=np.zeros(max(iter_cap, 1)),
                  iter_load=np.zeros(max(iter_cap, 1), np.uint32), iter_kv=np.zeros(max(iter_cap, 1), np.uint32),
-                 iter_flags=np.zeros(max(iter_cap, 1), np.uint8))
+                 iter_flags=np.zeros(max(iter_cap, 1), np.uint8),
+                 req_tadmit=np.full(n, np.nan), req_tqueue=np.full(n, np.nan))
         fd = None if force_decode is None else np.ascontiguousarray(force_decode, np.int32)
         fl = None if force_level is None else np.ascontiguousarray(force_level, np.uint16)
         keep += [fd, fl]
@@ -153,7 +155,8 @@ def simulate(arrival, in_len, out_len, duration_ms, slo, layout, ladder, prof, h
                      int(boundary), _ptr(fd), _ptr(fl), 0 if fl is None else len(fl),
                      _ptr(d["tokens"]), _ptr(d["kv_peak"]), int(iter_cap), 0, _ptr(d["iter_inst"]),
                      _ptr(d["iter_level"]), _ptr(d["iter_dur"]), _ptr(d["iter_target"]), _ptr(d["iter_start"]),
-                     _ptr(d["iter_load"]), _ptr(d["iter_kv"]), _ptr(d["iter_flags"]))
+                     _ptr(d["iter_load"]), _ptr(d["iter_kv"]), _ptr(d["iter_flags"]),
+                     _ptr(d["req_tadmit"]), _ptr(d["req_tqueue"]))
         if diag is not None:
             diag.update(d)
     lib().oracle_simulate(C.byref(sc), res.ctypes.data, None if dg is None else C.byref(dg))

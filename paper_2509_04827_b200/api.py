@@ -175,9 +175,11 @@ class DeviceWorkload:
     slos / layouts / grids / profiles: small host tables (objects with the documented fields).
     order: "lpt" (default) claims expensive scenarios first; records are returned in the
     caller's scenario order either way.
+    out: optional preallocated [n, 128] uint8 device tensor (e.g. a view of a collective's send
+    buffer) the records are written to, in kernel order (`perm`).
     """
 
-    def __init__(self, traces, slos, layouts, grids, profiles, scen, device="cuda", order="lpt"):
+    def __init__(self, traces, slos, layouts, grids, profiles, scen, device="cuda", order="lpt", out=None):
         self.device = torch.device(device)
         offset = np.asarray(traces.offset, np.uint64)
         lens = np.diff(offset.astype(np.int64))
@@ -225,7 +227,11 @@ class DeviceWorkload:
                                          self.max_requests, max(1, min(self.max_out, 65535)), 0)
         self.scen_struct = _lib.Scenarios(*[_p(self.sc[k]) for k in ("trace_id", "slo_id", "layout_id", "grid_id",
                                                                      "profile_id", "hash_seed")])
-        self.out = torch.empty((n, 128), dtype=torch.uint8, device=self.device)
+        if out is None:
+            out = torch.empty((n, 128), dtype=torch.uint8, device=self.device)
+        if tuple(out.shape) != (n, 128) or out.dtype != torch.uint8 or not out.is_contiguous():
+            raise ValueError("out must be a contiguous [n, 128] uint8 tensor")
+        self.out = out
         need = int(lib().voltana_simulate_workspace_bytes(C.byref(self.traces_struct), self.layouts,
                                                           len(layouts), n))
         self.workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)

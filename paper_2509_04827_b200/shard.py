@@ -63,3 +63,61 @@ def gather_records(local: torch.Tensor, parts: list[np.ndarray], n_total: int, g
     for r, p in enumerate(parts):
         res[p] = host[r, : len(p)]
     return res
+
+
+def weak_parts(n_local: int, world: int) -> list[np.ndarray]:
+    """Weak scaling: rank r owns global scenarios r*n_local .. (r+1)*n_local - 1 (its own seed
+    block; the global index is the record's position in the gathered sweep)."""
+    return [np.arange(r * n_local, (r + 1) * n_local, dtype=np.int64) for r in range(world)]
+
+
+class RecordGather:
+    """The per-step collective of the sharded sweep: every rank's 128-B records, padded to the
+    largest shard, all-gathered into one buffer (NCCL all_gather_into_tensor over NVLink; gloo
+    on CPU). The simulate launch writes straight into `local` (a view of the padded send
+    buffer), so the step adds no copy kernel. The records of a rank are in its kernel order
+    (`kernel_order` = the DeviceWorkload's permutation of its part); the host maps them back to
+    global scenario order once, outside the timed region."""
+
+    def __init__(self, parts: list[np.ndarray], device, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.parts = [np.asarray(p, np.int64) for p in parts]
+        self.m = max(1, max(len(p) for p in self.parts))
+        self.n_total = int(sum(len(p) for p in self.parts))
+        self.nccl = dist.get_backend(group) == "nccl"
+        self.pad = torch.zeros((self.m, RECORD_BYTES), dtype=torch.uint8, device=device)
+        self.local = self.pad[: len(self.parts[self.rank])]
+        self.out = torch.empty((self.world * self.m, RECORD_BYTES), dtype=torch.uint8, device=device)
+        self.kernel_order = None
+
+    def set_kernel_order(self, perm: np.ndarray):
+        """perm[j] = index into this rank's part of the scenario in kernel slot j; exchanged once
+        so rank 0 can place every rank's records."""
+        perm = np.asarray(perm, np.int64)
+        t = torch.full((self.m,), -1, dtype=torch.int64)
+        t[: len(perm)] = torch.from_numpy(perm)
+        dev = self.pad.device
+        buf = [torch.empty_like(t.to(dev)) for _ in range(self.world)]
+        dist.all_gather(buf, t.to(dev), group=self.group)
+        self.kernel_order = [b.cpu().numpy() for b in buf]
+
+    def enqueue(self):
+        """The step's collective (asynchronous on the current stream for NCCL)."""
+        if self.nccl:
+            dist.all_gather_into_tensor(self.out, self.pad, group=self.group)
+        else:
+            lst = list(self.out.view(self.world, self.m, RECORD_BYTES).unbind(0))
+            dist.all_gather(lst, self.pad, group=self.group)
+            self.out.view(self.world, self.m, RECORD_BYTES).copy_(torch.stack(lst))
+
+    def host_global(self) -> np.ndarray:
+        """All records in global scenario order (host [n_total, 128] uint8)."""
+        host = self.out.view(self.world, self.m, RECORD_BYTES).cpu().numpy()
+        res = np.zeros((self.n_total, RECORD_BYTES), np.uint8)
+        for r, p in enumerate(self.parts):
+            k = len(p)
+            order = np.arange(k) if self.kernel_order is None else self.kernel_order[r][:k]
+            res[p[order]] = host[r, :k]
+        return res

@@ -158,8 +158,9 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level,
  * prefill timelines of every scenario (K4a, one warp per prefill instance), then routing +
  * decode (K4b, one warp per scenario; the per-request ITL accounting runs in the same warp
  * after each scenario for the paper's-policy kernels).
- * Workspace (voltana_simulate_workspace_bytes) grows as n x max_requests x 32 B: per scenario
- * a 16-B node per request (K4a -> K4b) and a 16-B completion-log slot per request.
+ * Workspace (voltana_simulate_workspace_bytes[_ex]): a 16-B node per request of every
+ * scenario (K4a -> K4b) plus fixed per-warp scratch (see below).
+ * A non-OK return means nothing was enqueued (kernel attributes are set before any enqueue).
  * Errors: INVALID_ARG, LADDER, COVERAGE, CONFIG, WORKSPACE, CUDA. Per-scenario problems
  * go to out[i].status (then only status and n_requests are set).                        */
 typedef struct {
@@ -215,6 +216,12 @@ typedef struct {
 typedef struct {            /* device arrays [n]                                        */
   const uint32_t *trace_id, *slo_id, *layout_id, *grid_id, *profile_id;
   const uint64_t *hash_seed;/* h0 of the decision hash = global scenario index [A36]    */
+  const uint64_t *node_offset; /* device [n + 1] or NULL: exclusive prefix sum of the
+                               scenarios' request counts (array order), so the request
+                               nodes take total_requests x 16 B instead of n x
+                               max_requests x 16 B; a scenario whose range differs from
+                               its trace's length gets status E_INPUT                    */
+  uint64_t total_requests;  /* host: node_offset[n] (ignored when node_offset is NULL)  */
 } voltana_scenarios;
 
 typedef struct {            /* 128-byte per-scenario record                             */
@@ -225,9 +232,16 @@ typedef struct {            /* 128-byte per-scenario record                     
       e_decode_idle_j, busy_ms_prefill, busy_ms_decode, top_level_ms, horizon_ms;
 } voltana_result;
 
+/* Workspace of voltana_simulate for n_scenarios scenarios: the request nodes (16 B per
+ * request of every scenario: n_scenarios x max_requests, or total_requests when the scenario
+ * table carries node_offset — pass that total to the _ex form), plus per resident warp a
+ * far-list array (4 B x max_requests), a completion log (32 KB) and decode timing wheels. */
 size_t voltana_simulate_workspace_bytes(const voltana_traces *traces_h,
                                         const voltana_layout *layouts_h, int n_layouts,
                                         size_t n_scenarios);
+size_t voltana_simulate_workspace_bytes_ex(const voltana_traces *traces_h,
+                                           const voltana_layout *layouts_h, int n_layouts,
+                                           size_t n_scenarios, uint64_t total_requests);
 voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_slo *slos_h,
                                 int n_slos, const voltana_layout *layouts_h, int n_layouts,
                                 const voltana_grid *grids_h, int n_grids,

@@ -62,7 +62,7 @@ class Traces(C.Structure):
 
 class Scenarios(C.Structure):
     _fields_ = [("trace_id", vp), ("slo_id", vp), ("layout_id", vp), ("grid_id", vp), ("profile_id", vp),
-                ("hash_seed", vp)]
+                ("hash_seed", vp), ("node_offset", vp), ("total_requests", C.c_uint64)]
 
 
 class Outputs(C.Structure):
@@ -86,7 +86,8 @@ RESULT_DTYPE = np.dtype([
 assert RESULT_DTYPE.itemsize == 128
 
 EXPORTS = ("voltana_control_step", "voltana_route_batch", "voltana_fit_profile", "voltana_fit_workspace_bytes",
-           "voltana_simulate", "voltana_simulate_ex", "voltana_series_to_samples", "voltana_simulate_workspace_bytes", "voltana_status_string",
+           "voltana_simulate", "voltana_simulate_ex", "voltana_series_to_samples", "voltana_simulate_workspace_bytes",
+           "voltana_simulate_workspace_bytes_ex", "voltana_status_string",
            "voltana_last_error_detail", "voltana_last_launch_count", "voltana_debug_set_timing",
            "voltana_set_split_event")
 
@@ -113,6 +114,8 @@ def lib():
                                       vp, vp, vp, vp, vp, vp, vp, vp, vp, C.c_size_t, vp]
     L.voltana_simulate_workspace_bytes.argtypes = [P(Traces), P(Layout), C.c_int, C.c_size_t]
     L.voltana_simulate_workspace_bytes.restype = C.c_size_t
+    L.voltana_simulate_workspace_bytes_ex.argtypes = [P(Traces), P(Layout), C.c_int, C.c_size_t, C.c_uint64]
+    L.voltana_simulate_workspace_bytes_ex.restype = C.c_size_t
     L.voltana_simulate.argtypes = [P(Traces), P(Slo), C.c_int, P(Layout), C.c_int, P(Grid), C.c_int, P(Profile),
                                    C.c_int, P(Scenarios), C.c_size_t, vp, vp, C.c_size_t, vp]
     L.voltana_simulate_ex.argtypes = [P(Traces), P(Slo), C.c_int, P(Layout), C.c_int, P(Grid), C.c_int, P(Profile),

@@ -203,6 +203,13 @@ class DeviceWorkload:
         self.sc = {k: self._up(sc[k], torch.uint32) for k in ("trace_id", "slo_id", "layout_id", "grid_id",
                                                              "profile_id")}
         self.sc["hash_seed"] = self._up(np.asarray(sc["hash_seed"], np.uint64), torch.uint64)
+        # request-node ranges per scenario (kernel order): the workspace holds sum(N_s) nodes
+        tid = np.asarray(sc["trace_id"], np.int64)
+        nreq = np.where(tid < len(lens), lens[np.minimum(tid, max(len(lens) - 1, 0))], 0) if n and len(lens) \
+            else np.zeros(n, np.int64)
+        self.node_offset_host = np.concatenate([[0], np.cumsum(nreq)]).astype(np.uint64)
+        self.total_requests = int(self.node_offset_host[-1])
+        self.sc["node_offset"] = self._up(self.node_offset_host, torch.uint64)
         self.profiles = [p if isinstance(p, DeviceProfile) else DeviceProfile(p, self.device) for p in profiles]
         self.slos = (_lib.Slo * len(slos))(*[_lib.Slo(float(s.ttft), float(s.itl), float(s.scale)) for s in slos])
         # execution-noise factor tables (D1, D2) live on the device for the workload's lifetime
@@ -226,14 +233,15 @@ class DeviceWorkload:
                                          _p(self.tr["offset"]), _p(self.tr["duration"]), self.n_traces,
                                          self.max_requests, max(1, min(self.max_out, 65535)), 0)
         self.scen_struct = _lib.Scenarios(*[_p(self.sc[k]) for k in ("trace_id", "slo_id", "layout_id", "grid_id",
-                                                                     "profile_id", "hash_seed")])
+                                                                     "profile_id", "hash_seed", "node_offset")],
+                                          self.total_requests)
         if out is None:
             out = torch.empty((n, 128), dtype=torch.uint8, device=self.device)
         if tuple(out.shape) != (n, 128) or out.dtype != torch.uint8 or not out.is_contiguous():
             raise ValueError("out must be a contiguous [n, 128] uint8 tensor")
         self.out = out
-        need = int(lib().voltana_simulate_workspace_bytes(C.byref(self.traces_struct), self.layouts,
-                                                          len(layouts), n))
+        need = int(lib().voltana_simulate_workspace_bytes_ex(C.byref(self.traces_struct), self.layouts,
+                                                             len(layouts), n, self.total_requests))
         self.workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         self.n_layouts, self.n_slos, self.n_grids = len(layouts), len(slos), len(gs)
         # host copies the optional outputs are laid out from (caller order)

@@ -258,16 +258,11 @@ uint32_t wheel_buckets(uint32_t max_out) {
   return nb;
 }
 
-size_t tr_stride_clog(const voltana_traces *tr) {
-  return (size_t)tr->max_requests + 2 * VOLTANA_MAX_INSTANCES * CLOG_CHUNK;
-}
-
 struct SimLayout {
-  size_t node, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
-  uint32_t n_slots, nb, itl_smem, sw_off, ring_r = 0, ring_nd = 0, ks_off = 0;
+  size_t far, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
+  uint32_t n_slots, nb, itl_smem, ring_r = 0, ring_nd = 0, ks_off = 0;
   size_t ring_e_off = 0, ring_c_off = 0;
-  size_t nodes_off = 0, pares_off = 0, rtab_off = 0;  // VT_SPLIT_A
-  size_t clog_off = 0, clog_n_off = 0;                 // VT_DEFER_ITL
+  size_t nodes_off = 0, pares_off = 0, rtab_off = 0;
 };
 
 int resident_warps(size_t smem_per_block) {
@@ -286,34 +281,27 @@ int resident_warps(size_t smem_per_block) {
       cudaGetLastError();
       nb = 1;
     }
-    cached = nb * sm_count() * (SIM_THREADS / 32) * SPW;  // scenario slots
+    cached = nb * sm_count() * (SIM_THREADS / 32);  // scenario slots
     cached_smem = smem_per_block;
   }
   return cached;
 }
 
 // fast: the fast-table instantiation (K <= 8 staged tables) will run [DESIGN §5 item 7]
+// total_requests: sum of the scenarios' request counts (0: n x max_requests)
 SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n_layouts, int kmax, int tmax,
-                     size_t n, bool fast = false) {
+                     size_t n, uint64_t total_requests, bool fast = false) {
   SimLayout L;
   L.nb = wheel_buckets(tr->max_out);
   size_t itl_bytes = (size_t)kmax * tmax * 24;
   L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
   L.smem_per_warp = (sim_smem_fixed(fast) + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
-  L.sw_off = (uint32_t)L.smem_per_warp;
-#if VT_SPLIT_A && VT_DEFER_ITL && VT_ITL_INWARP
-  L.ks_off = (uint32_t)L.smem_per_warp;  // in-warp ITL pass scratch
-  L.smem_per_warp += ITL_SCRATCH;
-#endif
-#ifdef VT_SWHEEL
-  L.smem_per_warp += (size_t)max_nd(lays, n_layouts) * VT_SWHEEL * 16;
-#endif
-  L.smem = L.smem_per_warp * (SIM_THREADS / 32) * SPW;  // per-scenario block x scenarios per CTA
-  // VT_SPLIT_A: request nodes live per scenario (K4a writes them before K4b runs), so the
-  // per-warp slot keeps only the far-list array
-  L.node = VT_SPLIT_A ? 0 : align256((size_t)tr->max_requests * 16);
-  L.slot = L.node + align256((size_t)tr->max_requests * 4);
-  L.slot = L.slot > 256 ? L.slot : 256;
+  L.ks_off = (uint32_t)L.smem_per_warp;  // ITL-pass scratch
+  L.smem_per_warp += (sizeof(ItlScratch) + 15) & ~(size_t)15;
+  L.smem = L.smem_per_warp * (SIM_THREADS / 32);
+  // per resident warp: far-list finishing iterations [max_requests], then the completion log
+  L.far = align256((size_t)tr->max_requests * 4);
+  L.slot = L.far + (size_t)CLOG_CAP * sizeof(CEnt);
   L.wheel_per_slot = (size_t)max_nd(lays, n_layouts) * L.nb;
   size_t rw = (size_t)resident_warps(L.smem);
   L.n_slots = (uint32_t)(n < rw ? (n < 1 ? 1 : n) : rw);
@@ -332,26 +320,16 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
     L.ring_c_off = align256(L.ring_e_off + (size_t)L.n_slots * L.ring_nd * L.ring_r * sizeof(double));
     L.total = L.ring_c_off + (size_t)L.n_slots * L.ring_nd * L.ring_r * sizeof(uint32_t);
   }
-#if VT_UTAB
   L.utab_off = align256(L.total);
   L.total = L.utab_off + (size_t)MAX_PROFILES * 2 * SIM_UTAB * sizeof(double);
-#endif
-#if VT_SPLIT_A
+  // request nodes, written by K4a and read by K4b: one 16-B node per request per scenario
+  const uint64_t nodes = total_requests ? total_requests : (uint64_t)(n < 1 ? 1 : n) * tr->max_requests;
   L.nodes_off = align256(L.total);
-  L.total = L.nodes_off + align256((size_t)(n < 1 ? 1 : n) * tr->max_requests * 16);
+  L.total = L.nodes_off + align256((size_t)(nodes < 1 ? 1 : nodes) * 16);
   L.pares_off = L.total;
   L.total = L.pares_off + align256((size_t)(n < 1 ? 1 : n) * VOLTANA_MAX_INSTANCES * sizeof(PaRes));
   L.rtab_off = L.total;
   L.total = L.rtab_off + (size_t)MAX_GRIDS * MAX_PROFILES * RT_STRIDE * sizeof(double);
-#if VT_DEFER_ITL
-  // completion log: at most one entry per routed request of the scenario
-  L.clog_off = align256(L.total);
-  L.total = L.clog_off + align256((size_t)(n < 1 ? 1 : n) * (tr->max_requests + 2 * VOLTANA_MAX_INSTANCES * CLOG_CHUNK) *
-                                   sizeof(CEnt));
-  L.clog_n_off = L.total;
-  L.total = L.clog_n_off + align256((size_t)(n < 1 ? 1 : n) * sizeof(uint32_t));
-#endif
-#endif
   return L;
 }
 
@@ -365,11 +343,16 @@ void table_extent(const voltana_grid *grids, int n_grids, const voltana_profile 
 
 }  // namespace
 
-size_t voltana_simulate_workspace_bytes(const voltana_traces *traces_h, const voltana_layout *layouts_h,
-                                        int n_layouts, size_t n_scenarios) {
+size_t voltana_simulate_workspace_bytes_ex(const voltana_traces *traces_h, const voltana_layout *layouts_h,
+                                           int n_layouts, size_t n_scenarios, uint64_t total_requests) {
   if (!traces_h || !layouts_h || n_layouts < 1) return 0;
   // conservative table extent (ITL table staged in shared memory or not does not change the size)
-  return sim_layout(traces_h, layouts_h, n_layouts, VOLTANA_MAX_LEVELS, 64, n_scenarios).total;
+  return sim_layout(traces_h, layouts_h, n_layouts, VOLTANA_MAX_LEVELS, 64, n_scenarios, total_requests).total;
+}
+
+size_t voltana_simulate_workspace_bytes(const voltana_traces *traces_h, const voltana_layout *layouts_h,
+                                        int n_layouts, size_t n_scenarios) {
+  return voltana_simulate_workspace_bytes_ex(traces_h, layouts_h, n_layouts, n_scenarios, 0);
 }
 
 voltana_status voltana_simulate(const voltana_traces *traces_h, const voltana_slo *slos_h, int n_slos,
@@ -403,11 +386,13 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   if (n_grids < 1 || n_grids > MAX_GRIDS) return fail(VOLTANA_E_INVALID_ARG, "simulate: n_grids=%d (1..16)", n_grids);
   if (n_profiles < 1 || n_profiles > MAX_PROFILES)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: n_profiles=%d (1..8)", n_profiles);
-  if (n > 0xffffffffull) return fail(VOLTANA_E_INVALID_ARG, "simulate: n=%zu too large", n);
+  if (n > 0x7fffffffull) return fail(VOLTANA_E_INVALID_ARG, "simulate: n=%zu too large", n);
   if (traces_h->max_requests > 0x7ffffffeull)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_requests too large");
   if (traces_h->max_out < 1 || traces_h->max_out > 65535)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_out=%u outside 1..65535", traces_h->max_out);
+  if (scen_h->node_offset && scen_h->total_requests == 0 && n > 0)
+    return fail(VOLTANA_E_INVALID_ARG, "simulate: scenarios.total_requests must be node_offset[n] (> 0)");
   voltana_status s;
   for (int i = 0; i < n_slos; ++i) {
     const voltana_slo &x = slos_h[i];
@@ -460,10 +445,23 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   bool fast = (size_t)kmax * tmax * 24 <= SIM_ITL_SMEM_MAX && kmax <= 8;
   for (int i = 0; i < n_profiles; ++i)
     fast = fast && (profiles_h[i].tile_w & (profiles_h[i].tile_w - 1)) == 0 && profiles_h[i].n_ptiles <= 1;
-  SimLayout L = sim_layout(traces_h, layouts_h, n_layouts, kmax, tmax, n, fast);
-  const size_t need = voltana_simulate_workspace_bytes(traces_h, layouts_h, n_layouts, n);
+  const uint64_t total_req = scen_h->node_offset ? scen_h->total_requests : 0;
+  SimLayout L = sim_layout(traces_h, layouts_h, n_layouts, kmax, tmax, n, total_req, fast);
+  const size_t need = voltana_simulate_workspace_bytes_ex(traces_h, layouts_h, n_layouts, n, total_req);
   if (!workspace || ws_bytes < need || ws_bytes < L.total)
     return fail(VOLTANA_E_WORKSPACE, "simulate: workspace %zu < %zu bytes", ws_bytes, need);
+  int v = 0;  // variant bits of the instantiation: 1 energy scoring, 2 light variants / outputs
+  for (int i = 0; i < n_layouts; ++i) {
+    const voltana_layout &x = layouts_h[i];
+    if (x.policy == 2 || x.ctrl_mode != 0) v |= 1;
+    if (x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 || x.exec_noise != nullptr || x.itl_mode != 0) v |= 2;
+  }
+  if (outputs_h && (outputs_h->req_offset != nullptr || outputs_h->iter_offset != nullptr)) v |= 2;  // E1-E2
+  // every kernel attribute is set before anything of this call is enqueued: a non-OK return
+  // below this point is a launch failure (VOLTANA_E_CUDA), the only partial-enqueue case
+  cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(v, fast), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)L.smem);
+  if (e != cudaSuccess) return cuda_fail(e, "simulate kernel attribute");
 
   static_assert(sizeof(SimParams) < 32000, "kernel parameter block too large");
   SimParams *P = new SimParams;
@@ -472,6 +470,7 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->offset = traces_h->offset; P->duration = traces_h->duration_ms;
   P->trace_id = scen_h->trace_id; P->slo_id = scen_h->slo_id; P->layout_id = scen_h->layout_id;
   P->grid_id = scen_h->grid_id; P->profile_id = scen_h->profile_id; P->hash_seed = scen_h->hash_seed;
+  P->node_offset = scen_h->node_offset;
   P->n = (uint32_t)n; P->nb = L.nb; P->max_out = traces_h->max_out; P->out = out;
   P->n_slots = L.n_slots;
   P->n_slos = (uint32_t)n_slos; P->n_layouts = (uint32_t)n_layouts; P->n_grids = (uint32_t)n_grids;
@@ -482,7 +481,7 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->counter = (uint32_t *)ws;
   P->slots = ws + L.slots_off;
   P->slot_bytes = L.slot;
-  P->node_bytes = L.node;
+  P->far_bytes = L.far;
   P->wheels = (uint4 *)(ws + L.wheels_off);
   if (L.ring_r) {
     P->ring_e = (double *)(ws + L.ring_e_off);
@@ -490,29 +489,16 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     P->ring_r = L.ring_r;
     P->ring_nd = L.ring_nd;
   }
-#if VT_UTAB
   P->utab = (const double *)(ws + L.utab_off);
-#endif
-#if VT_SPLIT_A
   P->nodes = ws + L.nodes_off;
   P->pares = (PaRes *)(ws + L.pares_off);
   P->rtab = (double *)(ws + L.rtab_off);
-#if VT_DEFER_ITL
-  P->clog = (CEnt *)(ws + L.clog_off);
-  P->clog_n = (uint32_t *)(ws + L.clog_n_off);
-  P->clog_stride = tr_stride_clog(traces_h);
   P->ks_off = L.ks_off;
-#endif
   P->np_max = 1;
   for (int i = 0; i < n_layouts; ++i) P->np_max = (uint32_t)layouts_h[i].n_p > P->np_max ? layouts_h[i].n_p : P->np_max;
-#ifdef VT_PA_SPREAD
-  P->np_max = P->np_max < VT_PA_SPREAD ? VT_PA_SPREAD : P->np_max;  // experiment: threads per scenario in K4a
-#endif
-#endif
   P->wheel_per_slot = L.wheel_per_slot;
   P->itl_smem = L.itl_smem;
   P->smem_per_warp = (uint32_t)L.smem_per_warp;
-  P->sw_off = L.sw_off;
   P->timing = g_debug_timing;
   for (int i = 0; i < n_slos; ++i) P->slo[i] = slos_h[i];
   for (int i = 0; i < n_layouts; ++i) P->lay[i] = layouts_h[i];
@@ -520,43 +506,24 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   for (int i = 0; i < n_profiles; ++i) P->prof[i] = to_dev(profiles_h[i]);
   cudaStream_t st = (cudaStream_t)stream;
   // scenario counter = 0; every wheel bucket empty (buckets are left clean after use)
-  cudaError_t e = cudaMemsetAsync(P->counter, 0, 4 * sizeof(uint32_t), st);
+  e = cudaMemsetAsync(P->counter, 0, 4 * sizeof(uint32_t), st);
   if (e == cudaSuccess)
     e = cudaMemsetAsync(P->wheels, 0, (size_t)L.n_slots * L.wheel_per_slot * sizeof(uint4), st);
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate memset"); }
-  const int per_cta = (SIM_THREADS / 32) * SPW;
+  const int per_cta = SIM_THREADS / 32;
   const int grid = (int)((L.n_slots + per_cta - 1) / per_cta);
-  int v = 0;  // variant bits of the instantiation: 1 energy scoring, 2 light variants / outputs
-  for (int i = 0; i < n_layouts; ++i) {
-    const voltana_layout &x = layouts_h[i];
-    if (x.policy == 2 || x.ctrl_mode != 0) v |= 1;
-    if (x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 || x.exec_noise != nullptr || x.itl_mode != 0) v |= 2;
-  }
-  if (P->o.req_offset != nullptr || P->o.iter_offset != nullptr) v |= 2;  // outputs (E1-E2)
-#if VT_UTAB || VT_SPLIT_A
   e = launch_utab(*P, st);  // setup: utilisation table and ladder-resolved prefill rows
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate setup launch"); }
-#endif
-#if VT_SPLIT_A
   e = launch_prefill(*P, v, fast, st);  // K4a: every prefill timeline of every scenario
   if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate prefill launch"); }
-#endif
   if (g_split_event) {
     e = cudaEventRecord((cudaEvent_t)g_split_event, st);
     if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate split event"); }
   }
-  e = launch_sim(*P, v, fast, grid, L.smem, st);
-  if (e != cudaSuccess) { delete P; return cuda_fail(e, "simulate launch"); }
-  int k4c = 0;
-#if VT_SPLIT_A && VT_DEFER_ITL && !VT_ITL_INWARP
-  if (!(v & 2)) {  // K4c: the decode ITL accounting the paper's-policy kernels deferred
-    e = launch_itl(*P, st);
-    k4c = 1;
-  }
-#endif
+  e = launch_sim(*P, v, fast, grid, L.smem, st);  // K4b: routing + decode, ITL pass in-warp
   delete P;
-  if (e != cudaSuccess) return cuda_fail(e, "simulate itl launch");
-  g_launches = 1 + ((VT_UTAB || VT_SPLIT_A) ? 1 : 0) + (VT_SPLIT_A ? 1 : 0) + k4c;
+  if (e != cudaSuccess) return cuda_fail(e, "simulate launch");
+  g_launches = 3;
   return ok();
 }
 

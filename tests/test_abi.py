@@ -124,17 +124,24 @@ def test_product_has_no_cpu_fallback():
 
 
 def test_simulate_workspace_grows_with_requests(vt):
-    """The split K4 keeps, per scenario, a 16-B request node (K4a -> K4b) and a 16-B
-    completion-log slot per request: the workspace bound grows by >= 32 B per (scenario,
-    request) of max_requests (voltana.h, voltana_simulate)."""
+    """K4 keeps one 16-B request node per request of every scenario (K4a -> K4b): n x
+    max_requests x 16 B without node offsets, total_requests x 16 B with them; everything else
+    is per resident warp (voltana.h, voltana_simulate_workspace_bytes[_ex])."""
     L = vt.lib()
     lib = vt._lib
     lays = (lib.Layout * 1)(lib.Layout(2, 2, 0, 150, 8192, 400000, 0.0))
 
-    def ws(n, mr):
+    def ws(n, mr, total=None):
         tr = lib.Traces(1, 1, 1, 1, 1, 1, mr, 100, 0)
-        return int(L.voltana_simulate_workspace_bytes(C.byref(tr), lays, 1, n))
+        if total is None:
+            return int(L.voltana_simulate_workspace_bytes(C.byref(tr), lays, 1, n))
+        return int(L.voltana_simulate_workspace_bytes_ex(C.byref(tr), lays, 1, n, total))
 
-    assert ws(100, 2000) - ws(100, 1000) >= 100 * 1000 * 32
-    assert ws(200, 1000) - ws(100, 1000) >= 100 * 1000 * 32
-    assert ws(4096, 45412) >= 4096 * 45412 * 32
+    assert ws(100, 2000) - ws(100, 1000) >= 100 * 1000 * 16
+    assert ws(20000, 1000) - ws(10000, 1000) >= 10000 * 1000 * 16
+    assert ws(4096, 45412) >= 4096 * 45412 * 16
+    # node offsets: the node region is exactly 16 B per request of the sweep (to 256-B alignment)
+    d = ws(4096, 45412, 90_000_000) - ws(4096, 45412, 80_000_000)
+    assert abs(d - 10_000_000 * 16) <= 512
+    assert ws(4096, 45412, 89_000_000) < ws(4096, 45412) - 4096 * 45412 * 16 + 89_000_000 * 16 + 1024
+    assert ws(4096, 45412) == ws(4096, 45412, 0)

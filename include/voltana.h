@@ -11,8 +11,10 @@
  *    the library never allocates device memory; scratch comes from a caller workspace.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream). All device work is
  *    enqueued asynchronously on it; pointers must stay valid until it completes.
- *  - Host-side validation is synchronous: a non-OK return means NOTHING was enqueued;
- *    voltana_last_error_detail() names the offending argument.
+ *  - Host-side validation is synchronous: a non-OK return other than VOLTANA_E_CUDA means
+ *    NOTHING was enqueued; voltana_last_error_detail() names the offending argument.
+ *    VOLTANA_E_CUDA is a launch/runtime failure and may follow a partial enqueue (earlier
+ *    memsets or kernels of the same call); kernel attributes are set before any enqueue.
  *  - Problems found on the device are reported per item (status bytes / result.status),
  *    never by aborting the batch.
  *  - Arithmetic: IEEE fp64, every operation rounded separately, no FMA contraction

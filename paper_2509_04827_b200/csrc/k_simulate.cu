@@ -151,6 +151,36 @@ __device__ int lowest_itl(const WS &W, uint32_t n, uint32_t kv, double target, d
   return K - 1;
 }
 
+// The same lowest feasible level, searched from a start level k0 (the instance's previous
+// decision): on coefficient-monotone tables (A32) the feasible levels are upward closed, so a
+// walk down from a feasible k0 (or up from an infeasible one) stops at the scan's answer —
+// usually after one or two evaluations instead of up to K.
+template <bool F, class WS>
+__device__ __forceinline__ int lowest_itl_from(const WS &W, uint32_t n, uint32_t kv, double target, int k0,
+                                               double *pred) {
+  const int K = (int)W.K;
+  if (!W.mono_it || K < 3) return lowest_itl<F>(W, n, kv, target, pred);
+  const uint32_t j = tile_j<F>(W, n);
+  const double dn = (double)n, dkv = (double)kv;
+  int k = k0 < K - 2 ? k0 : K - 2;
+  double p = itl_at<F>(W, j, k, dn, dkv);
+  if (p <= target) {
+    while (k > 0) {
+      const double q = itl_at<F>(W, j, k - 1, dn, dkv);
+      if (!(q <= target)) break;
+      --k;
+      p = q;
+    }
+  } else {
+    do {
+      ++k;
+      p = itl_at<F>(W, j, k, dn, dkv);
+    } while (k < K - 1 && !(p <= target));
+  }
+  *pred = p;
+  return k;
+}
+
 // busy power (eq:P-f P:187, A22) with the utilisation from the launch's table (the entries
 // are the same division, so the value is identical)
 __device__ __forceinline__ double bpow_u(const double *ut, double p_idle, double tdp, double uh, int phase, double dyn,
@@ -214,6 +244,7 @@ struct Err {               // first error of one lane in its own event order
 
 struct Dec {               // decode instance d, owned by lane d
   uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both, far_h, far_hfin;
+  int klast;               // the last EcoFreq level found by the search (start of the next one)
   uint32_t lpos, lend;     // this lane's chunk [lpos, lend) of the completion log
   bool busy, dead, lneed;  // lneed: the chunk is full, dec_advance stopped before an END
   double end, ebusy, bms, top, sitl, tlast;
@@ -385,7 +416,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       fl |= 1u;
       if (backlog) { k = (int)W.K - 1; dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
       else if ((V & 1) && W.ctrl) k = energy_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
-      else k = lowest_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);
+      else { k = lowest_itl_from<F>(W, D.nreq, D.nkv, W.tgt_itl, D.klast, &dur); D.klast = k; }
       D.h = fold(D.h, 2, (uint64_t)d, (uint64_t)k, 0);
       if ((V & 2) && W.wo) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
     }
@@ -544,8 +575,7 @@ __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, doub
                                          uint32_t out, uint32_t nbm) {
   D.pn += 1u;
   D.pkv += in + 1u;
-  L.node[i].next = NIL;
-  if (D.qt == NIL) {
+  if (D.qt == NIL) {  // (K4a wrote node i with next = NIL)
     D.qh = i;
     prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // its bucket at the next START
     D.qhn.tf = tf; D.qhn.next = NIL; D.qhn.in = (uint16_t)in; D.qhn.out = (uint16_t)out;
@@ -671,51 +701,64 @@ __device__ __noinline__ uint32_t route_refill(RouteWin &R, const Node *node, uin
 
 // EcoRoute's case analysis (A13-A17) from the feasibility ballot of the what-if
 // lanes (bit 2Kd + k: level k feasible for instance d now; bit 2Kd + K + k: after adding the
-// request). Every lane computes the same decision; MHz from the staged ladder.
-__device__ __forceinline__ void eco_cases(unsigned fm, int ND, int K, const int32_t *mhz, int32_t delta,
-                                          uint32_t &cursor, int &dsel, int &cse) {
+// request). Every lane computes the same decision; MHz from the staged ladder. ND is a
+// template parameter so the per-instance loops are straight-line code.
+template <int ND>
+__device__ __forceinline__ void eco_cases_nd(unsigned fm, int K, const int32_t *mhz, int32_t delta,
+                                             uint32_t &cursor, int &dsel, int &cse) {
   const unsigned km = (1u << K) - 1u;
-  int fn[NI], fa[NI];
-  int mnAll = 0x7fffffff, mnU = 0x7fffffff, maR = 0x7fffffff, maAll = 0x7fffffff;
-  unsigned Rm = 0u;
+  int fn[ND], fa[ND];
 #pragma unroll
-  for (int d = 0; d < NI; ++d) {
-    fn[d] = fa[d] = 0x7fffffff;
-    if (d >= ND) continue;
+  for (int d = 0; d < ND; ++d) {
     const unsigned cm = (fm >> (2 * K * d)) & km, am = (fm >> (2 * K * d + K)) & km;
     fn[d] = mhz[cm ? ffs0(cm) : K - 1];   // f: lowest feasible level now (A10, A11)
     fa[d] = mhz[am ? ffs0(am) : K - 1];   // f': after the hypothetical addition (A12)
+  }
+  int mnAll = fn[0], maAll = fa[0], mnU = 0x7fffffff, maR = 0x7fffffff;
+  unsigned Rm = 0u;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
     if (fa[d] > fn[d]) { Rm |= 1u << d; maR = fa[d] < maR ? fa[d] : maR; }   // crossed (A13)
     else mnU = fn[d] < mnU ? fn[d] : mnU;
     mnAll = fn[d] < mnAll ? fn[d] : mnAll;
     maAll = fa[d] < maAll ? fa[d] : maAll;
   }
-  unsigned inset = 0u;
-  const unsigned all = (1u << ND) - 1u;
-  if (Rm == 0u) {            // nobody crosses: the lowest current frequency, unique (1) or tied (2)
-#pragma unroll
-    for (int d = 0; d < NI; ++d) if (d < ND && fn[d] == mnAll) inset |= 1u << d;
-    cse = __popc(inset) == 1 ? 1 : 2;
+  constexpr unsigned all = (1u << ND) - 1u;
+  // candidate set: argmin of f over U (3), over everybody (1, 2, 4), or of f' (5)
+  int key = mnAll;
+  bool use_fa = false, only_u = false;
+  if (Rm == 0u) {
+    cse = 1;                 // nobody crosses: the lowest current frequency (1 unique, 2 tied)
   } else if (Rm != all) {    // some cross: the gap decides (A14, A15)
-    const long long g = (long long)mnU - (long long)maR;
-    if (g <= (long long)delta) {
-#pragma unroll
-      for (int d = 0; d < NI; ++d) if (d < ND && !((Rm >> d) & 1u) && fn[d] == mnU) inset |= 1u << d;
-      cse = 3;
-    } else {
-#pragma unroll
-      for (int d = 0; d < NI; ++d) if (d < ND && fn[d] == mnAll) inset |= 1u << d;
-      cse = 4;
-    }
+    if ((long long)mnU - (long long)maR <= (long long)delta) { key = mnU; only_u = true; cse = 3; }
+    else cse = 4;
   } else {                   // everybody crosses: the lowest new frequency
-#pragma unroll
-    for (int d = 0; d < NI; ++d) if (d < ND && fa[d] == maAll) inset |= 1u << d;
-    cse = 5;
+    key = maAll; use_fa = true; cse = 5;
   }
+  unsigned inset = 0u;
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    const int v = use_fa ? fa[d] : fn[d];
+    if (v == key && !(only_u && ((Rm >> d) & 1u))) inset |= 1u << d;
+  }
+  if (cse == 1 && __popc(inset) > 1) cse = 2;
   // round robin among the candidate set from the cursor (A17)
   const unsigned rot = ((inset >> cursor) | (inset << (ND - (int)cursor))) & all;
   dsel = (int)wrap_nd(cursor + (uint32_t)ffs0(rot), (uint32_t)ND);
   if (__popc(inset) >= 2) cursor = wrap_nd((uint32_t)dsel + 1u, (uint32_t)ND);
+}
+
+__device__ __forceinline__ void eco_cases(unsigned fm, int ND, int K, const int32_t *mhz, int32_t delta,
+                                          uint32_t &cursor, int &dsel, int &cse) {
+  switch (ND) {
+    case 2: eco_cases_nd<2>(fm, K, mhz, delta, cursor, dsel, cse); break;
+    case 3: eco_cases_nd<3>(fm, K, mhz, delta, cursor, dsel, cse); break;
+    case 4: eco_cases_nd<4>(fm, K, mhz, delta, cursor, dsel, cse); break;
+    case 5: eco_cases_nd<5>(fm, K, mhz, delta, cursor, dsel, cse); break;
+    case 6: eco_cases_nd<6>(fm, K, mhz, delta, cursor, dsel, cse); break;
+    case 7: eco_cases_nd<7>(fm, K, mhz, delta, cursor, dsel, cse); break;
+    default: eco_cases_nd<8>(fm, K, mhz, delta, cursor, dsel, cse); break;
+  }
 }
 
 // ------------------------------------------------------------------ K4a: prefill instance p
@@ -788,11 +831,19 @@ __device__ int energy_ttft(const PCtxS &C, uint32_t nbt, double budget, double *
   return best;
 }
 
-struct PState {   // uniform state of one prefill instance (every lane holds the same values)
+struct PState {   // uniform state of one prefill instance (every lane holds the same values) ...
   double ebusy, bms, top, sttft, tlast, errt, tfree, last;
   uint64_t h;
   uint32_t iters, ttft_ok, itl_ok, both, errc, cur, ndec;
+  uint64_t tok;   // ... except the input checks of the requests this lane accounted (A40)
+  bool vok;
 };
+
+// Input checks of request i (A40): 1 <= in <= 65535, 1 <= out <= max_out, 0 <= arrival < 1e9,
+// arrivals non-decreasing (prev = arrival of request i - 1).
+__device__ __forceinline__ bool req_ok(double a, uint32_t x, uint32_t o, uint32_t max_out, uint32_t i, double prev) {
+  return x >= 1u && x <= 65535u && o >= 1u && o <= max_out && a >= 0.0 && a < 1e9 && !(i > 0u && a < prev);
+}
 
 // O7 decision for a batch of nbt tokens starting at ts, head arrival a0: EcoFreq,
 // duration, energy (A23). false: per-item error recorded in S.
@@ -840,12 +891,18 @@ __device__ __forceinline__ bool pa_decide(const SimParams &P, const PCtxS &C, PS
 
 // O5 for lanes [0, n): request base + lane*NP (arrival a, in x, out o) finished prefill at e.
 template <int V>
-__device__ __forceinline__ void pa_account(const SimParams &P, PCtxS &C, PState &S, Node *node, uint32_t base,
-                                           uint32_t NP, uint32_t n, double e, double a, uint32_t x, uint32_t o) {
+__device__ __forceinline__ void pa_account(const SimParams &P, PCtxS &C, PState &S, Node *node, const double *arr,
+                                           uint32_t base, uint32_t NP, uint32_t n, double e, double a, uint32_t x,
+                                           uint32_t o) {
   if (n == 0u) return;
   const uint32_t lane = threadIdx.x & 31u;
   const bool valid = lane < n;
   const uint32_t i = base + lane * NP;
+  if (valid) {  // every request is accounted exactly once: its input checks (A40)
+    const double prev = i > 0u ? arr[i - 1u] : 0.0;
+    S.vok = S.vok && req_ok(a, x, o, P.max_out, i, prev);
+    S.tok += (uint64_t)x + o;
+  }
   const double ttft = valid ? sub(e, a) : 0.0;  // A26
   const bool ok = valid && ttft <= C.slo_ttft;
   __syncwarp();
@@ -924,7 +981,7 @@ __device__ uint32_t pa_batch_general(const SimParams &P, PCtxS &C, PState &S, No
     double a = 0.0;
     uint32_t x = 0u, o = 0u;
     if (lane < nv) { a = arr[i]; x = inl[i]; o = outl[i]; }
-    pa_account<V>(P, C, S, node, nxt + q0 * NP, NP, nv, end, a, x, o);
+    pa_account<V>(P, C, S, node, arr, nxt + q0 * NP, NP, nv, end, a, x, o);
   }
   return id;
 }
@@ -955,6 +1012,8 @@ __device__ void prefill_warp(const SimParams &P, PCtxS &C, Node *node, const dou
   S.h = h0;
   S.iters = S.ttft_ok = S.itl_ok = S.both = S.errc = S.ndec = 0;
   S.cur = C.K - 1u;          // [C2] running level (starts at the top)
+  S.tok = 0;
+  S.vok = true;
   uint32_t wbase = p;        // request of lane 0 in the window (the instance's next unbatched request)
   uint32_t pf2 = p;          // next entry to prefetch into L2
   while (wbase < N) {
@@ -1005,7 +1064,7 @@ __device__ void prefill_warp(const SimParams &P, PCtxS &C, Node *node, const dou
       if (lane >= hl && lane < f) e = end;
       hl = f;
     }
-    pa_account<V>(P, C, S, node, wbase, NP, hl, e, a, x, o);  // O5 for the window's batches
+    pa_account<V>(P, C, S, node, arr, wbase, NP, hl, e, a, x, o);  // O5 for the window's batches
     wbase += hl * NP;
     if (err) break;
     if (general) {
@@ -1014,9 +1073,19 @@ __device__ void prefill_warp(const SimParams &P, PCtxS &C, Node *node, const dou
       wbase = nx;
     }
   }
+  // the requests after an error were not accounted: their input checks (A40)
+  for (uint32_t i = wbase + lane * NP; i < N; i += 32u * NP) {
+    const uint32_t x = inl[i], o = outl[i];
+    S.vok = S.vok && req_ok(arr[i], x, o, P.max_out, i, i > 0u ? arr[i - 1u] : 0.0);
+    S.tok += (uint64_t)x + o;
+  }
+  uint64_t tok = S.tok;
+  for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(FULL, tok, o);
   R.ebusy = S.ebusy; R.bms = S.bms; R.top = S.top; R.sttft = S.sttft; R.tlast = S.tlast; R.errt = S.errt;
   R.h = S.h; R.iters = S.iters; R.ttft_ok = S.ttft_ok; R.itl_ok = S.itl_ok; R.both = S.both; R.errc = S.errc;
-  R.ndec = S.ndec; R.send = wbase < N ? wbase : N; R.pad = 0;
+  R.ndec = S.ndec; R.send = wbase < N ? wbase : N;
+  R.valid = __all_sync(FULL, S.vok) ? 1u : 0u;
+  R.tok = tok;
   if ((V & 2) && C.it_on && lane == 0) P.o.iter_count[C.it_base / P.o.iter_cap + p] = S.iters;
 }
 
@@ -1116,23 +1185,18 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const uint64_t off = P.offset[tr];
   const uint64_t N64 = P.offset[tr + 1] - off;
   const double Dur = P.duration[tr];
-  const double *arr = P.arrival + off;
-  const uint32_t *inl = P.in_len + off;
-  const uint32_t *outl = P.out_len + off;
 
   // ---------------------------------------------------------------- device validation (A40)
+  // the per-request checks ran in K4a (each prefill warp over its stream); here their results
+  const int NP = LY.n_p, ND = LY.n_d;
   uint32_t tok_total;
   {
     bool ok = N64 <= P.max_requests && Dur >= 0.0 && node_range_ok(P, s, N64);
     uint64_t tok = 0;
-    if (ok) {
-      for (uint64_t i = lane; i < N64; i += 32u) {
-        const uint32_t a = inl[i], b = outl[i];
-        const double x = arr[i];
-        ok = ok && a >= 1u && a <= 65535u && b >= 1u && b <= P.max_out && x >= 0.0 && x < 1e9;
-        if (i > 0) ok = ok && !(x < arr[i - 1]);
-        tok += (uint64_t)a + b;
-      }
+    if (ok && lane < NP) {
+      W.pa[lane] = P.pares[(size_t)s * NI + lane];
+      ok = W.pa[lane].valid != 0u;
+      tok = W.pa[lane].tok;
     }
     for (int o = 16; o > 0; o >>= 1) tok += __shfl_xor_sync(FULL, tok, o);
     ok = __all_sync(FULL, ok) && tok <= 0x7fffffffull;
@@ -1143,7 +1207,6 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     tok_total = (uint32_t)tok + 2u;
   }
   const uint32_t N = (uint32_t)N64;
-  const int NP = LY.n_p, ND = LY.n_d;
   uint64_t rq_base = 0, it_base = 0;
   bool rq_on = false;
   if ((V & 2) && P.o.req_offset) {  // per-request range: empty (skip) or exactly the trace (E1)
@@ -1219,7 +1282,6 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const uint64_t h0 = P.hash_seed[s];
   // ================================================================ PHASE A results (K4a)
   if (lane < NP) {
-    W.pa[lane] = P.pares[(size_t)s * NI + lane];
     W.rw.sbase[lane] = (uint32_t)lane;
     W.rw.send[lane] = W.pa[lane].send;
   }
@@ -1235,6 +1297,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   if (lane == 0) W.clog_m = (uint32_t)ND * CLOG_CHUNK;  // the first chunk of every decode lane
   Dec D;
   D.nreq = D.nkv = D.pn = D.pkv = D.iters = D.cur = 0;
+  D.klast = 0;
   D.qh = D.qt = NIL;
   D.far_h = D.far_hfin = NIL;
   D.busy = false;
@@ -1263,10 +1326,14 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const bool ens = (V & 1) && LY.policy == 2 && ND > 1;
   const bool wif = F && eco && (uint32_t)ND * 2u * K <= 32u;   // the lane-parallel what-if
   const int32_t delta = LY.delta_mhz;
-  // what-if lane (fast path): instance wd, state ws (0 now, 1 after), level wk
-  const uint32_t wd = (uint32_t)lane / (2u * K), wr = (uint32_t)lane - wd * 2u * K;
-  const uint32_t ws = wr >= K ? 1u : 0u, wk = ws ? wr - K : wr;
-  const bool wact = wif && wd < (uint32_t)ND;
+  // what-if lane (fast path): instance wd, state ws (0 now, 1 after), level wk, packed
+  // wk | ws << 8 | wd << 16 (NIL: an idle lane)
+  uint32_t wpk = NIL;
+  {
+    const uint32_t wd = (uint32_t)lane / (2u * K), wr = (uint32_t)lane - wd * 2u * K;
+    const uint32_t ws = wr >= K ? 1u : 0u, wk = ws ? wr - K : wr;
+    if (wif && wd < (uint32_t)ND) wpk = wk | ws << 8 | wd << 16;
+  }
 #ifdef VT_LAT_PROBE
   // experiment: clock64 cycles per phase of the route loop, summed over the scenario
   // [0] window read / refill, [1] decode advance, [2] EcoRoute + push, [3] drain + ITL pass
@@ -1277,42 +1344,44 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #endif
   uint32_t rcnt = route_refill(W.rw, node, (uint32_t)NP), rpos = 0;
   for (;;) {
-    // the next request of the merged stream; none left: the drain (t = +inf)
-    bool fin = false;
-    if (rpos == rcnt) {
-      if (rcnt < 32u) {
-        fin = true;  // every stream is exhausted
-      } else {
+    // the next request of the merged stream; none left: the drain marker (t = +inf, io = 0)
+    RouteEnt e;
+    if (rpos < rcnt) {
+      e = W.rw.ring[rpos++];
+    } else {
+      if (rcnt == 32u) {  // a full window was consumed: the streams may hold more
         rcnt = route_refill(W.rw, node, (uint32_t)NP);
         rpos = 0;
-        fin = rcnt == 0u;
+      }
+      if (rpos < rcnt) {
+        e = W.rw.ring[rpos++];
+      } else {
+        e.tf = INF; e.id = NIL; e.io = 0u;
       }
     }
-    RouteEnt e;
-    e.tf = INF; e.id = NIL; e.io = 0u;
-    if (!fin) e = W.rw.ring[rpos++];
     const uint32_t out_i = e.io >> 16;
-    if (!fin && out_i == 1u) continue;              // first token from prefill: not routed (A8)
-    if (steps_route > N) { dE.t = 0.0; dE.code = VOLTANA_ITEM_E_INTERNAL; fin = true; e.tf = INF; }  // watchdog
+    if (out_i == 1u) continue;                      // first token from prefill: not routed (A8)
     const double t = fabs(e.tf);
-    const uint32_t i = e.id;
-    const uint32_t in_i = e.io & 0xffffu;
     LP_MARK(0);
     // decode instances catch up to t: events strictly before t (PrefillDone drains first);
-    // t = +inf runs every instance to completion
+    // the drain marker (t = +inf) runs every instance to completion
     if (t != t_adv) {  // routes of one batch share t: nothing new happens between them
       dec_advance_all<V, F>(D, lane, L, W, t, dE, P.o, ND, S, k_sd, k_ok, k_both);
       t_adv = t;
+      if (e.io == 0u) break;
     }
-    if (fin) break;
+    const uint32_t i = e.id;
+    const uint32_t in_i = e.io & 0xffffu;
     LP_MARK(1);
     // ---- O8 EcoRoute
     int dsel, cse;
     if (wif) {   // one lane per (instance, state, level): the whole what-if in one ballot
       const uint32_t en = D.nreq + D.pn, ek = D.nkv + D.pkv;   // A9 effective state (lane d)
-      const uint32_t n0 = wshfl(en, (int)(wact ? wd : 0u)), kv0 = wshfl(ek, (int)(wact ? wd : 0u));
+      const int src = (int)((wpk >> 16) & 0xffu);
+      const uint32_t n0 = wshfl(en, src & 31), kv0 = wshfl(ek, src & 31);
       bool feas = false;
-      if (wact) {
+      if (wpk != NIL) {
+        const uint32_t ws = (wpk >> 8) & 1u, wk = wpk & 0xffu;
         const uint32_t n = n0 + ws, kv = kv0 + (ws ? in_i + 1u : 0u);   // A12
         if (n == 0u) feas = wk == 0u;                                   // n = 0 -> level 0 (A11)
         else feas = itl_at<F>(W, tile_j<F>(W, n), (int)wk, (double)n, (double)kv) <= W.tgt_itl;

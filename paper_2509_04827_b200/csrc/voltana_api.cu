@@ -391,8 +391,6 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_requests too large");
   if (traces_h->max_out < 1 || traces_h->max_out > 65535)
     return fail(VOLTANA_E_INVALID_ARG, "simulate: traces.max_out=%u outside 1..65535", traces_h->max_out);
-  if (scen_h->node_offset && scen_h->total_requests == 0 && n > 0)
-    return fail(VOLTANA_E_INVALID_ARG, "simulate: scenarios.total_requests must be node_offset[n] (> 0)");
   voltana_status s;
   for (int i = 0; i < n_slos; ++i) {
     const voltana_slo &x = slos_h[i];

@@ -28,7 +28,8 @@ struct PaRes {     // phase-A result of one prefill instance (K4a -> K4b; the re
   uint64_t h;                                  // decision-hash chain (A36)
   uint32_t iters, ttft_ok, itl_ok, both, errc, ndec;
   uint32_t send;   // stream end: the first request id of this instance whose node was not written
-  uint32_t pad;
+  uint32_t valid;  // every request of this instance's stream passed the input checks (A40)
+  uint64_t tok;    // sum of in + out over the stream (A40: the scenario total must be < 2^31)
 };
 
 // Completion log (K4b -> its in-warp ITL pass): one 16-B entry per decode iteration end with

@@ -11,16 +11,7 @@
 #include "vt_decide.h"
 #include "vt_device.cuh"
 
-#ifndef VT_ITS4
-#define VT_ITS4 0            // K2/K3 ITL rows padded to 4 doubles, a2+b2 in one LDS.128 (measured: K2 66 -> 51 %, K3 30 -> 29 %: off)
-#endif
-constexpr int ITS = VT_ITS4 ? 4 : 3;
-#ifndef VT_DECIDE_ILP
-#define VT_DECIDE_ILP 1      // K2/K3 with K <= 8: branch-free level evaluation
-#endif
-#ifndef VT_ROUTE_LOCKSTEP
-#define VT_ROUTE_LOCKSTEP 0  // K3: the 2*N_D what-if scans of an item advance in lockstep over the levels
-#endif
+constexpr int ITS = 3;       // ITL rows {a2, b2, c2} per (tile, level)
 
 namespace vt {
 
@@ -68,7 +59,6 @@ __device__ void stage_tables(const DevProfile &PR, const LadderParam &LP, bool n
       int j = x / K, k = x - j * K;
       size_t o = (size_t)j * PR.k + LP.level[k];
       it[ITS * x] = PR.a2[o]; it[ITS * x + 1] = PR.b2[o]; it[ITS * x + 2] = PR.c2[o];
-      if (ITS == 4) it[ITS * x + 3] = 0.0;
     }
   }
   __syncthreads();
@@ -78,7 +68,6 @@ template <int KK>
 __device__ __forceinline__ int scan_ttft_ilp(const double *tt, uint32_t nbt, double budget);
 
 __device__ __forceinline__ int scan_ttft(const double *tt, int K, uint32_t nbt, double budget) {
-#if VT_DECIDE_ILP
   switch (K) {
     case 1: return 0;
     case 2: return scan_ttft_ilp<2>(tt, nbt, budget);
@@ -90,7 +79,6 @@ __device__ __forceinline__ int scan_ttft(const double *tt, int K, uint32_t nbt, 
     case 8: return scan_ttft_ilp<8>(tt, nbt, budget);
     default: break;
   }
-#endif
   for (int k = 0; k < K; ++k)
     if (ttft_pred(tt[2 * k], tt[2 * k + 1], nbt) <= budget) return k;
   return K - 1;
@@ -106,12 +94,7 @@ __device__ __forceinline__ const double *itl_row(const double *it, const DevProf
 }
 
 __device__ __forceinline__ double itl_eval(const double *row, int k, double dn, double dkv) {
-#if VT_ITS4
-  const double2 ab = *reinterpret_cast<const double2 *>(row + 4 * k);  // one LDS.128 for a2, b2
-  return add(add(mul(ab.x, dn), mul(ab.y, dkv)), row[4 * k + 2]);
-#else
   return add(add(mul(row[3 * k], dn), mul(row[3 * k + 1], dkv)), row[3 * k + 2]);
-#endif
 }
 
 __device__ __forceinline__ uint32_t itl_tile(const DevProfile &PR, uint64_t n, int wshift) {
@@ -143,7 +126,6 @@ __device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, 
                                         uint64_t kv, double target, int wshift) {
   const double *row = itl_row(it, PR, K, n, wshift);
   const double dn = (double)n, dkv = (double)kv;
-#if VT_DECIDE_ILP
   switch (K) {
     case 1: return 0;
     case 2: return scan_itl_ilp<2>(row, dn, dkv, target);
@@ -155,10 +137,57 @@ __device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, 
     case 8: return scan_itl_ilp<8>(row, dn, dkv, target);
     default: break;
   }
-#endif
   for (int k = 0; k < K; ++k)
     if (itl_eval(row, k, dn, dkv) <= target) return k;
   return K - 1;
+}
+
+// EcoRoute's what-if pair of one instance (A10-A12): the lowest feasible level now (n, kv) and
+// after the hypothetical addition (n + 1, kv + in + 1). Both states usually fall in the same
+// batch-size tile, so each level's {a2, b2, c2} is loaded once and evaluated twice (the
+// shared-memory loads, not the FP64 work, bound this kernel). Same values as two scans.
+template <int KK>
+__device__ __forceinline__ void scan_pair_ilp(const double *r0, const double *r1, double n0, double k0d, double n1,
+                                              double k1d, double target, int &kn, int &ka) {
+  kn = KK - 1;
+  ka = KK - 1;
+  if (r0 == r1) {
+#pragma unroll
+    for (int k = KK - 2; k >= 0; --k) {
+      const double a = r0[3 * k], b = r0[3 * k + 1], c = r0[3 * k + 2];
+      if (add(add(mul(a, n0), mul(b, k0d)), c) <= target) kn = k;
+      if (add(add(mul(a, n1), mul(b, k1d)), c) <= target) ka = k;
+    }
+  } else {
+#pragma unroll
+    for (int k = KK - 2; k >= 0; --k) {
+      if (itl_eval(r0, k, n0, k0d) <= target) kn = k;
+      if (itl_eval(r1, k, n1, k1d) <= target) ka = k;
+    }
+  }
+}
+
+__device__ __forceinline__ void scan_pair(const double *it, const DevProfile &PR, int K, uint64_t n, uint64_t kv,
+                                          uint64_t in, double target, int wshift, int &kn, int &ka) {
+  const uint64_t n1 = n + 1u, kv1 = kv + in + 1u;  // A12
+  const double *r1 = itl_row(it, PR, K, n1, wshift);
+  const double *r0 = n == 0u ? r1 : itl_row(it, PR, K, n, wshift);
+  const double dn0 = (double)n, dk0 = (double)kv, dn1 = (double)n1, dk1 = (double)kv1;
+  switch (K) {
+    case 1: kn = 0; ka = 0; return;
+    case 2: scan_pair_ilp<2>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    case 3: scan_pair_ilp<3>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    case 4: scan_pair_ilp<4>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    case 5: scan_pair_ilp<5>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    case 6: scan_pair_ilp<6>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    case 7: scan_pair_ilp<7>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    case 8: scan_pair_ilp<8>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
+    default:
+      kn = scan_itl(it, PR, K, n, kv, target, wshift);
+      ka = scan_itl(it, PR, K, n1, kv1, target, wshift);
+      break;
+  }
+  if (n == 0u) kn = 0;  // an idle instance: level 0 (A11)
 }
 
 // busy power (eq:P-f P:187, A22) for a 64-bit load
@@ -198,11 +227,9 @@ __device__ __forceinline__ int energy_itl(const double *it, const double *dy, co
 }
 
 // ---------------------------------------------------------------- K2 control_step
-#ifndef VT_CTL_MINB
-#define VT_CTL_MINB 8     // 8 CTAs x 8 warps per SM with 2 items per thread: measured best (55 % of HBM)
-#endif
+constexpr int CTL_MINB = 8;       // 8 CTAs x 8 warps per SM with 2 items per thread: measured best
 template <int PHASE>
-__global__ void __launch_bounds__(DECIDE_THREADS, VT_CTL_MINB)
+__global__ void __launch_bounds__(DECIDE_THREADS, CTL_MINB)
 control_kernel(const __grid_constant__ ControlParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
@@ -328,43 +355,12 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   } else {
   int fnow[NI], faft[NI];
   int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
-#if VT_ROUTE_LOCKSTEP
-  // all 2*N_D what-if scans advance together over the levels (independent evaluations
-  // interleave); each stops at its lowest feasible level exactly like scan_itl
-  int lv[2 * NI], row[2 * NI];
-  double xn[2 * NI], xk[2 * NI];
-  bool dn[2 * NI];
-#pragma unroll
-  for (int q = 0; q < 2 * NI; ++q) {
-    const int d = q >> 1;
-    const uint64_t nn = (uint64_t)n[d < NI ? d : 0] + (q & 1), kk = (uint64_t)kv[d < NI ? d : 0] + ((q & 1) ? in + 1u : 0u);
-    lv[q] = (q & 1) == 0 && nn == 0 ? 0 : K - 1;
-    dn[q] = d >= ND || ((q & 1) == 0 && nn == 0);
-    row[q] = dn[q] ? 0 : ITS * K * (int)itl_tile(P.prof, nn, wshift);
-    xn[q] = (double)nn; xk[q] = (double)kk;
-  }
-  for (int k = 0; k < K - 1; ++k) {
-    bool all = true;
-#pragma unroll
-    for (int q = 0; q < 2 * NI; ++q) {
-      if (dn[q]) continue;
-      const double *r = it + row[q] + ITS * k;
-      if (add(add(mul(r[0], xn[q]), mul(r[1], xk[q])), r[2]) <= tgt) { lv[q] = k; dn[q] = true; }
-      all = all && dn[q];
-    }
-    if (all) break;
-  }
-#endif
 #pragma unroll
   for (int d = 0; d < NI; ++d) {
     fnow[d] = faft[d] = 0;
     if (d < ND) {
-#if VT_ROUTE_LOCKSTEP
-      const int kn = lv[2 * d], ka = lv[2 * d + 1];
-#else
-      const int kn = n[d] == 0u ? 0 : scan_itl(it, P.prof, K, n[d], kv[d], tgt, wshift);   // A10, A11
-      const int ka = scan_itl(it, P.prof, K, (uint64_t)n[d] + 1u, (uint64_t)kv[d] + in + 1u, tgt, wshift);  // A12
-#endif
+      int kn, ka;   // A10-A12
+      scan_pair(it, P.prof, K, n[d], kv[d], in, tgt, wshift, kn, ka);
       fnow[d] = smi[kn];
       faft[d] = smi[ka];
       const bool cr = faft[d] > fnow[d];                                                 // A13
@@ -403,14 +399,10 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   if (__popc(inset) >= 2) cursor = (d + 1u) % (uint32_t)ND;                             // A17
 }
 
-#ifndef VT_ROUTE_MINB
-#define VT_ROUTE_MINB 4   // 4 CTAs x 8 warps per SM (<= 64 registers): measured best with 2 items/thread
-#endif
-#ifndef VT_ROUTE_U2
-#define VT_ROUTE_U2 2     // items per thread per tile when N_D <= 2
-#endif
+constexpr int ROUTE_MINB = 4;     // 4 CTAs x 8 warps per SM (<= 64 registers): measured best with 2 items/thread
+constexpr int ROUTE_U2 = 2;       // items per thread per tile when N_D <= 2
 template <int ND_MAX>
-__global__ void __launch_bounds__(DECIDE_THREADS, VT_ROUTE_MINB)
+__global__ void __launch_bounds__(DECIDE_THREADS, ROUTE_MINB)
 route_kernel(const __grid_constant__ RouteParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
@@ -419,7 +411,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
   const double *it = itl_smem(sm, K, P.prof);
   const double *dy = dyn_smem(sm, K, P.prof);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
-  constexpr int U = ND_MAX <= 2 ? VT_ROUTE_U2 : 2;
+  constexpr int U = ND_MAX <= 2 ? ROUTE_U2 : 2;
   const size_t tile = (size_t)blockDim.x * U;
   for (size_t base = (size_t)blockIdx.x * tile; base < P.n; base += (size_t)gridDim.x * tile) {
     uint32_t inv[U], cur[U], n[U][ND_MAX], kv[U][ND_MAX];

@@ -58,6 +58,8 @@ struct RouteEnt {   // one request of the merged route stream (16 B)
 };
 
 constexpr int NI = VOLTANA_MAX_INSTANCES;
+constexpr int ECO_LUT_K = 5;   // the N_D = 2 EcoRoute decision table covers ladders up to 5 levels
+constexpr int ECO_LUT_N = ECO_LUT_K * ECO_LUT_K * ECO_LUT_K * ECO_LUT_K * 2;
 
 struct RouteWin {   // the merged window of the prefill streams (per warp, shared memory)
   RouteEnt ring[32];
@@ -93,6 +95,7 @@ struct WarpSmemT {
   // ---- variant-kernel per-instance controller state [C1-C3]
   double dl_last[NI];              // decode lane: time of the last decision (-inf: none)
   uint32_t dl_cur[NI], dl_ndec[NI];  // decode lane: running level, decisions taken
+  uint8_t lut[KC == 8 ? ECO_LUT_N : 1];  // N_D = 2 EcoRoute decision table (fast kernel)
   // ---- staged ladder tables
   uint16_t lad[KC];
   int32_t mhz[KC];
@@ -372,7 +375,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     uint4 lb = make_uint4(0u, 0u, 0u, 0u);
     // far requests whose finishing iteration entered the window join their bucket now,
     // before any direct admission can reach that bucket (admission order, A37)
-    while (D.far_h != NIL && D.far_hfin - D.iters < W.nb) {
+    while (D.far_hfin - D.iters < W.nb) {   // (an empty far list has far_hfin = NIL)
       const uint32_t i = D.far_h;
       const Node fn = L.node[i];
       const uint32_t fin = D.far_hfin;
@@ -704,15 +707,13 @@ __device__ __noinline__ uint32_t route_refill(RouteWin &R, const Node *node, uin
 // request). Every lane computes the same decision; MHz from the staged ladder. ND is a
 // template parameter so the per-instance loops are straight-line code.
 template <int ND>
-__device__ __forceinline__ void eco_cases_nd(unsigned fm, int K, const int32_t *mhz, int32_t delta,
-                                             uint32_t &cursor, int &dsel, int &cse) {
-  const unsigned km = (1u << K) - 1u;
+__device__ __forceinline__ void eco_from_levels(const int *kn, const int *ka, const int32_t *mhz, int32_t delta,
+                                                uint32_t &cursor, int &dsel, int &cse) {
   int fn[ND], fa[ND];
 #pragma unroll
   for (int d = 0; d < ND; ++d) {
-    const unsigned cm = (fm >> (2 * K * d)) & km, am = (fm >> (2 * K * d + K)) & km;
-    fn[d] = mhz[cm ? ffs0(cm) : K - 1];   // f: lowest feasible level now (A10, A11)
-    fa[d] = mhz[am ? ffs0(am) : K - 1];   // f': after the hypothetical addition (A12)
+    fn[d] = mhz[kn[d]];   // f: lowest feasible level now (A10, A11)
+    fa[d] = mhz[ka[d]];   // f': after the hypothetical addition (A12)
   }
   int mnAll = fn[0], maAll = fa[0], mnU = 0x7fffffff, maR = 0x7fffffff;
   unsigned Rm = 0u;
@@ -746,6 +747,37 @@ __device__ __forceinline__ void eco_cases_nd(unsigned fm, int K, const int32_t *
   const unsigned rot = ((inset >> cursor) | (inset << (ND - (int)cursor))) & all;
   dsel = (int)wrap_nd(cursor + (uint32_t)ffs0(rot), (uint32_t)ND);
   if (__popc(inset) >= 2) cursor = wrap_nd((uint32_t)dsel + 1u, (uint32_t)ND);
+}
+
+// lowest feasible level of a K-bit feasibility mask, else K-1 (A2)
+__device__ __forceinline__ int lowest_of(unsigned m, int K) { return ffs0(m | (1u << (K - 1))); }
+
+template <int ND>
+__device__ __forceinline__ void eco_cases_nd(unsigned fm, int K, const int32_t *mhz, int32_t delta,
+                                             uint32_t &cursor, int &dsel, int &cse) {
+  const unsigned km = (1u << K) - 1u;
+  int kn[ND], ka[ND];
+#pragma unroll
+  for (int d = 0; d < ND; ++d) {
+    kn[d] = lowest_of((fm >> (2 * K * d)) & km, K);
+    ka[d] = lowest_of((fm >> (2 * K * d + K)) & km, K);
+  }
+  eco_from_levels<ND>(kn, ka, mhz, delta, cursor, dsel, cse);
+}
+
+// N_D = 2, K <= ECO_LUT_K: the whole case analysis as a table over (f, f' of both instances,
+// cursor), built per scenario by the same function (so it is the same decision), read with one
+// shared-memory byte load per route: dsel | cse << 1 | new cursor << 4.
+__device__ __forceinline__ void eco_lut_build(uint8_t *lut, int K, const int32_t *mhz, int32_t delta) {
+  const int K2 = K * K, n = K2 * K2 * 2;
+  for (int e = (int)(threadIdx.x & 31u); e < n; e += 32) {
+    const int c0 = e / (2 * K2), c1 = (e / 2) % K2;
+    int kn[2] = {c0 / K, c1 / K}, ka[2] = {c0 % K, c1 % K};
+    uint32_t cur = (uint32_t)(e & 1);
+    int dsel, cse;
+    eco_from_levels<2>(kn, ka, mhz, delta, cur, dsel, cse);
+    lut[e] = (uint8_t)(dsel | cse << 1 | cur << 4);
+  }
 }
 
 __device__ __forceinline__ void eco_cases(unsigned fm, int ND, int K, const int32_t *mhz, int32_t delta,
@@ -1278,6 +1310,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     mi = __all_sync(FULL, mi);
     if (lane == 0) W.mono_it = mi;
   }
+  // N_D = 2 EcoRoute decision table (fast kernel, K <= 5)
+  const bool lut_on = F && LY.policy == 0 && ND == 2 && K <= (uint32_t)ECO_LUT_K;
+  if (lut_on) eco_lut_build(W.lut, (int)K, W.mhz, LY.delta_mhz);
   Node *node = (Node *)node_base(P, s);
   const uint64_t h0 = P.hash_seed[s];
   // ================================================================ PHASE A results (K4a)
@@ -1386,7 +1421,19 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         if (n == 0u) feas = wk == 0u;                                   // n = 0 -> level 0 (A11)
         else feas = itl_at<F>(W, tile_j<F>(W, n), (int)wk, (double)n, (double)kv) <= W.tgt_itl;
       }
-      eco_cases(wballot(feas), ND, (int)K, W.mhz, delta, cursor, dsel, cse);
+      const unsigned fm = wballot(feas);
+      if (F && lut_on) {   // N_D = 2: one table read (built by eco_from_levels at scenario start)
+        const unsigned km = (1u << K) - 1u;
+        const uint32_t c0 = (uint32_t)lowest_of(fm & km, (int)K) * K + (uint32_t)lowest_of((fm >> K) & km, (int)K);
+        const uint32_t c1 = (uint32_t)lowest_of((fm >> (2 * K)) & km, (int)K) * K +
+                            (uint32_t)lowest_of((fm >> (3 * K)) & km, (int)K);
+        const uint32_t v = W.lut[((c0 * K * K + c1) << 1) | cursor];
+        dsel = (int)(v & 1u);
+        cse = (int)((v >> 1) & 7u);
+        cursor = v >> 4;
+      } else {
+        eco_cases(fm, ND, (int)K, W.mhz, delta, cursor, dsel, cse);
+      }
     } else if (ens) {  // ---- energy-scored router [B1-B3]
       const bool act = lane < ND;
       bool feas = false;

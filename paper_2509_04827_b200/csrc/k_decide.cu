@@ -67,7 +67,10 @@ __device__ void stage_tables(const DevProfile &PR, const LadderParam &LP, bool n
 template <int KK>
 __device__ __forceinline__ int scan_ttft_ilp(const double *tt, uint32_t nbt, double budget);
 
+template <int KK = 0>
 __device__ __forceinline__ int scan_ttft(const double *tt, int K, uint32_t nbt, double budget) {
+  if (KK == 1) return 0;
+  if (KK > 1) return scan_ttft_ilp<(KK > 1 ? KK : 2)>(tt, nbt, budget);
   switch (K) {
     case 1: return 0;
     case 2: return scan_ttft_ilp<2>(tt, nbt, budget);
@@ -122,10 +125,13 @@ __device__ __forceinline__ int scan_ttft_ilp(const double *tt, uint32_t nbt, dou
   return kk;
 }
 
+template <int KK = 0>
 __device__ __forceinline__ int scan_itl(const double *it, const DevProfile &PR, int K, uint64_t n,
                                         uint64_t kv, double target, int wshift) {
   const double *row = itl_row(it, PR, K, n, wshift);
   const double dn = (double)n, dkv = (double)kv;
+  if (KK == 1) return 0;
+  if (KK > 1) return scan_itl_ilp<(KK > 1 ? KK : 2)>(row, dn, dkv, target);
   switch (K) {
     case 1: return 0;
     case 2: return scan_itl_ilp<2>(row, dn, dkv, target);
@@ -167,12 +173,19 @@ __device__ __forceinline__ void scan_pair_ilp(const double *r0, const double *r1
   }
 }
 
+template <int KK = 0>
 __device__ __forceinline__ void scan_pair(const double *it, const DevProfile &PR, int K, uint64_t n, uint64_t kv,
                                           uint64_t in, double target, int wshift, int &kn, int &ka) {
   const uint64_t n1 = n + 1u, kv1 = kv + in + 1u;  // A12
   const double *r1 = itl_row(it, PR, K, n1, wshift);
   const double *r0 = n == 0u ? r1 : itl_row(it, PR, K, n, wshift);
   const double dn0 = (double)n, dk0 = (double)kv, dn1 = (double)n1, dk1 = (double)kv1;
+  if (KK == 1) { kn = 0; ka = 0; return; }
+  if (KK > 1) {
+    scan_pair_ilp<(KK > 1 ? KK : 2)>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka);
+    if (n == 0u) kn = 0;
+    return;
+  }
   switch (K) {
     case 1: kn = 0; ka = 0; return;
     case 2: scan_pair_ilp<2>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
@@ -183,8 +196,8 @@ __device__ __forceinline__ void scan_pair(const double *it, const DevProfile &PR
     case 7: scan_pair_ilp<7>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
     case 8: scan_pair_ilp<8>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka); break;
     default:
-      kn = scan_itl(it, PR, K, n, kv, target, wshift);
-      ka = scan_itl(it, PR, K, n1, kv1, target, wshift);
+      kn = scan_itl<>(it, PR, K, n, kv, target, wshift);
+      ka = scan_itl<>(it, PR, K, n1, kv1, target, wshift);
       break;
   }
   if (n == 0u) kn = 0;  // an idle instance: level 0 (A11)
@@ -228,13 +241,13 @@ __device__ __forceinline__ int energy_itl(const double *it, const double *dy, co
 
 // ---------------------------------------------------------------- K2 control_step
 constexpr int CTL_MINB = 8;       // 8 CTAs x 8 warps per SM with 2 items per thread: measured best
-template <int PHASE>
+template <int PHASE, int KK>   // KK: the ladder length when known at compile time (0: runtime)
 __global__ void __launch_bounds__(DECIDE_THREADS, CTL_MINB)
 control_kernel(const __grid_constant__ ControlParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
   stage_tables(P.prof, P.lad, PHASE == 0, PHASE == 1, P.mode == 1 ? PHASE : -1, sm, smi);
-  const int K = P.lad.k;
+  const int K = KK > 0 ? KK : P.lad.k;
   const double *dy = dyn_smem(sm, K, P.prof);
   const double *its = itl_smem(sm, K, P.prof);
   const bool emode = P.mode == 1;
@@ -270,7 +283,7 @@ control_kernel(const __grid_constant__ ControlParams P) {
           double b = sub(tgt[u], wait[u]);
           b = b > 0.0 ? b : 0.0;
           const double *ttr = tt_row(sm, K, P.prof, load[u]);   // prefill tile (F1)
-          lvl = (uint16_t)(emode ? energy_ttft(ttr, dy, P.prof, K, load[u], b) : scan_ttft(ttr, K, load[u], b));
+          lvl = (uint16_t)(emode ? energy_ttft(ttr, dy, P.prof, K, load[u], b) : scan_ttft<KK>(ttr, K, load[u], b));
         }
       } else {
         if (load[u] == 0u || kv[u] < load[u]) {
@@ -279,7 +292,7 @@ control_kernel(const __grid_constant__ ControlParams P) {
           lvl = (uint16_t)(K - 1);
         } else {
           lvl = (uint16_t)(emode ? energy_itl(its, dy, P.prof, K, load[u], kv[u], tgt[u], wshift)
-                                 : scan_itl(its, P.prof, K, load[u], kv[u], tgt[u], wshift));
+                                 : scan_itl<KK>(its, P.prof, K, load[u], kv[u], tgt[u], wshift));
         }
       }
       P.out_level[i] = lvl;
@@ -291,7 +304,7 @@ control_kernel(const __grid_constant__ ControlParams P) {
 // ---------------------------------------------------------------- K3 route_batch
 // One EcoRoute decision on caller-given effective states; NI = the kernel's
 // instance bound (2, 4 or 8), so the per-instance arrays stay in registers at that size.
-template <int NI>
+template <int NI, int KK>
 __device__ __forceinline__ void route_item(const RouteParams &P, const double *it, const double *dy, const int *smi,
                                            int K, int ND, int wshift, uint32_t in, double tgt, uint32_t &cursor,
                                            const uint32_t *n, const uint32_t *kv, uint16_t &dsel, uint8_t &cse,
@@ -322,7 +335,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
       double enow = 0.0;
       if (n[d] != 0u) {
         const double *r0 = itl_row(it, P.prof, K, n[d], wshift);
-        const int k0 = scan_itl(it, P.prof, K, n[d], kv[d], tgt, wshift);        // A10, A11
+        const int k0 = scan_itl<KK>(it, P.prof, K, n[d], kv[d], tgt, wshift);        // A10, A11
         enow = mul(power_at(P.prof, 1, dy[k0], n[d]), itl_eval(r0, k0, (double)n[d], (double)kv[d]));
       }
       const uint64_t n1 = (uint64_t)n[d] + 1u, kv1 = (uint64_t)kv[d] + in + 1u;   // A12
@@ -360,7 +373,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
     fnow[d] = faft[d] = 0;
     if (d < ND) {
       int kn, ka;   // A10-A12
-      scan_pair(it, P.prof, K, n[d], kv[d], in, tgt, wshift, kn, ka);
+      scan_pair<KK>(it, P.prof, K, n[d], kv[d], in, tgt, wshift, kn, ka);
       fnow[d] = smi[kn];
       faft[d] = smi[ka];
       const bool cr = faft[d] > fnow[d];                                                 // A13
@@ -401,13 +414,13 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
 
 constexpr int ROUTE_MINB = 4;     // 4 CTAs x 8 warps per SM (<= 64 registers): measured best with 2 items/thread
 constexpr int ROUTE_U2 = 2;       // items per thread per tile when N_D <= 2
-template <int ND_MAX>
+template <int ND_MAX, int KK>   // KK: the ladder length when known at compile time (0: runtime)
 __global__ void __launch_bounds__(DECIDE_THREADS, ROUTE_MINB)
 route_kernel(const __grid_constant__ RouteParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
   stage_tables(P.prof, P.lad, false, true, P.policy == 2 ? 1 : -1, sm, smi);
-  const int K = P.lad.k, ND = P.n_d;
+  const int K = KK > 0 ? KK : P.lad.k, ND = P.n_d;
   const double *it = itl_smem(sm, K, P.prof);
   const double *dy = dyn_smem(sm, K, P.prof);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
@@ -435,7 +448,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
       if (i >= P.n) continue;
       uint16_t dsel;
       uint8_t cse, st;
-      route_item<ND_MAX>(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], n[u], kv[u], dsel, cse, st);
+      route_item<ND_MAX, KK>(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], n[u], kv[u], dsel, cse, st);
       P.out_instance[i] = dsel;
       P.out_case[i] = cse;
       P.out_status[i] = st;
@@ -449,32 +462,51 @@ size_t decide_smem_bytes(int k, int n_tiles, int n_ptiles) {
   return (size_t)(2 * tp * k + ITS * n_tiles * k + k) * sizeof(double) + (size_t)k * sizeof(int);
 }
 
-cudaError_t launch_control(const ControlParams &P, int phase, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e;
-  if (phase == 0) {
-    e = cudaFuncSetAttribute(control_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    control_kernel<0><<<grid, DECIDE_THREADS, smem, st>>>(P);
-  } else {
-    e = cudaFuncSetAttribute(control_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    control_kernel<1><<<grid, DECIDE_THREADS, smem, st>>>(P);
-  }
+template <int PHASE, int KK>
+static cudaError_t launch_control_t(const ControlParams &P, int grid, size_t smem, cudaStream_t st) {
+  cudaError_t e = cudaFuncSetAttribute(control_kernel<PHASE, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  control_kernel<PHASE, KK><<<grid, DECIDE_THREADS, smem, st>>>(P);
   return cudaGetLastError();
 }
 
-template <int NDM>
+template <int PHASE>
+static cudaError_t launch_control_p(const ControlParams &P, int grid, size_t smem, cudaStream_t st) {
+  switch (P.lad.k) {
+    case 2: return launch_control_t<PHASE, 2>(P, grid, smem, st);
+    case 5: return launch_control_t<PHASE, 5>(P, grid, smem, st);
+    default: return launch_control_t<PHASE, 0>(P, grid, smem, st);
+  }
+}
+
+cudaError_t launch_control(const ControlParams &P, int phase, int grid, size_t smem, cudaStream_t st) {
+  return phase == 0 ? launch_control_p<0>(P, grid, smem, st) : launch_control_p<1>(P, grid, smem, st);
+}
+
+template <int NDM, int KK>
 static cudaError_t launch_route_t(const RouteParams &P, int grid, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(route_kernel<NDM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(route_kernel<NDM, KK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  route_kernel<NDM><<<grid, DECIDE_THREADS, smem, st>>>(P);
+  route_kernel<NDM, KK><<<grid, DECIDE_THREADS, smem, st>>>(P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_route(const RouteParams &P, int grid, size_t smem, cudaStream_t st) {
-  if (P.n_d <= 2) return launch_route_t<2>(P, grid, smem, st);
-  if (P.n_d <= 4) return launch_route_t<4>(P, grid, smem, st);
-  return launch_route_t<8>(P, grid, smem, st);
+  if (P.n_d <= 2) {
+    switch (P.lad.k) {  // ladder length as a template argument: straight-line scans, small code
+      case 1: return launch_route_t<2, 1>(P, grid, smem, st);
+      case 2: return launch_route_t<2, 2>(P, grid, smem, st);
+      case 3: return launch_route_t<2, 3>(P, grid, smem, st);
+      case 4: return launch_route_t<2, 4>(P, grid, smem, st);
+      case 5: return launch_route_t<2, 5>(P, grid, smem, st);
+      case 6: return launch_route_t<2, 6>(P, grid, smem, st);
+      case 7: return launch_route_t<2, 7>(P, grid, smem, st);
+      case 8: return launch_route_t<2, 8>(P, grid, smem, st);
+      default: return launch_route_t<2, 0>(P, grid, smem, st);
+    }
+  }
+  if (P.n_d <= 4) return launch_route_t<4, 0>(P, grid, smem, st);
+  return launch_route_t<8, 0>(P, grid, smem, st);
 }
 
 }  // namespace vt

@@ -5,10 +5,10 @@
 //   pass 2: per-cell centred S11, S12, S22, S1y, S2y                  -> OLS solve
 //   pass 3: per-cell sum |y - y_hat|                                   -> MAE
 // Determinism without fp64 atomics: every warp owns a contiguous sample range and a
-// private shared-memory accumulator row per cell. Within a 32-sample chunk, lanes of
-// equal cell are ranked with __match_any_sync and add in ascending lane order (one
-// round per rank; lanes of one round touch distinct cells), so each warp's partial is
-// the sequential sum over its range. Warp partials are combined in warp order per
+// private shared-memory accumulator row per cell. A 32-sample chunk of one cell (the usual
+// case: calibration samples come cell by cell) is summed by a fixed binary tree over the
+// lanes; otherwise lanes of equal cell are ranked with __match_any_sync and add in ascending
+// lane order (one round per rank; lanes of one round touch distinct cells). Warp partials are combined in warp order per
 // CTA, CTA partials in CTA order per cell: a fixed tree, independent of timing.
 #include <cstdint>
 
@@ -70,6 +70,101 @@ __device__ __forceinline__ Sample decode_sample(const FitParams &P, const Raw &r
     s.x2 = r.kv;
   }
   return s;
+}
+
+// grid reduction of CTA partials in CTA order, one thread per (cell, stat): red[c][q]
+template <int NS>
+__device__ void grid_reduce(const FitParams &P, int nblocks) {
+  const size_t stride = (size_t)P.cells * NS;
+  for (int x = threadIdx.x; x < P.cells * NS; x += blockDim.x) {
+    if (NS == 4 && (x % NS) < 3) {
+      uint64_t s = 0;
+      for (int b = 0; b < nblocks; ++b) s += __ldcg((const unsigned long long *)P.part + (size_t)b * stride + x);
+      ((uint64_t *)P.red)[x] = s;
+    } else {
+      double s = 0.0;
+      for (int b = 0; b < nblocks; ++b) s = add(s, __ldcg(P.part + (size_t)b * stride + x));
+      P.red[x] = s;
+    }
+  }
+}
+
+__device__ void fit_means(const FitParams &P) {
+  for (int c = threadIdx.x; c < P.cells; c += blockDim.x) {
+  const uint64_t *u = (const uint64_t *)(P.red + 4 * (size_t)c);
+  const uint64_t cnt = u[0];
+  P.cnt[c] = cnt;
+  double *m = P.means + 3 * (size_t)c;
+  if (cnt > 0) {
+    const double dc = (double)cnt;
+    m[0] = div((double)u[1], dc);
+    m[1] = div((double)u[2], dc);
+    m[2] = div(P.red[4 * (size_t)c + 3], dc);
+  } else {
+    m[0] = m[1] = m[2] = 0.0;
+  }
+  }
+}
+
+__device__ void fit_solve(const FitParams &P) {
+  // thread k < K: TTFT level k; thread K + k: ITL level k over tiles j = 0..T-1 (F4 chains)
+  const int K = P.k, T = P.n_tiles;
+  for (int t = threadIdx.x; t < 2 * K; t += blockDim.x) {
+  if (t < K) {  // TTFT level t over prefill tiles jp = 0..T_p-1 (empty jp > 0 inherits jp-1, F2)
+    for (int jp = 0; jp < P.n_ptiles; ++jp) {
+      const int c = jp * K + t;
+      const double *m = P.means + 3 * (size_t)c;
+      const double *r = P.red + 5 * (size_t)c;
+      double a = 0.0, cc = 0.0;
+      uint8_t st;
+      const double s11 = r[0], s1y = r[4];
+      if (P.cnt[c] == 0) {
+        if (jp == 0) st = 2;
+        else { a = P.a1[c - K]; cc = add(P.c1[c - K], P.tile_step); st = 1; }
+      } else if (P.cnt[c] < 2 || !(s11 > 0.0)) st = 3;   // A31
+      else {
+        a = div(s1y, s11);
+        cc = sub(m[2], mul(a, m[0]));
+        st = 0;
+      }
+      P.a1[c] = a; P.c1[c] = cc; P.status[c] = st;
+    }
+    continue;
+  }
+  const int k = t - K;
+  for (int j = 0; j < T; ++j) {
+    const int c = P.kp + j * K + k, o = j * K + k;
+    const double *m = P.means + 3 * (size_t)c;
+    const double *r = P.red + 5 * (size_t)c;
+    double a = 0.0, b = 0.0, cc = 0.0;
+    uint8_t st;
+    if (P.cnt[c] == 0) {
+      if (j == 0) st = 2;
+      else {                                 // inherit tile j-1 plus the step (F4)
+        a = P.a2[o - K]; b = P.b2[o - K]; cc = add(P.c2[o - K], P.tile_step);
+        st = 1;
+      }
+    } else {
+      const double s11 = r[0], s12 = r[1], s22 = r[2], s2y = r[3], s1y = r[4];
+      const double pr = mul(s11, s22);
+      const double det = sub(mul(s11, s22), mul(s12, s12));
+      if (P.cnt[c] < 3 || !(pr > 0.0) || !(det > mul(1e-10, pr))) {
+        st = 3;
+      } else {
+        a = div(sub(mul(s22, s1y), mul(s12, s2y)), det);
+        b = div(sub(mul(s11, s2y), mul(s12, s1y)), det);
+        cc = sub(sub(m[2], mul(a, m[0])), mul(b, m[1]));
+        st = 0;
+      }
+    }
+    P.a2[o] = a; P.b2[o] = b; P.c2[o] = cc; P.status[c] = st;
+  }
+  }
+}
+
+__device__ void fit_mae(const FitParams &P) {
+  for (int c = threadIdx.x; c < P.cells; c += blockDim.x)
+    P.mae[c] = P.status[c] == 0 ? div(P.red[c], (double)P.cnt[c]) : 0.0;
 }
 
 // Ordered per-warp accumulation of NS doubles (pass 2/3) or the pass-1 record.
@@ -137,6 +232,42 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
     const bool act = s.cell >= 0 && (PASS != 3 || P.status[s.cell] == 0);
     const int key = act ? s.cell : -1 - lane;
     const unsigned peers = __match_any_sync(FULL, key);
+    if (peers == FULL) {
+      // the whole chunk is one cell (profiling samples come cell by cell): a fixed binary tree
+      // over the 32 lanes (lane i adds lane i + o), then one update of the warp's row
+      double t[NS];
+#pragma unroll
+      for (int q = 0; q < NS; ++q) t[q] = v[q];
+      uint64_t x1 = s.x1, x2 = s.x2;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if (PASS == 1 && q < 3) continue;
+          const double y = __shfl_down_sync(FULL, t[q], o);
+          if (lane < (unsigned)o) t[q] = add(t[q], y);
+        }
+        if (PASS == 1) {
+          const uint64_t y1 = __shfl_down_sync(FULL, x1, o), y2 = __shfl_down_sync(FULL, x2, o);
+          if (lane < (unsigned)o) { x1 += y1; x2 += y2; }
+        }
+      }
+      if (lane == 0) {
+        double *a = acc + (size_t)s.cell * NS;
+        if (PASS == 1) {
+          uint64_t *u = (uint64_t *)a;
+          u[0] += 32u;
+          u[1] += x1;
+          u[2] += x2;
+          a[3] = add(a[3], t[3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < NS; ++q) a[q] = add(a[q], t[q]);
+        }
+      }
+      __syncwarp();
+      continue;
+    }
     const unsigned rank = __popc(peers & ((1u << lane) - 1u));
     const unsigned maxr = __reduce_max_sync(FULL, act ? rank : 0u);
     for (unsigned r = 0; r <= maxr; ++r) {
@@ -175,102 +306,21 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
       out[x] = s;
     }
   }
-}
-
-// grid reduction of CTA partials in CTA order, one thread per (cell, stat): red[c][q]
-template <int NS>
-__global__ void fit_reduce_kernel(const __grid_constant__ FitParams P, int nblocks) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= P.cells * NS) return;
-  const size_t stride = (size_t)P.cells * NS;
-  if (NS == 4 && (x % NS) < 3) {
-    uint64_t s = 0;
-    for (int b = 0; b < nblocks; ++b) s += ((const uint64_t *)P.part)[(size_t)b * stride + x];
-    ((uint64_t *)P.red)[x] = s;
-  } else {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s = add(s, P.part[(size_t)b * stride + x]);
-    P.red[x] = s;
-  }
-}
-
-__global__ void fit_means_kernel(const __grid_constant__ FitParams P) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= P.cells) return;
-  const uint64_t *u = (const uint64_t *)(P.red + 4 * (size_t)c);
-  const uint64_t cnt = u[0];
-  P.cnt[c] = cnt;
-  double *m = P.means + 3 * (size_t)c;
-  if (cnt > 0) {
-    const double dc = (double)cnt;
-    m[0] = div((double)u[1], dc);
-    m[1] = div((double)u[2], dc);
-    m[2] = div(P.red[4 * (size_t)c + 3], dc);
-  } else {
-    m[0] = m[1] = m[2] = 0.0;
-  }
-}
-
-__global__ void fit_solve_kernel(const __grid_constant__ FitParams P) {
-  // thread k < K: TTFT level k; thread K + k: ITL level k over tiles j = 0..T-1 (F4 chains)
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  const int K = P.k, T = P.n_tiles;
-  if (t >= 2 * K) return;
-  if (t < K) {  // TTFT level t over prefill tiles jp = 0..T_p-1 (empty jp > 0 inherits jp-1, F2)
-    for (int jp = 0; jp < P.n_ptiles; ++jp) {
-      const int c = jp * K + t;
-      const double *m = P.means + 3 * (size_t)c;
-      const double *r = P.red + 5 * (size_t)c;
-      double a = 0.0, cc = 0.0;
-      uint8_t st;
-      const double s11 = r[0], s1y = r[4];
-      if (P.cnt[c] == 0) {
-        if (jp == 0) st = 2;
-        else { a = P.a1[c - K]; cc = add(P.c1[c - K], P.tile_step); st = 1; }
-      } else if (P.cnt[c] < 2 || !(s11 > 0.0)) st = 3;   // A31
-      else {
-        a = div(s1y, s11);
-        cc = sub(m[2], mul(a, m[0]));
-        st = 0;
-      }
-      P.a1[c] = a; P.c1[c] = cc; P.status[c] = st;
-    }
-    return;
-  }
-  const int k = t - K;
-  for (int j = 0; j < T; ++j) {
-    const int c = P.kp + j * K + k, o = j * K + k;
-    const double *m = P.means + 3 * (size_t)c;
-    const double *r = P.red + 5 * (size_t)c;
-    double a = 0.0, b = 0.0, cc = 0.0;
-    uint8_t st;
-    if (P.cnt[c] == 0) {
-      if (j == 0) st = 2;
-      else {                                 // inherit tile j-1 plus the step (F4)
-        a = P.a2[o - K]; b = P.b2[o - K]; cc = add(P.c2[o - K], P.tile_step);
-        st = 1;
-      }
-    } else {
-      const double s11 = r[0], s12 = r[1], s22 = r[2], s2y = r[3], s1y = r[4];
-      const double pr = mul(s11, s22);
-      const double det = sub(mul(s11, s22), mul(s12, s12));
-      if (P.cnt[c] < 3 || !(pr > 0.0) || !(det > mul(1e-10, pr))) {
-        st = 3;
-      } else {
-        a = div(sub(mul(s22, s1y), mul(s12, s2y)), det);
-        b = div(sub(mul(s11, s2y), mul(s12, s1y)), det);
-        cc = sub(sub(m[2], mul(a, m[0])), mul(b, m[1]));
-        st = 0;
-      }
-    }
-    P.a2[o] = a; P.b2[o] = b; P.c2[o] = cc; P.status[c] = st;
-  }
-}
-
-__global__ void fit_mae_kernel(const __grid_constant__ FitParams P) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= P.cells) return;
-  P.mae[c] = P.status[c] == 0 ? div(P.red[c], (double)P.cnt[c]) : 0.0;
+  // the last CTA to finish reduces the partials in CTA order and runs this pass's epilogue
+  // (one launch per pass; the order of the sums does not depend on which CTA is last)
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(P.ticket + (PASS - 1), 1u) == gridDim.x - 1u;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  grid_reduce<NS>(P, (int)gridDim.x);
+  __syncthreads();
+  if (PASS == 1) fit_means(P);
+  else if (PASS == 2) fit_solve(P);
+  else fit_mae(P);
+  if (threadIdx.x == 0) P.ticket[PASS - 1] = 0u;   // ready for the next call
 }
 
 int fit_warps_per_block(int cells) {
@@ -292,17 +342,10 @@ static cudaError_t launch_pass(const FitParams &P, int blocks, int wpb, cudaStre
 
 cudaError_t launch_fit(const FitParams &P, int blocks, int wpb, cudaStream_t st, int *launches) {
   cudaError_t e;
-  const int cb = (P.cells + 127) / 128;
-  if ((e = launch_pass<1>(P, blocks, wpb, st)) != cudaSuccess) return e;
-  fit_reduce_kernel<4><<<(4 * P.cells + 127) / 128, 128, 0, st>>>(P, blocks);
-  fit_means_kernel<<<cb, 128, 0, st>>>(P);
-  if ((e = launch_pass<2>(P, blocks, wpb, st)) != cudaSuccess) return e;
-  fit_reduce_kernel<5><<<(5 * P.cells + 127) / 128, 128, 0, st>>>(P, blocks);
-  fit_solve_kernel<<<(2 * P.k + 127) / 128, 128, 0, st>>>(P);
-  if ((e = launch_pass<3>(P, blocks, wpb, st)) != cudaSuccess) return e;
-  fit_reduce_kernel<1><<<(P.cells + 127) / 128, 128, 0, st>>>(P, blocks);
-  fit_mae_kernel<<<cb, 128, 0, st>>>(P);
-  *launches = 9;
+  if ((e = launch_pass<1>(P, blocks, wpb, st)) != cudaSuccess) return e;   // + means
+  if ((e = launch_pass<2>(P, blocks, wpb, st)) != cudaSuccess) return e;   // + OLS solve
+  if ((e = launch_pass<3>(P, blocks, wpb, st)) != cudaSuccess) return e;   // + MAE
+  *launches = 3;
   return cudaGetLastError();
 }
 

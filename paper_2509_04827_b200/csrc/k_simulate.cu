@@ -250,7 +250,7 @@ struct Dec {               // decode instance d, owned by lane d
   int klast;               // the last EcoFreq level found by the search (start of the next one)
   uint32_t lpos, lend;     // this lane's chunk [lpos, lend) of the completion log
   bool busy, dead, lneed;  // lneed: the chunk is full, dec_advance stopped before an END
-  double end, ebusy, bms, top, sitl, tlast;
+  double end, ebusy, bms, top, sitl;
   uint64_t h;
   uint4 bcur;              // bucket of the running iteration, read at its START (final by then)
   Node qhn;                // register copy of the admission-queue head node
@@ -362,7 +362,6 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
         }
       }
       D.busy = false;
-      D.tlast = tnow;
     } else {
       // idle: the next START happens when the head of the admission queue becomes available
       if (D.qh == NIL) return;
@@ -1341,7 +1340,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   D.lpos = (uint32_t)lane * CLOG_CHUNK;  // first chunks: one per lane, allocated in lane order
   D.lend = D.lpos + CLOG_CHUNK;
   D.lneed = false;
-  D.ebusy = D.bms = D.top = D.sitl = D.tlast = 0.0;
+  D.ebusy = D.bms = D.top = D.sitl = 0.0;
   D.h = h0; D.n_itl_ok = D.n_both = 0;
   D.bcur = make_uint4(0u, 0u, 0u, 0u);
   D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.in = 0; D.qhn.out = 0;
@@ -1555,7 +1554,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       for (uint32_t b = 0; b < P.nb; ++b) wheels[(size_t)lane * P.nb + b] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
-  double tl = lane < ND ? D.tlast : 0.0;
+  // the last decode event of instance d is the END of its last iteration (the drain ran them all)
+  double tl = lane < ND && D.iters > 0u ? D.end : 0.0;
   if (lane < NP) tl = tl > W.pa[lane].tlast ? tl : W.pa[lane].tlast;
   for (int o = 16; o > 0; o >>= 1) {
     const double x = __shfl_xor_sync(FULL, tl, o);

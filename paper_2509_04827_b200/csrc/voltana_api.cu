@@ -167,7 +167,7 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
 
 // ------------------------------------------------------------------ K1
 namespace {
-struct FitLayout { int cells, wpb, blocks; size_t chunk, part, red, means, cnt, total; };
+struct FitLayout { int cells, wpb, blocks; size_t chunk, part, red, means, cnt, ticket, total; };
 
 FitLayout fit_layout(size_t n, int k, int n_tiles, int n_ptiles) {
   FitLayout L;
@@ -188,7 +188,8 @@ FitLayout fit_layout(size_t n, int k, int n_tiles, int n_ptiles) {
   L.red = align256(L.part + (size_t)L.blocks * L.cells * 5 * sizeof(double));
   L.means = align256(L.red + (size_t)L.cells * 5 * sizeof(double));
   L.cnt = align256(L.means + (size_t)L.cells * 3 * sizeof(double));
-  L.total = align256(L.cnt + (size_t)L.cells * sizeof(uint64_t));
+  L.ticket = align256(L.cnt + (size_t)L.cells * sizeof(uint64_t));
+  L.total = align256(L.ticket + 4 * sizeof(uint32_t));
   return L;
 }
 }  // namespace
@@ -231,11 +232,11 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, 
   P.red = (double *)(ws + L.red);
   P.means = (double *)(ws + L.means);
   P.cnt = (uint64_t *)(ws + L.cnt);
+  P.ticket = (uint32_t *)(ws + L.ticket);
   cudaStream_t st = (cudaStream_t)stream;
-  if (invalid_count) {
-    cudaError_t e = cudaMemsetAsync(invalid_count, 0, sizeof(uint64_t), st);
-    if (e != cudaSuccess) return cuda_fail(e, "fit_profile memset");
-  }
+  cudaError_t e0 = cudaMemsetAsync(P.ticket, 0, 4 * sizeof(uint32_t), st);
+  if (e0 == cudaSuccess && invalid_count) e0 = cudaMemsetAsync(invalid_count, 0, sizeof(uint64_t), st);
+  if (e0 != cudaSuccess) return cuda_fail(e0, "fit_profile memset");
   int launches = 0;
   cudaError_t e = launch_fit(P, L.blocks, L.wpb, st, &launches);
   if (e != cudaSuccess) return cuda_fail(e, "fit_profile launch");
@@ -294,10 +295,19 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   SimLayout L;
   L.nb = wheel_buckets(tr->max_out);
   size_t itl_bytes = (size_t)kmax * tmax * 24;
+  // the ladder's ITL table is staged in shared memory when it is small, or when the launch has
+  // fewer scenarios than the warps that stay resident with the larger block (C2: 28 levels x
+  // 16 tiles = 10.7 KB per warp, 1024 scenarios): then staging costs no occupancy that is used
+  auto block = [&](bool stage) {
+    size_t w = (sim_smem_fixed(fast) + (stage ? itl_bytes : 0) + 15) & ~(size_t)15;
+    return w + ((sizeof(ItlScratch) + 15) & ~(size_t)15);
+  };
   L.itl_smem = itl_bytes <= SIM_ITL_SMEM_MAX ? 1u : 0u;
-  L.smem_per_warp = (sim_smem_fixed(fast) + (L.itl_smem ? itl_bytes : 0) + 15) & ~(size_t)15;
-  L.ks_off = (uint32_t)L.smem_per_warp;  // ITL-pass scratch
-  L.smem_per_warp += (sizeof(ItlScratch) + 15) & ~(size_t)15;
+  if (!L.itl_smem && itl_bytes <= SIM_ITL_SMEM_BIG && block(true) * (SIM_THREADS / 32) <= 200 * 1024 &&
+      (size_t)resident_warps(block(true) * (SIM_THREADS / 32)) >= n)
+    L.itl_smem = 1u;
+  L.smem_per_warp = block(L.itl_smem != 0u);
+  L.ks_off = (uint32_t)(L.smem_per_warp - ((sizeof(ItlScratch) + 15) & ~(size_t)15));  // ITL-pass scratch
   L.smem = L.smem_per_warp * (SIM_THREADS / 32);
   // per resident warp: far-list finishing iterations [max_requests], then the completion log
   L.far = align256((size_t)tr->max_requests * 4);

@@ -26,6 +26,7 @@ struct FitParams {
   double *red;                // [cells][<=5] grid sums
   double *means;              // [cells][3]
   uint64_t *cnt;              // [cells]
+  uint32_t *ticket;           // [3] CTAs finished per pass (zeroed by the call; reset by the last CTA)
 };
 
 int fit_warps_per_block(int cells);

@@ -11,10 +11,11 @@
 namespace vt {
 
 constexpr int SIM_THREADS = 128;      // K4b: 4 warps per CTA, one scenario per warp
-constexpr int SIM_MIN_BLOCKS = 4;     // <= 128 registers, 16 warps per SM
+constexpr int SIM_MIN_BLOCKS = 4;     // <= 128 registers, 16 warps per SM (5: 96 registers, spills: 87 vs 80 ms)
 constexpr int MAX_SLOS = 64, MAX_LAYOUTS = 16, MAX_GRIDS = 16, MAX_PROFILES = 8;
 size_t sim_smem_fixed(bool fast);     // per-warp shared-memory block without the staged ITL table
-constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size
+constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size ...
+constexpr size_t SIM_ITL_SMEM_BIG = 24576;  // ... or up to this size when the occupancy is not needed
 constexpr uint32_t SIM_WHEEL_MAX = 2048;    // decode wheel buckets; longer requests use the far list
 constexpr uint32_t SIM_UTAB = 8192;         // loads with a tabulated utilisation u = l / (l + u_half)
 

@@ -1,2 +1,2 @@
-bash tools/gpu_check.sh r02d
-VOLTANA_SO=variants/lib_lat.so timeout 600 python tools/lat_probe.py 2>&1 | tail -2 | tee gpurun_out/r02d_latprobe.txt
+timeout 900 python -m pytest tests -m gpu -x -q -k "route or control or energy or ptiles or c1_full or edge" -p no:cacheprovider 2>&1 | tail -2
+timeout 300 python tools/stream_bench.py 2>&1 | tail -5

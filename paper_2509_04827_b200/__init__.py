@@ -8,6 +8,6 @@ binding (api), the multi-GPU scenario sharder (shard) and the build script.
 
 from .api import (  # noqa: F401
     DeviceProfile, DeviceWorkload, RESULT_DTYPE, SimOutputs, VOLTANA_DELTA_INF, control_step, fit_profile,
-    fit_workspace_bytes, last_launch_count, lpt_order, route_batch, series_to_samples, simulate, simulate_ex,
+    fit_workspace_bytes, last_launch_count, lpt_order, scenario_cost, route_batch, series_to_samples, simulate, simulate_ex,
 )
 from ._lib import ITERATION_DTYPE, VoltanaError, exported_symbols, lib  # noqa: F401

@@ -95,6 +95,14 @@ __device__ __forceinline__ const double *itl_row(const double *it, const DevProf
   if (j > (uint64_t)(PR.n_tiles - 1)) j = (uint64_t)(PR.n_tiles - 1);
   return it + ITS * (size_t)j * K;
 }
+// Row of the tile holding N_req = m + 1 for a 32-bit m (the tile of n is row32(n - 1), of n + 1
+// is row32(n): no 64-bit arithmetic and no overflow), power-of-two tile width.
+__device__ __forceinline__ const double *itl_row32(const double *it, uint32_t m, int wshift, uint32_t tmax,
+                                                   uint32_t row_len) {
+  uint32_t j = m >> wshift;
+  j = j < tmax ? j : tmax;
+  return it + j * row_len;
+}
 
 __device__ __forceinline__ double itl_eval(const double *row, int k, double dn, double dkv) {
   return add(add(mul(row[3 * k], dn), mul(row[3 * k + 1], dkv)), row[3 * k + 2]);
@@ -177,8 +185,15 @@ template <int KK = 0>
 __device__ __forceinline__ void scan_pair(const double *it, const DevProfile &PR, int K, uint64_t n, uint64_t kv,
                                           uint64_t in, double target, int wshift, int &kn, int &ka) {
   const uint64_t n1 = n + 1u, kv1 = kv + in + 1u;  // A12
-  const double *r1 = itl_row(it, PR, K, n1, wshift);
-  const double *r0 = n == 0u ? r1 : itl_row(it, PR, K, n, wshift);
+  const double *r0, *r1;
+  if (KK > 0 && wshift >= 0) {   // 32-bit tile rows (n < 2^32 by type)
+    const uint32_t tmax = (uint32_t)PR.n_tiles - 1u, rl = (uint32_t)(ITS * K);
+    r1 = itl_row32(it, (uint32_t)n, wshift, tmax, rl);
+    r0 = n == 0u ? r1 : itl_row32(it, (uint32_t)n - 1u, wshift, tmax, rl);
+  } else {
+    r1 = itl_row(it, PR, K, n1, wshift);
+    r0 = n == 0u ? r1 : itl_row(it, PR, K, n, wshift);
+  }
   const double dn0 = (double)n, dk0 = (double)kv, dn1 = (double)n1, dk1 = (double)kv1;
   if (KK == 1) { kn = 0; ka = 0; return; }
   if (KK > 1) {
@@ -318,7 +333,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   st = VOLTANA_ITEM_OK;
   if (P.policy == 1 || ND == 1) {
     dsel = (uint16_t)cursor;
-    cursor = (cursor + 1u) % (uint32_t)ND;
+    cursor = cursor + 1u >= (uint32_t)ND ? 0u : cursor + 1u;
     cse = 0;
     return;
   }
@@ -407,12 +422,13 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
   }
   }
   const unsigned rot = ((inset >> cursor) | (inset << (ND - cursor))) & ((1u << ND) - 1u);
-  const uint32_t d = (cursor + (uint32_t)ffs0(rot)) % (uint32_t)ND;
+  uint32_t d = cursor + (uint32_t)ffs0(rot);   // < 2 N_D: wrap without a division
+  d = d >= (uint32_t)ND ? d - (uint32_t)ND : d;
   dsel = (uint16_t)d;
-  if (__popc(inset) >= 2) cursor = (d + 1u) % (uint32_t)ND;                             // A17
+  if (__popc(inset) >= 2) cursor = d + 1u >= (uint32_t)ND ? 0u : d + 1u;                 // A17
 }
 
-constexpr int ROUTE_MINB = 4;     // 4 CTAs x 8 warps per SM (<= 64 registers): measured best with 2 items/thread
+constexpr int ROUTE_MINB = 4;     // CTAs of 8 warps per SM (<= 64 registers); 5 CTAs or 3-4 items: slower
 constexpr int ROUTE_U2 = 2;       // items per thread per tile when N_D <= 2
 template <int ND_MAX, int KK>   // KK: the ladder length when known at compile time (0: runtime)
 __global__ void __launch_bounds__(DECIDE_THREADS, ROUTE_MINB)
@@ -436,10 +452,17 @@ route_kernel(const __grid_constant__ RouteParams P) {
       inv[u] = in ? P.req_in[i] : 1u;
       tg[u] = in ? P.target[i] : 0.0;
       cur[u] = in ? P.cursor[i] : 0u;
+      if (ND_MAX == 2 && ND == 2 && P.pad) {   // one 8-byte load per array (8-B aligned, host-checked)
+        const uint2 a = in ? reinterpret_cast<const uint2 *>(P.n_req)[i] : make_uint2(0u, 0u);
+        const uint2 b = in ? reinterpret_cast<const uint2 *>(P.n_kv)[i] : make_uint2(0u, 0u);
+        n[u][0] = a.x; n[u][ND_MAX > 1 ? 1 : 0] = a.y;
+        kv[u][0] = b.x; kv[u][ND_MAX > 1 ? 1 : 0] = b.y;
+      } else {
 #pragma unroll
-      for (int d = 0; d < ND_MAX; ++d) {
-        n[u][d] = in && d < ND ? P.n_req[i * ND + d] : 0u;
-        kv[u][d] = in && d < ND ? P.n_kv[i * ND + d] : 0u;
+        for (int d = 0; d < ND_MAX; ++d) {
+          n[u][d] = in && d < ND ? P.n_req[i * ND + d] : 0u;
+          kv[u][d] = in && d < ND ? P.n_kv[i * ND + d] : 0u;
+        }
       }
     }
 #pragma unroll

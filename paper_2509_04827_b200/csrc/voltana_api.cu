@@ -159,6 +159,7 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
   P.n_d = n_d; P.policy = policy; P.delta = delta_mhz;
   P.n_req = n_req; P.n_kv = n_kv; P.req_in = req_in; P.target = itl_target_ms; P.cursor = cursor;
   P.n = n; P.out_instance = out_instance; P.out_case = out_case; P.out_status = out_status;
+  P.pad = (((uintptr_t)n_req | (uintptr_t)n_kv) & 7u) == 0 ? 1 : 0;  // 8-B vector loads of the N_D = 2 states
   cudaError_t e = launch_route(P, decide_grid(n), decide_smem_bytes(k, prof_h->n_tiles, prof_h->n_ptiles), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "route_batch launch");
   g_launches = 1;

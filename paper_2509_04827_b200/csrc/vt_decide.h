@@ -34,7 +34,7 @@ struct ControlParams {
 struct RouteParams {
   DevProfile prof;
   LadderParam lad;
-  int32_t n_d, policy, delta, pad;
+  int32_t n_d, policy, delta, pad;   // pad: 1 = n_req / n_kv are 8-byte aligned (vector loads)
   const uint32_t *n_req, *n_kv, *req_in;
   const double *target;
   uint32_t *cursor;

@@ -34,11 +34,12 @@ def lpt_partition(costs, world: int) -> list[np.ndarray]:
 
 
 def scenario_costs(w) -> np.ndarray:
-    """Cost estimate per scenario: requests of its trace (each is one route and part of a
-    prefill batch), weighted by the number of decode instances."""
+    """Cost estimate per scenario (api.scenario_cost): requests of its trace, weighted by the
+    number of decode instances."""
+    from .api import scenario_cost
     lens = np.diff(np.asarray(w.traces.offset, np.int64))
     nd = np.array([w.layouts[i].n_d for i in np.asarray(w.scen["layout_id"], np.int64)])
-    return lens[np.asarray(w.scen["trace_id"], np.int64)] * (1.0 + 0.05 * nd)
+    return scenario_cost(lens[np.asarray(w.scen["trace_id"], np.int64)], nd)
 
 
 def gather_records(local: torch.Tensor, parts: list[np.ndarray], n_total: int, group=None) -> np.ndarray:

@@ -1219,7 +1219,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 
   // ---------------------------------------------------------------- device validation (A40)
   // the per-request checks ran in K4a (each prefill warp over its stream); here their results
-  const int NP = LY.n_p, ND = LY.n_d;
+  // V & 4: every layout of the launch is N_D = 2 EcoRoute on a ladder of <= 5 levels (host-checked):
+  // the route loop keeps only the what-if lanes and the decision table (fewer live registers)
+  const int NP = LY.n_p, ND = (V & 4) ? 2 : LY.n_d;
   uint32_t tok_total;
   {
     bool ok = N64 <= P.max_requests && Dur >= 0.0 && node_range_ok(P, s, N64);
@@ -1310,7 +1312,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     if (lane == 0) W.mono_it = mi;
   }
   // N_D = 2 EcoRoute decision table (fast kernel, K <= 5)
-  const bool lut_on = F && LY.policy == 0 && ND == 2 && K <= (uint32_t)ECO_LUT_K;
+  const bool lut_on = (V & 4) || (F && LY.policy == 0 && ND == 2 && K <= (uint32_t)ECO_LUT_K);
   if (lut_on) eco_lut_build(W.lut, (int)K, W.mhz, LY.delta_mhz);
   Node *node = (Node *)node_base(P, s);
   const uint64_t h0 = P.hash_seed[s];
@@ -1356,9 +1358,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   int c_lvl = 0;                                    // the lane's effective state (c_n, c_kv)
   int ka_last = 0;
   double c_en = 0.0, en_new = 0.0;                  // energy router: P*T of the cached state / successor
-  const bool eco = LY.policy == 0 && ND > 1;
+  const bool eco = (V & 4) || (LY.policy == 0 && ND > 1);
   const bool ens = (V & 1) && LY.policy == 2 && ND > 1;
-  const bool wif = F && eco && (uint32_t)ND * 2u * K <= 32u;   // the lane-parallel what-if
+  const bool wif = (V & 4) || (F && eco && (uint32_t)ND * 2u * K <= 32u);   // the lane-parallel what-if
   const int32_t delta = LY.delta_mhz;
   // what-if lane (fast path): instance wd, state ws (0 now, 1 after), level wk, packed
   // wk | ws << 8 | wd << 16 (NIL: an idle lane)
@@ -1376,6 +1378,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #else
 #define LP_MARK(q) do { } while (0)
 #endif
+  uint32_t e_n0 = 0u, e_k0 = 0u, e_n1 = 0u, e_k1 = 0u;   // V & 4: both instances' effective states
   uint32_t rcnt = route_refill(W.rw, node, (uint32_t)NP), rpos = 0;
   for (;;) {
     // the next request of the merged stream; none left: the drain marker (t = +inf, io = 0)
@@ -1403,6 +1406,10 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       dec_advance_all<V, F>(D, lane, L, W, t, dE, P.o, ND, S, k_sd, k_ok, k_both);
       t_adv = t;
       if (e.io == 0u) break;
+      if (V & 4) {
+        const uint32_t en = D.nreq + D.pn, ek = D.nkv + D.pkv;
+        e_n0 = wshfl(en, 0); e_k0 = wshfl(ek, 0); e_n1 = wshfl(en, 1); e_k1 = wshfl(ek, 1);
+      }
     }
     const uint32_t i = e.id;
     const uint32_t in_i = e.io & 0xffffu;
@@ -1410,9 +1417,17 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     // ---- O8 EcoRoute
     int dsel, cse;
     if (wif) {   // one lane per (instance, state, level): the whole what-if in one ballot
-      const uint32_t en = D.nreq + D.pn, ek = D.nkv + D.pkv;   // A9 effective state (lane d)
-      const int src = (int)((wpk >> 16) & 0xffu);
-      const uint32_t n0 = wshfl(en, src & 31), kv0 = wshfl(ek, src & 31);
+      uint32_t n0, kv0;   // A9 effective state (running + pending) of the lane's instance
+      if (V & 4) {        // kept in every lane (re-read after a catch-up, bumped by each push)
+        const bool one = ((wpk >> 16) & 0xffu) != 0u;
+        n0 = one ? e_n1 : e_n0;
+        kv0 = one ? e_k1 : e_k0;
+      } else {
+        const uint32_t en = D.nreq + D.pn, ek = D.nkv + D.pkv;
+        const int src = (int)((wpk >> 16) & 0xffu);
+        n0 = wshfl(en, src & 31);
+        kv0 = wshfl(ek, src & 31);
+      }
       bool feas = false;
       if (wpk != NIL) {
         const uint32_t ws = (wpk >> 8) & 1u, wk = wpk & 0xffu;
@@ -1516,6 +1531,9 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
     }
     steps_route++;
     h_r = fold(h_r, 3, (uint64_t)dsel, 0, (uint64_t)cse);
+    if (V & 4) {   // the pending request joins instance dsel's effective state (A9, A12)
+      if (dsel == 0) { e_n0 += 1u; e_k0 += in_i + 1u; } else { e_n1 += 1u; e_k1 += in_i + 1u; }
+    }
     if (lane == dsel) {
       if (eco && !wif) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_lvl = ka_last; }  // its new state
       if (ens) { c_n = D.nreq + D.pn + 1u; c_kv = D.nkv + D.pkv + in_i + 1u; c_en = en_new; }
@@ -1731,6 +1749,7 @@ static const void *kptr(bool fast) {
 }
 
 const void *sim_kernel_ptr(int v, bool fast) {
+  if (v == 4 && fast) return (const void *)simulate_kernel<4, true>;
   switch (v & 3) {
     case 1: return kptr<1>(fast);
     case 2: return kptr<2>(fast);
@@ -1748,6 +1767,10 @@ static void launch_v(const SimParams &P, bool fast, int grid, size_t smem, cudaS
 // The dynamic shared-memory attribute of the instantiation is set by the host before anything
 // of the call is enqueued (voltana_simulate_ex), so a failure here is a launch error only.
 cudaError_t launch_sim(const SimParams &P, int v, bool fast, int grid, size_t smem, cudaStream_t st) {
+  if (v == 4 && fast) {
+    simulate_kernel<4, true><<<grid, SIM_THREADS, smem, st>>>(P);
+    return cudaGetLastError();
+  }
   switch (v & 3) {
     case 1: launch_v<1>(P, fast, grid, smem, st); break;
     case 2: launch_v<2>(P, fast, grid, smem, st); break;

@@ -466,6 +466,11 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
     if (x.ctrl_interval_ms > 0.0 || x.freq_overhead_ms > 0.0 || x.exec_noise != nullptr || x.itl_mode != 0) v |= 2;
   }
   if (outputs_h && (outputs_h->req_offset != nullptr || outputs_h->iter_offset != nullptr)) v |= 2;  // E1-E2
+  if (v == 0 && fast && kmax <= 5) {  // the N_D = 2 EcoRoute instantiation (decision table, fewer registers)
+    bool nd2 = true;
+    for (int i = 0; i < n_layouts; ++i) nd2 = nd2 && layouts_h[i].n_d == 2 && layouts_h[i].policy == 0;
+    if (nd2) v = 4;
+  }
   // every kernel attribute is set before anything of this call is enqueued: a non-OK return
   // below this point is a launch failure (VOLTANA_E_CUDA), the only partial-enqueue case
   cudaError_t e = cudaFuncSetAttribute(sim_kernel_ptr(v, fast), cudaFuncAttributeMaxDynamicSharedMemorySize,

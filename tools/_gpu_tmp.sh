@@ -1,2 +1,1 @@
-python tools/sim_ab.py paper_2509_04827_b200/libvoltana.so 2>&1 | tail -1
-timeout 1500 python -m pytest tests -m gpu -x -q -p no:cacheprovider 2>&1 | tail -3
+python tools/sim_ab.py variants/lib_v4e.so variants/lib_v4e.so 2>&1 | tail -2

@@ -17,6 +17,7 @@ size_t sim_smem_fixed(bool fast);     // per-warp shared-memory block without th
 constexpr size_t SIM_ITL_SMEM_MAX = 4096;   // stage the ladder's ITL table in smem up to this size ...
 constexpr size_t SIM_ITL_SMEM_BIG = 24576;  // ... or up to this size when the occupancy is not needed
 constexpr uint32_t SIM_WHEEL_MAX = 2048;    // decode wheel buckets; longer requests use the far list
+                                            // (512 / 1024 / 4096: 80.2 / 78.0 / 77.7 vs 77.8 ms on C4)
 constexpr uint32_t SIM_UTAB = 8192;         // loads with a tabulated utilisation u = l / (l + u_half)
 
 constexpr int PA_G = 32;              // K4a: one warp per (scenario, prefill instance)

@@ -1,1 +1,1 @@
-python tools/sim_ab.py variants/lib_v4e.so variants/lib_v4e.so 2>&1 | tail -2
+python tools/sim_ab.py variants/lib_nb2048.so variants/lib_nb1024.so variants/lib_nb512.so variants/lib_nb4096.so variants/lib_nb2048.so 2>&1 | tail -5

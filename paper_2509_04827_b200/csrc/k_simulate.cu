@@ -162,7 +162,8 @@ template <bool F, class WS>
 __device__ __forceinline__ int lowest_itl_from(const WS &W, uint32_t n, uint32_t kv, double target, int k0,
                                                double *pred) {
   const int K = (int)W.K;
-  if (!W.mono_it || K < 3) return lowest_itl<F>(W, n, kv, target, pred);
+  // long ladders: the binary search of lowest_itl is bounded by log2 K (a walk is not)
+  if (!W.mono_it || K < 3 || (!F && K > 8)) return lowest_itl<F>(W, n, kv, target, pred);
   const uint32_t j = tile_j<F>(W, n);
   const double dn = (double)n, dkv = (double)kv;
   int k = k0 < K - 2 ? k0 : K - 2;

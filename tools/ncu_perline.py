@@ -5,7 +5,7 @@ from collections import defaultdict
 rep, kern, obj, units = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4])
 lo, hi = (map(int, sys.argv[5].split("-")) if len(sys.argv) > 5 else (0, 10**9))
 top = int(sys.argv[6]) if len(sys.argv) > 6 else 60
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "-k", "regex:" + kern.split("ILi")[0].replace("_ZN2vt", "").lstrip("0123456789")],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = next(i for i, r in enumerate(rows) if r and r[0] == "Address")

@@ -130,9 +130,11 @@ def build_shard(args, rank, world):
 
 
 def fit_samples(prof):
+    """2 M calibration samples in recording order (one profiling run per frequency level, P:503;
+    DESIGN.md §4)."""
     from synth.samples import profile_samples
     m = max(2, N_SAMPLES // (prof.k * (1 + prof.n_tiles)))
-    return profile_samples(prof, m, m, noise_sigma=0.02, seed=0)
+    return profile_samples(prof, m, m, noise_sigma=0.02, seed=0, shuffle=False)
 
 
 def fitted_host_profile(prof, fit):
@@ -309,8 +311,12 @@ def streaming_kernels(vt, torch, dev, hbm_gbs, reps=100):
     by = m * (8 * nd + 4 + 8 + 4 + 4 + 2 + 1 + 1)
     out["route_batch"] = {"items": m, "bytes_per_item": 8 * nd + 24, "ms": s * 1e3, "achieved_gbs": by / s / 1e9,
                           "frac": by / s / 1e9 / hbm_gbs, "decisions_per_s": m / s}
-    for label, per_cell in (("fit_profile", 4096), ("fit_profile_large", 32768)):
-        smp = profile_samples(prof, per_cell, per_cell, noise_sigma=0.02, seed=9)
+    # samples in the order a profiling run records them (one run per frequency level,
+    # iterations in time order, batch sizes drifting: cell-clustered); "_shuffled" is the
+    # adversarial order (random cells in every 32-sample chunk)
+    for label, per_cell, shuffled in (("fit_profile", 4096, False), ("fit_profile_large", 32768, False),
+                                      ("fit_profile_large_shuffled", 32768, True)):
+        smp = profile_samples(prof, per_cell, per_cell, noise_sigma=0.02, seed=9, shuffle=shuffled)
         to = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else
                                         (a.view(np.int16) if a.dtype == np.uint16 else a)).to(dev)
         d = {k: to(v) for k, v in smp.items()}

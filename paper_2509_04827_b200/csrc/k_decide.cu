@@ -436,7 +436,8 @@ route_kernel(const __grid_constant__ RouteParams P) {
   extern __shared__ double sm[];
   int *smi = mhz_smem(sm, P.lad.k, P.prof);
   stage_tables(P.prof, P.lad, false, true, P.policy == 2 ? 1 : -1, sm, smi);
-  const int K = KK > 0 ? KK : P.lad.k, ND = P.n_d;
+  // <2, KK > 0> instantiations run only for N_D == 2 (host dispatch): N_D is a constant there
+  const int K = KK > 0 ? KK : P.lad.k, ND = (ND_MAX == 2 && KK > 0) ? 2 : P.n_d;
   const double *it = itl_smem(sm, K, P.prof);
   const double *dy = dyn_smem(sm, K, P.prof);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
@@ -515,8 +516,8 @@ static cudaError_t launch_route_t(const RouteParams &P, int grid, size_t smem, c
 }
 
 cudaError_t launch_route(const RouteParams &P, int grid, size_t smem, cudaStream_t st) {
-  if (P.n_d <= 2) {
-    switch (P.lad.k) {  // ladder length as a template argument: straight-line scans, small code
+  if (P.n_d == 2) {
+    switch (P.lad.k) {  // ladder length (and N_D = 2) as template arguments: straight-line code
       case 1: return launch_route_t<2, 1>(P, grid, smem, st);
       case 2: return launch_route_t<2, 2>(P, grid, smem, st);
       case 3: return launch_route_t<2, 3>(P, grid, smem, st);
@@ -528,6 +529,7 @@ cudaError_t launch_route(const RouteParams &P, int grid, size_t smem, cudaStream
       default: return launch_route_t<2, 0>(P, grid, smem, st);
     }
   }
+  if (P.n_d <= 2) return launch_route_t<2, 0>(P, grid, smem, st);
   if (P.n_d <= 4) return launch_route_t<4, 0>(P, grid, smem, st);
   return launch_route_t<8, 0>(P, grid, smem, st);
 }

@@ -5,10 +5,11 @@
 //   pass 2: per-cell centred S11, S12, S22, S1y, S2y                  -> OLS solve
 //   pass 3: per-cell sum |y - y_hat|                                   -> MAE
 // Determinism without fp64 atomics: every warp owns a contiguous sample range and a
-// private shared-memory accumulator row per cell. A 32-sample chunk of one cell (the usual
-// case: calibration samples come cell by cell) is summed by a fixed binary tree over the
-// lanes; otherwise lanes of equal cell are ranked with __match_any_sync and add in ascending
-// lane order (one round per rank; lanes of one round touch distinct cells). Warp partials are combined in warp order per
+// private shared-memory accumulator row per cell. Consecutive 32-sample chunks of one cell (the
+// usual case: calibration samples come run by run) accumulate in registers, each lane
+// summing its own samples in order, and at the end of the run a fixed binary tree over the
+// lanes adds them to the row; otherwise lanes of equal cell are ranked with __match_any_sync and
+// add in ascending lane order (one round per rank; lanes of one round touch distinct cells). Warp partials are combined in warp order per
 // CTA, CTA partials in CTA order per cell: a fixed tree, independent of timing.
 #include <cstdint>
 
@@ -186,6 +187,51 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
 #pragma unroll
   for (int u = 0; u < PF; ++u) buf[u] = load_raw(P, lo + (size_t)u * 32 + lane, lo + (size_t)u * 32 + lane < hi);
   int slot = 0;
+  // a run of one-cell chunks accumulates in registers (lane l sums its own samples in order);
+  // flush: a fixed tree over the lanes, added to the warp's row once per run
+  int run_cell = -1;
+  double racc[NS];
+  uint64_t rx1 = 0, rx2 = 0, rcnt = 0;
+#pragma unroll
+  for (int q = 0; q < NS; ++q) racc[q] = 0.0;
+  auto flush = [&]() {
+    if (run_cell < 0) return;
+    double t[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) t[q] = racc[q];
+    uint64_t x1 = rx1, x2 = rx2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+      for (int q = 0; q < NS; ++q) {
+        if (PASS == 1 && q < 3) continue;
+        const double y = __shfl_down_sync(FULL, t[q], o);
+        if (lane < o) t[q] = add(t[q], y);
+      }
+      if (PASS == 1) {
+        const uint64_t y1 = __shfl_down_sync(FULL, x1, o), y2 = __shfl_down_sync(FULL, x2, o);
+        if (lane < o) { x1 += y1; x2 += y2; }
+      }
+    }
+    if (lane == 0) {
+      double *a = acc + (size_t)run_cell * NS;
+      if (PASS == 1) {
+        uint64_t *u = (uint64_t *)a;
+        u[0] += rcnt * 32u;
+        u[1] += x1;
+        u[2] += x2;
+        a[3] = add(a[3], t[3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) a[q] = add(a[q], t[q]);
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int q = 0; q < NS; ++q) racc[q] = 0.0;
+    rx1 = rx2 = rcnt = 0;
+    run_cell = -1;
+  };
   for (size_t base = lo; base < hi; base += 32) {
     const Sample s = decode_sample(P, buf[0]);
 #pragma unroll
@@ -232,42 +278,20 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
     const bool act = s.cell >= 0 && (PASS != 3 || P.status[s.cell] == 0);
     const int key = act ? s.cell : -1 - lane;
     const unsigned peers = __match_any_sync(FULL, key);
-    if (peers == FULL) {
-      // the whole chunk is one cell (profiling samples come cell by cell): a fixed binary tree
-      // over the 32 lanes (lane i adds lane i + o), then one update of the warp's row
-      double t[NS];
+    if (peers == FULL) {   // the whole chunk is one cell: extend (or start) the register run
+      if (s.cell != run_cell) { flush(); run_cell = s.cell; }
+      if (PASS == 1) {
+        rx1 += s.x1;
+        rx2 += s.x2;
+        rcnt += 1u;
+        racc[3] = add(racc[3], v[3]);
+      } else {
 #pragma unroll
-      for (int q = 0; q < NS; ++q) t[q] = v[q];
-      uint64_t x1 = s.x1, x2 = s.x2;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int q = 0; q < NS; ++q) {
-          if (PASS == 1 && q < 3) continue;
-          const double y = __shfl_down_sync(FULL, t[q], o);
-          if (lane < (unsigned)o) t[q] = add(t[q], y);
-        }
-        if (PASS == 1) {
-          const uint64_t y1 = __shfl_down_sync(FULL, x1, o), y2 = __shfl_down_sync(FULL, x2, o);
-          if (lane < (unsigned)o) { x1 += y1; x2 += y2; }
-        }
+        for (int q = 0; q < NS; ++q) racc[q] = add(racc[q], v[q]);
       }
-      if (lane == 0) {
-        double *a = acc + (size_t)s.cell * NS;
-        if (PASS == 1) {
-          uint64_t *u = (uint64_t *)a;
-          u[0] += 32u;
-          u[1] += x1;
-          u[2] += x2;
-          a[3] = add(a[3], t[3]);
-        } else {
-#pragma unroll
-          for (int q = 0; q < NS; ++q) a[q] = add(a[q], t[q]);
-        }
-      }
-      __syncwarp();
       continue;
     }
+    flush();
     const unsigned rank = __popc(peers & ((1u << lane) - 1u));
     const unsigned maxr = __reduce_max_sync(FULL, act ? rank : 0u);
     for (unsigned r = 0; r <= maxr; ++r) {
@@ -287,6 +311,7 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
       __syncwarp();
     }
   }
+  flush();
   if (PASS == 1) {
     for (int o = 16; o > 0; o >>= 1) invalid += __shfl_xor_sync(FULL, invalid, o);
     if (lane == 0 && invalid && P.invalid_count) atomicAdd((unsigned long long *)P.invalid_count, invalid);

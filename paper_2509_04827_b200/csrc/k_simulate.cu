@@ -155,34 +155,69 @@ __device__ int lowest_itl(const WS &W, uint32_t n, uint32_t kv, double target, d
 }
 
 // The same lowest feasible level, searched from a start level k0 (the instance's previous
-// decision): on coefficient-monotone tables (A32) the feasible levels are upward closed, so a
-// walk down from a feasible k0 (or up from an infeasible one) stops at the scan's answer —
-// usually after one or two evaluations instead of up to K.
+// decision): on coefficient-monotone tables (A32) the feasible levels are upward closed, so
+// galloping from k0 (steps 1, 2, 4, ... towards the boundary, then a binary search between
+// the last infeasible and the first feasible probe) ends at the ascending scan's answer —
+// usually after two or three evaluations instead of up to K (or log2 K for a long ladder).
+// Level K-1 counts as feasible (A2: nothing feasible below it selects it).
 template <bool F, class WS>
 __device__ __forceinline__ int lowest_itl_from(const WS &W, uint32_t n, uint32_t kv, double target, int k0,
                                                double *pred) {
   const int K = (int)W.K;
-  // long ladders: the binary search of lowest_itl is bounded by log2 K (a walk is not)
-  if (!W.mono_it || K < 3 || (!F && K > 8)) return lowest_itl<F>(W, n, kv, target, pred);
+  if (!W.mono_it || K < 3) return lowest_itl<F>(W, n, kv, target, pred);
   const uint32_t j = tile_j<F>(W, n);
   const double dn = (double)n, dkv = (double)kv;
   int k = k0 < K - 2 ? k0 : K - 2;
   double p = itl_at<F>(W, j, k, dn, dkv);
+  if (F) {   // short ladders: a plain walk (fewer instructions than galloping; 77.7 vs 80.4 ms on C4)
+    if (p <= target) {
+      while (k > 0) {
+        const double q = itl_at<F>(W, j, k - 1, dn, dkv);
+        if (!(q <= target)) break;
+        --k;
+        p = q;
+      }
+    } else {
+      do {
+        ++k;
+        p = itl_at<F>(W, j, k, dn, dkv);
+      } while (k < K - 1 && !(p <= target));
+    }
+    *pred = p;
+    return k;
+  }
+  int bad, ok;            // bad: infeasible (or -1), ok: feasible (or K-1); answer in (bad, ok]
+  double pok;
   if (p <= target) {
-    while (k > 0) {
-      const double q = itl_at<F>(W, j, k - 1, dn, dkv);
-      if (!(q <= target)) break;
-      --k;
-      p = q;
+    ok = k; pok = p; bad = -1;
+    for (int step = 1; ok > 0; step <<= 1) {
+      const int q = ok - step >= 0 ? ok - step : 0;
+      const double pq = itl_at<F>(W, j, q, dn, dkv);
+      if (!(pq <= target)) { bad = q; break; }
+      ok = q; pok = pq;
+      if (q == 0) break;
     }
   } else {
-    do {
-      ++k;
-      p = itl_at<F>(W, j, k, dn, dkv);
-    } while (k < K - 1 && !(p <= target));
+    bad = k; ok = K - 1; pok = 0.0;
+    bool have = false;
+    for (int step = 1; bad < K - 2; step <<= 1) {
+      const int q = bad + step <= K - 2 ? bad + step : K - 2;
+      const double pq = itl_at<F>(W, j, q, dn, dkv);
+      if (pq <= target) { ok = q; pok = pq; have = true; break; }
+      bad = q;
+    }
+    if (!have) {          // nothing feasible below K-1 (A2)
+      *pred = itl_at<F>(W, j, K - 1, dn, dkv);
+      return K - 1;
+    }
   }
-  *pred = p;
-  return k;
+  while (ok - bad > 1) {  // (bad, ok]: bad infeasible, ok feasible
+    const int mid = (bad + ok) >> 1;
+    const double pm = itl_at<F>(W, j, mid, dn, dkv);
+    if (pm <= target) { ok = mid; pok = pm; } else bad = mid;
+  }
+  *pred = pok;
+  return ok;
 }
 
 // busy power (eq:P-f P:187, A22) with the utilisation from the launch's table (the entries

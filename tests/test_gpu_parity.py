@@ -135,6 +135,32 @@ def test_fit_parity(vt, orc, kind, T, noise, n_cell):
         assert torch.equal(out[name], out2[name])
 
 
+@pytest.mark.parametrize("kind,T,noise,n_cell", [("L8", 16, 0.05, 96), ("B200", 4, 0.0, 70)])
+def test_fit_parity_recording_order(vt, orc, kind, T, noise, n_cell):
+    """Samples in recording order (cell by cell, as one profiling run per level records them,
+    P:503): most 32-sample chunks are one cell and take K1's lane-tree path; cells of 70 / 96
+    samples also leave mixed chunks at every cell boundary."""
+    prof = synth.make_profile(kind, n_tiles=T)
+    s = profile_samples(prof, n_cell * 2, n_cell, noise_sigma=noise, seed=12, shuffle=False)
+    ref = orc.fit_profile(s["phase"], s["level"], s["n_bt"], s["n_req"], s["n_kv"], s["lat_ms"], prof.k, T, 128, 0.0)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int32) if v.dtype == np.uint32 else v).to("cuda")
+         for k, v in s.items()}
+    for k in ("n_bt", "n_req", "n_kv"):
+        d[k] = d[k].view(torch.uint32)
+    d["level"] = torch.from_numpy(s["level"].view(np.int16)).to("cuda").view(torch.uint16)
+    out = vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k, T, 128, 0.0)
+    torch.cuda.synchronize()
+    assert (out["cell_status"].cpu().numpy() == ref["cell_status"]).all()
+    for name in ("a1", "c1", "a2", "b2", "c2", "mae"):
+        g, o = out[name].cpu().numpy(), ref[name]
+        err = np.abs(g - o) / np.maximum(np.abs(o), 1e-9)
+        assert err.max() <= 1e-12 or np.abs(g - o).max() < 1e-12, (name, err.max())
+    out2 = vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k, T, 128, 0.0)
+    torch.cuda.synchronize()
+    for name in ("a1", "c1", "a2", "b2", "c2", "mae"):
+        assert torch.equal(out[name], out2[name])
+
+
 def test_fit_degenerate_and_empty(vt, orc):
     prof = synth.make_profile("L8", n_tiles=5)
     s = profile_samples(prof, 10, 12, seed=4, tiles=[0, 1, 2])

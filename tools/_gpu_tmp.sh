@@ -1,1 +1,2 @@
-timeout 1200 python bench.py --config C5 --steps 3 --warmup 2 --no-streaming --no-parity --e2e-steps 1 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C5', d['value']/1e9, d['kernel_ms'])"
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:"fit_pass|route_kernel" --launch-skip 4 -c 4 -o gpurun_out/r02l_stream python tools/prof_stream.py > /dev/null 2>&1; echo ncu $?
+timeout 300 python tools/stream_bench.py 2>&1 | tail -6

@@ -27,7 +27,7 @@ tgt = torch.rand(n, generator=g, device=dev, dtype=torch.float64) * 60 + 20
 m = 1 << 24
 nr, nk, rin = u32(0, 500, (2 * m,)), u32(500, 200000, (2 * m,)), u32(1, 4000, (m,))
 cur = torch.zeros(m, dtype=torch.int32, device=dev).view(torch.uint32)
-smp = profile_samples(prof, 32768, 32768, noise_sigma=0.02, seed=9)
+smp = profile_samples(prof, 32768, 32768, noise_sigma=0.02, seed=9, shuffle=False)
 to = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else (a.view(np.int16) if a.dtype == np.uint16 else a)).to(dev)
 d = {k: to(v) for k, v in smp.items()}
 for k in ("n_bt", "n_req", "n_kv"):

@@ -65,7 +65,8 @@ __device__ __forceinline__ Sample decode_sample(const FitParams &P, const Raw &r
     s.cell = (int)jp * P.k + (int)lv;
     s.x1 = nb;
   } else {
-    uint32_t j = tile_of(nr, (uint32_t)P.tile_w, (uint32_t)P.n_tiles);
+    uint32_t j = P.pad ? (nr - 1u) >> (P.pad - 1u) : (nr - 1u) / (uint32_t)P.tile_w;  // pad = log2 W + 1
+    j = j < (uint32_t)P.n_tiles - 1u ? j : (uint32_t)P.n_tiles - 1u;
     s.cell = P.kp + (int)j * P.k + (int)lv;
     s.x1 = nr;
     s.x2 = r.kv;
@@ -186,7 +187,6 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
   Raw buf[PF];
 #pragma unroll
   for (int u = 0; u < PF; ++u) buf[u] = load_raw(P, lo + (size_t)u * 32 + lane, lo + (size_t)u * 32 + lane < hi);
-  int slot = 0;
   // a run of one-cell chunks accumulates in registers (lane l sums its own samples in order);
   // flush: a fixed tree over the lanes, added to the warp's row once per run
   int run_cell = -1;
@@ -232,15 +232,9 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
     rx1 = rx2 = rcnt = 0;
     run_cell = -1;
   };
-  for (size_t base = lo; base < hi; base += 32) {
-    const Sample s = decode_sample(P, buf[0]);
-#pragma unroll
-    for (int u = 0; u + 1 < PF; ++u) buf[u] = buf[u + 1];
-    {
-      const size_t ni = base + (size_t)PF * 32 + lane;
-      buf[PF - 1] = load_raw(P, ni, ni < hi);
-    }
-    (void)slot;
+  // chunk processing (in sample order); the PF chunks ahead sit in a ring of registers, refilled
+  // slot by slot in a loop unrolled by PF (no register shifting)
+  auto process = [&](const Sample &s) {
     if (s.cell == -2) invalid++;
     double v[NS];
     if (PASS == 1) {
@@ -289,7 +283,7 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
 #pragma unroll
         for (int q = 0; q < NS; ++q) racc[q] = add(racc[q], v[q]);
       }
-      continue;
+      return;
     }
     flush();
     const unsigned rank = __popc(peers & ((1u << lane) - 1u));
@@ -309,6 +303,17 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32) fit_pass_kernel(const __gr
         }
       }
       __syncwarp();
+    }
+    };
+  for (size_t base = lo; base < hi; base += (size_t)PF * 32) {
+#pragma unroll
+    for (int u = 0; u < PF; ++u) {
+      const size_t cb = base + (size_t)u * 32;
+      if (cb >= hi) break;
+      const Sample s = decode_sample(P, buf[u]);
+      const size_t ni = cb + (size_t)PF * 32 + lane;
+      buf[u] = load_raw(P, ni, ni < hi);
+      process(s);
     }
   }
   flush();

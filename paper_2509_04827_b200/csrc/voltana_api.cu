@@ -226,6 +226,7 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, 
   P.n = n; P.chunk = L.chunk; P.k = k; P.n_tiles = n_tiles; P.tile_w = tile_w; P.cells = L.cells;
   P.tile_step = tile_step;
   P.n_ptiles = n_ptiles; P.kp = n_ptiles * k; P.pcut = prefill_cutoff;
+  P.pad = (tile_w & (tile_w - 1)) == 0 ? (uint32_t)__builtin_ctz((unsigned)tile_w) + 1u : 0u;  // log2 W + 1 (pow2 W)
   P.a1 = a1; P.c1 = c1; P.a2 = a2; P.b2 = b2; P.c2 = c2; P.mae = mae; P.status = cell_status;
   P.invalid_count = invalid_count;
   char *ws = (char *)workspace;

@@ -16,7 +16,7 @@ struct FitParams {
   size_t n, chunk;            // samples, samples per warp
   int32_t k, n_tiles, tile_w, cells;
   int32_t n_ptiles, kp;       // prefill tiles T_p (>= 1) and TTFT cells kp = T_p * k [F1]
-  uint32_t pcut, pad;         // prefill cutoff (N_bt above it: the last prefill tile)
+  uint32_t pcut, pad;         // prefill cutoff (N_bt above it: the last prefill tile); pad: log2 W + 1 when W is a power of two, else 0
   double tile_step;
   double *a1, *c1, *a2, *b2, *c2, *mae;
   uint8_t *status;

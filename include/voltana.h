@@ -237,7 +237,7 @@ typedef struct {            /* 128-byte per-scenario record                     
 /* Workspace of voltana_simulate for n_scenarios scenarios: the request nodes (16 B per
  * request of every scenario: n_scenarios x max_requests, or total_requests when the scenario
  * table carries node_offset — pass that total to the _ex form), plus per resident warp a
- * far-list array (4 B x max_requests), a completion log (32 KB) and decode timing wheels. */
+ * completion log (32 KB) and decode timing wheels (16 B x max N_D x 2048).               */
 size_t voltana_simulate_workspace_bytes(const voltana_traces *traces_h,
                                         const voltana_layout *layouts_h, int n_layouts,
                                         size_t n_scenarios);

@@ -194,11 +194,26 @@ __device__ __forceinline__ void scan_pair(const double *it, const DevProfile &PR
     r1 = itl_row(it, PR, K, n1, wshift);
     r0 = n == 0u ? r1 : itl_row(it, PR, K, n, wshift);
   }
-  const double dn0 = (double)n, dk0 = (double)kv, dn1 = (double)n1, dk1 = (double)kv1;
+  // (n + 1, kv + in + 1) < 2^34: exact as doubles, so the successor is formed in fp64 (no 64-bit
+  // integer adds and conversions); the values equal (double)n1 and (double)kv1
+  const double dn0 = (double)n, dk0 = (double)kv, dn1 = add(dn0, 1.0), dk1 = add(dk0, (double)(in + 1u));
   if (KK == 1) { kn = 0; ka = 0; return; }
   if (KK > 1) {
-    scan_pair_ilp<(KK > 1 ? KK : 2)>(r0, r1, dn0, dk0, dn1, dk1, target, kn, ka);
+    // both states with the row of n (the successor's tile differs only when n is a multiple of
+    // the tile width: then f' is re-scanned on its own row, a rare, per-lane fix-up instead of
+    // a second path the whole warp would execute)
+    constexpr int KQ = KK > 1 ? KK : 2;
+    const double *r = n == 0u ? r1 : r0;
+    kn = KQ - 1;
+    ka = KQ - 1;
+#pragma unroll
+    for (int k = KQ - 2; k >= 0; --k) {
+      const double a = r[3 * k], b = r[3 * k + 1], c = r[3 * k + 2];
+      if (add(add(mul(a, dn0), mul(b, dk0)), c) <= target) kn = k;
+      if (add(add(mul(a, dn1), mul(b, dk1)), c) <= target) ka = k;
+    }
     if (n == 0u) kn = 0;
+    if (r1 != r) ka = scan_itl_ilp<KQ>(r1, dn1, dk1, target);
     return;
   }
   switch (K) {

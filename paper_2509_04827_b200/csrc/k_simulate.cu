@@ -48,8 +48,10 @@ template <class T> __device__ __forceinline__ T wshfl(T v, int src) { return __s
 struct Node {       // 16 B per request (workspace, written by K4a)
   double tf;        // +t_first if the TTFT SLO was met, -t_first otherwise (t_first > 0)
   uint32_t next;    // K4b: admission-queue / wheel-bucket / far-list link
-  uint16_t in, out;
+  uint32_t io;      // in | out << 16; on the far list: the finishing iteration (see far_insert)
 };
+__device__ __forceinline__ uint32_t node_in(const Node &n) { return n.io & 0xffffu; }
+__device__ __forceinline__ uint32_t node_out(const Node &n) { return n.io >> 16; }
 
 struct RouteEnt {   // one request of the merged route stream (16 B)
   double tf;        // as Node.tf
@@ -81,6 +83,7 @@ struct WarpSmemT {
   uint32_t itl_smem, mono_it;
   uint32_t ctrl;                   // layout ctrl_mode: 0 EcoFreq, 1 energy argmin [B4]
   double ctrl_iv, fs_ov;           // window interval, blocking frequency-set overhead [C1-C3]
+  const uint32_t *tin, *tout;      // this scenario's trace lengths (far-list requests, see far_insert)
   const double *noise;             // execution-noise factor table or NULL [D1, D2]
   uint32_t noise_mask, np;         // np: N_P (decode instance d is noise instance N_P + d)
   uint64_t seed;                   // scenario hash seed (noise index)
@@ -294,7 +297,6 @@ struct Dec {               // decode instance d, owned by lane d
 
 struct Lane {              // per-lane pointers
   Node *node;
-  uint32_t *farfin;        // [N] finishing iteration of requests on the far list
   uint4 *wheel;            // this lane's decode instance: [NB] buckets
   CEnt *clog;              // the warp's completion log [CLOG_CAP]
 };
@@ -306,14 +308,14 @@ __device__ void itl_walk(Dec &D, const Lane &L, WS &W, int d, const voltana_outp
   const double slo = W.slo_itl;
   Node nd = L.node[id];
   for (uint32_t hop = 0; hop < W.max_steps; ++hop) {
-    const double itl = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
+    const double itl = div(sub(td, fabs(nd.tf)), (double)(node_out(nd) - 1u));
     D.sitl = add(D.sitl, itl);
     bool ok = itl <= slo;
     if ((V & 2) && W.itlm) {
       // ITL Max / P99 (E3): the request's gaps are e_a - t_first and the iteration gaps of
       // (a, f], f = this iteration, a = f - (out - 2); count those above the SLO from the
       // instance's rings and compare with the nearest-rank allowance (0 for Max)
-      const uint32_t n = (uint32_t)nd.out - 1u;
+      const uint32_t n = node_out(nd) - 1u;
       const uint32_t a = D.cur - (n - 1u);
       const double ea = W.re[(size_t)d * (W.rmask + 1u) + (a & W.rmask)];
       const uint32_t ca = W.rc[(size_t)d * (W.rmask + 1u) + (a & W.rmask)];
@@ -349,9 +351,11 @@ __device__ __forceinline__ void bucket_append(const Lane &L, uint32_t nbm, uint3
 }
 
 // A request finishing NB or more iterations ahead waits on the far list, sorted by
-// (finishing iteration, admission order); rare (out > NB + 1).
+// (finishing iteration, admission order); rare (out > NB + 1). While it waits, its node's io
+// field holds the finishing iteration (no per-request side array in the workspace); in and out
+// are restored from the trace when it joins its bucket.
 __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i, uint32_t fin) {
-  L.farfin[i] = fin;
+  L.node[i].io = fin;
   if (D.far_h == NIL || fin < D.far_hfin) {
     L.node[i].next = D.far_h;
     D.far_h = i;
@@ -361,7 +365,7 @@ __device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i
   uint32_t prev = D.far_h;
   for (uint32_t hop = 0; hop < max_steps; ++hop) {
     const uint32_t nx = L.node[prev].next;
-    if (nx == NIL || L.farfin[nx] > fin) break;
+    if (nx == NIL || L.node[nx].io > fin) break;
     prev = nx;
   }
   L.node[i].next = L.node[prev].next;
@@ -415,8 +419,10 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       const Node fn = L.node[i];
       const uint32_t fin = D.far_hfin;
       D.far_h = fn.next;
-      D.far_hfin = fn.next != NIL ? L.farfin[fn.next] : NIL;
-      bucket_append(L, nbm, i, fin, (uint32_t)fn.in + fn.out, lfin, lb);
+      D.far_hfin = fn.next != NIL ? L.node[fn.next].io : NIL;
+      const uint32_t io = (uint32_t)(uint16_t)W.tin[i] | (uint32_t)(uint16_t)W.tout[i] << 16;  // as K4a wrote it
+      L.node[i].io = io;
+      bucket_append(L, nbm, i, fin, (io & 0xffffu) + (io >> 16), lfin, lb);
     }
     // FCFS admission while KV fits (A20)
     const double tau = W.tau;
@@ -424,14 +430,14 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     while (D.qh != NIL) {
       const Node hn = D.qhn;
       if (!(add(fabs(hn.tf), tau) <= tnow)) break;  // still in KV transfer
-      const uint32_t need = (uint32_t)hn.in + 1u;
+      const uint32_t need = node_in(hn) + 1u;
       if (D.nkv + need > kvcap) break;
       const uint32_t i = D.qh;
       D.qh = hn.next;
       if (D.qh == NIL) D.qt = NIL;
       else D.qhn = L.node[D.qh];
-      const uint32_t fin = D.iters + (uint32_t)hn.out - 2u;  // its last iteration
-      if ((uint32_t)hn.out - 2u < W.nb) bucket_append(L, nbm, i, fin, (uint32_t)hn.in + hn.out, lfin, lb);
+      const uint32_t fin = D.iters + node_out(hn) - 2u;  // its last iteration
+      if (node_out(hn) - 2u < W.nb) bucket_append(L, nbm, i, fin, node_in(hn) + node_out(hn), lfin, lb);
       else far_insert(D, L, W.max_steps, i, fin);
       D.nreq += 1u;
       D.nkv += need;
@@ -509,7 +515,7 @@ __device__ __noinline__ void itl_pass(uint32_t m, int ND, double slo, uint32_t m
     for (uint32_t jj = 0; jj < ITL_CAP; ++jj) {
       if (id != NIL) {
         const Node nd = node[id];
-        const double x = div(sub(td, fabs(nd.tf)), (double)(nd.out - 1u));
+        const double x = div(sub(td, fabs(nd.tf)), (double)(node_out(nd) - 1u));
         const bool ok = x <= slo;
         c_ok += ok;
         c_both += ok && nd.tf > 0.0;
@@ -555,7 +561,7 @@ __device__ __noinline__ void itl_pass(uint32_t m, int ND, double slo, uint32_t m
           uint32_t rr = S.id[slot];
           for (uint32_t hop = 0; rr != NIL && hop < max_hops; ++hop) {
             const Node nd = node[rr];
-            const double itl = div(sub(t, fabs(nd.tf)), (double)(nd.out - 1u));
+            const double itl = div(sub(t, fabs(nd.tf)), (double)(node_out(nd) - 1u));
             sd = add(sd, itl);
             const bool ok = itl <= slo;
             c_ok += ok;
@@ -616,7 +622,7 @@ __device__ __forceinline__ void dec_push(Dec &D, const Lane &L, uint32_t i, doub
   if (D.qt == NIL) {  // (K4a wrote node i with next = NIL)
     D.qh = i;
     prefetch_l1(L.wheel + ((D.iters + out - 2u) & nbm));  // its bucket at the next START
-    D.qhn.tf = tf; D.qhn.next = NIL; D.qhn.in = (uint16_t)in; D.qhn.out = (uint16_t)out;
+    D.qhn.tf = tf; D.qhn.next = NIL; D.qhn.io = (uint32_t)(uint16_t)in | (uint32_t)(uint16_t)out << 16;
   } else {
     L.node[D.qt].next = i;
     if (D.qt == D.qh) D.qhn.next = i;  // keep the register copy coherent
@@ -689,6 +695,7 @@ __device__ __noinline__ uint32_t route_refill(RouteWin &R, const Node *node, uin
   const double INF = __longlong_as_double(0x7ff0000000000000ll);
   double key[NI], tf[NI];
   uint32_t io[NI], id[NI];
+  __syncwarp();  // every lane has read the old window before any lane overwrites it
 #pragma unroll
   for (int q = 0; q < NI; ++q) {
     key[q] = INF; tf[q] = 0.0; io[q] = 0u; id[q] = NIL;
@@ -696,7 +703,7 @@ __device__ __noinline__ uint32_t route_refill(RouteWin &R, const Node *node, uin
       const uint32_t x = R.sbase[q] + lane * NP;
       if (x < R.send[q]) {
         const Node nd = node[x];
-        tf[q] = nd.tf; io[q] = (uint32_t)nd.in | ((uint32_t)nd.out << 16); key[q] = fabs(nd.tf); id[q] = x;
+        tf[q] = nd.tf; io[q] = nd.io; key[q] = fabs(nd.tf); id[q] = x;
       }
     }
   }
@@ -998,8 +1005,7 @@ __device__ __forceinline__ void pa_account(const SimParams &P, PCtxS &C, PState 
     Node me;
     me.tf = ok ? e : -e;
     me.next = NIL;
-    me.in = (uint16_t)x;
-    me.out = (uint16_t)o;
+    me.io = (uint32_t)(uint16_t)x | (uint32_t)(uint16_t)o << 16;
     node[i] = me;
   }
 }
@@ -1292,6 +1298,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   // ---------------------------------------------------------------- stage constants and tables
   const uint32_t K = (uint32_t)GR.k, T = (uint32_t)PR.n_tiles;
   if (lane == 0) {
+    W.tin = P.in_len + off; W.tout = P.out_len + off;
     W.tau = LY.kv_transfer_ms; W.slo_itl = SL.itl_ms; W.slo_ttft = SL.ttft_ms;
     W.tgt_itl = mul(SL.scale, SL.itl_ms);   // A3
     W.tgt_ttft = mul(SL.scale, SL.ttft_ms);
@@ -1349,6 +1356,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   // N_D = 2 EcoRoute decision table (fast kernel, K <= 5)
   const bool lut_on = (V & 4) || (F && LY.policy == 0 && ND == 2 && K <= (uint32_t)ECO_LUT_K);
+  __syncwarp();  // the staged ladder (W.mhz) is complete before any lane reads it
   if (lut_on) eco_lut_build(W.lut, (int)K, W.mhz, LY.delta_mhz);
   Node *node = (Node *)node_base(P, s);
   const uint64_t h0 = P.hash_seed[s];
@@ -1363,8 +1371,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   const int dl = lane < ND ? lane : 0;
   Lane L;
   L.node = node;
-  L.farfin = (uint32_t *)slot;
-  L.clog = (CEnt *)(slot + P.far_bytes);
+  L.clog = (CEnt *)slot;
   L.wheel = wheels + (size_t)dl * P.nb;
   if (lane == 0) W.clog_m = (uint32_t)ND * CLOG_CHUNK;  // the first chunk of every decode lane
   Dec D;
@@ -1381,7 +1388,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   D.ebusy = D.bms = D.top = D.sitl = 0.0;
   D.h = h0; D.n_itl_ok = D.n_both = 0;
   D.bcur = make_uint4(0u, 0u, 0u, 0u);
-  D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.in = 0; D.qhn.out = 0;
+  D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.io = 0u;
   Err dE = {INF, 0};
   double k_sd = 0.0;                                // deferred ITL pass: lane d's instance sum
   uint32_t k_ok = 0u, k_both = 0u;                  // ... and this lane's counts

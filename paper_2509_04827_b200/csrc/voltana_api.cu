@@ -262,7 +262,7 @@ uint32_t wheel_buckets(uint32_t max_out) {
 }
 
 struct SimLayout {
-  size_t far, slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
+  size_t slot, wheel_per_slot, slots_off, wheels_off, total, smem_per_warp, smem, utab_off;
   uint32_t n_slots, nb, itl_smem, ring_r = 0, ring_nd = 0, ks_off = 0;
   size_t ring_e_off = 0, ring_c_off = 0;
   size_t nodes_off = 0, pares_off = 0, rtab_off = 0;
@@ -311,9 +311,8 @@ SimLayout sim_layout(const voltana_traces *tr, const voltana_layout *lays, int n
   L.smem_per_warp = block(L.itl_smem != 0u);
   L.ks_off = (uint32_t)(L.smem_per_warp - ((sizeof(ItlScratch) + 15) & ~(size_t)15));  // ITL-pass scratch
   L.smem = L.smem_per_warp * (SIM_THREADS / 32);
-  // per resident warp: far-list finishing iterations [max_requests], then the completion log
-  L.far = align256((size_t)tr->max_requests * 4);
-  L.slot = L.far + (size_t)CLOG_CAP * sizeof(CEnt);
+  // per resident warp: the completion log
+  L.slot = (size_t)CLOG_CAP * sizeof(CEnt);
   L.wheel_per_slot = (size_t)max_nd(lays, n_layouts) * L.nb;
   size_t rw = (size_t)resident_warps(L.smem);
   L.n_slots = (uint32_t)(n < rw ? (n < 1 ? 1 : n) : rw);
@@ -496,7 +495,6 @@ voltana_status voltana_simulate_ex(const voltana_traces *traces_h, const voltana
   P->counter = (uint32_t *)ws;
   P->slots = ws + L.slots_off;
   P->slot_bytes = L.slot;
-  P->far_bytes = L.far;
   P->wheels = (uint4 *)(ws + L.wheels_off);
   if (L.ring_r) {
     P->ring_e = (double *)(ws + L.ring_e_off);

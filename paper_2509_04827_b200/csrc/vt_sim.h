@@ -72,8 +72,8 @@ struct SimParams {
   voltana_result *out;
   // workspace
   uint32_t *counter;
-  char *slots;                 // [n_slots][slot_bytes]: far-list finishing iterations [max_requests] u32,
-  size_t slot_bytes, far_bytes;//   then the completion log [CLOG_CAP] CEnt
+  char *slots;                 // [n_slots][slot_bytes]: the completion log [CLOG_CAP] CEnt
+  size_t slot_bytes;
   uint4 *wheels;               // [n_slots][wheel_per_slot]: decode timing wheels (16-B buckets, 0 = empty)
   size_t wheel_per_slot;       // max N_D * nb buckets
   uint32_t itl_smem;           // stage the ladder's ITL table in shared memory

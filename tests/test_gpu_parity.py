@@ -285,6 +285,28 @@ def test_simulate_wheel_bucket_reuse(vt, orc):
         _one(vt, orc, arr, inl, outl, 4000.0, p, Slo(600, 60), Layout(2, 1, kv_capacity=cap), [0, 27])
 
 
+def test_simulate_far_list(vt, orc):
+    """Many requests finishing more than the wheel's 2048 iterations ahead (out up to 6000): the
+    far list's sorted insertion with equal finishing iterations from different admissions, its
+    node field holding the finishing iteration, and the in/out restored when a request joins its
+    bucket (ITL accounting reads out afterwards), in the default and the variant kernel."""
+    p = synth.make_profile("L8")
+    rng = np.random.default_rng(11)
+    n = 700
+    arr = np.sort(rng.uniform(0, 30000, n))
+    arr[100:140] = arr[100]                                            # one START admits 40 at once
+    outl = rng.integers(1, 200, n)
+    outl[::3] = 2050 + rng.integers(0, 3, len(outl[::3])) * 1000      # 2050 / 3050 / 4050: equal fins
+    outl[1::29] = 6000
+    outl[5::41] = 2050                                                 # exactly at the far threshold
+    outl[6::41] = 2049
+    inl = rng.integers(1, 2500, n)
+    lad5 = [0, 6, 13, 20, 27]
+    for lay in (Layout(1, 2), Layout(2, 2, kv_capacity=60000), Layout(3, 1, kv_transfer_ms=3.0),
+                Layout(2, 2, itl_mode=2), Layout(1, 3, itl_mode=1, freq_overhead_ms=3.0)):
+        _one(vt, orc, arr, inl, outl, 30000.0, p, Slo(600, 60), lay, lad5)
+
+
 def test_simulate_invalid_trace_status(vt, orc):
     p = synth.make_profile("L8")
     r = _one(vt, orc, [5.0, 1.0], [10, 10], [5, 5], 100.0, p, Slo(600, 60), Layout(1, 1), [0, 27])

@@ -5,7 +5,7 @@
 set -u
 OUT=${1:-gpurun_out/sanitize}
 mkdir -p "$OUT"
-SEL='test_simulate_c1_full or test_simulate_edge_cases or test_simulate_wheel_bucket_reuse or test_simulate_prefill_windows or test_simulate_configs_reduced or test_random_scenarios or test_fit_parity or test_route_batch_parity or test_control_step_parity or test_simulate_itl_modes or test_simulate_noise_parity or test_outputs_c1_full'
+SEL='test_simulate_c1_full or test_simulate_edge_cases or test_simulate_wheel_bucket_reuse or test_simulate_far_list or test_simulate_prefill_windows or test_simulate_configs_reduced or test_random_scenarios or test_fit_parity or test_route_batch_parity or test_control_step_parity or test_simulate_itl_modes or test_simulate_noise_parity or test_outputs_c1_full'
 : > "$OUT/summary.txt"
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""

@@ -168,25 +168,31 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
 
 // ------------------------------------------------------------------ K1
 namespace {
-struct FitLayout { int cells, wpb, blocks; size_t chunk, part, red, means, cnt, ticket, total; };
+struct FitLayout { int cells, wpb, blocks; size_t chunk, rows, part, red, means, cnt, ticket, total; };
 
 FitLayout fit_layout(size_t n, int k, int n_tiles, int n_ptiles) {
   FitLayout L;
   L.cells = (n_ptiles < 1 ? 1 : n_ptiles) * k + n_tiles * k;
   L.wpb = fit_warps_per_block(L.cells);
 #ifndef VT_FIT_SPW
-#define VT_FIT_SPW 2048
+#define VT_FIT_SPW 256
 #endif
-  size_t warps_want = (n + VT_FIT_SPW - 1) / VT_FIT_SPW;  // >= VT_FIT_SPW samples per warp
-  size_t cap = (size_t)sm_count() * 2 * L.wpb;         // two CTAs per SM at most
-  size_t warps = warps_want < 1 ? 1 : (warps_want < cap ? warps_want : cap);
-  L.blocks = (int)((warps + L.wpb - 1) / L.wpb);
+  // co-resident CTAs (cooperative launch): the occupancy of this device, else an upper bound
+  // from the shared-memory and thread limits (the workspace is sized by the bound)
+  const int bound = sm_count() * FIT_CTAS_PER_SM;
+  const int occ = fit_max_blocks(L.cells, L.wpb);
+  const int cap = occ > 0 && occ < bound ? occ : bound;
+  size_t warps_want = (n + VT_FIT_SPW - 1) / VT_FIT_SPW;  // >= VT_FIT_SPW samples per warp (small n: more CTAs)
+  size_t want_b = (warps_want + L.wpb - 1) / L.wpb;
+  L.blocks = (int)(want_b < 1 ? 1 : (want_b < (size_t)cap ? want_b : (size_t)cap));
   size_t tw = (size_t)L.blocks * L.wpb;
   L.chunk = (n + tw - 1) / tw;
-  L.chunk = (L.chunk + 31) & ~(size_t)31;
-  if (L.chunk == 0) L.chunk = 32;
-  L.part = 0;
-  L.red = align256(L.part + (size_t)L.blocks * L.cells * 5 * sizeof(double));
+  L.chunk = (L.chunk + 127) & ~(size_t)127;
+  if (L.chunk == 0) L.chunk = 128;
+  const int pb = bound > L.blocks ? bound : L.blocks;   // partials and rows for any grid up to the bound
+  L.rows = 0;
+  L.part = align256(L.rows + (size_t)pb * L.wpb * L.cells * 5 * sizeof(double));
+  L.red = align256(L.part + (size_t)pb * L.cells * 5 * sizeof(double));
   L.means = align256(L.red + (size_t)L.cells * 5 * sizeof(double));
   L.cnt = align256(L.means + (size_t)L.cells * 3 * sizeof(double));
   L.ticket = align256(L.cnt + (size_t)L.cells * sizeof(uint64_t));
@@ -216,13 +222,15 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, 
     return fail(VOLTANA_E_INVALID_ARG, "fit_profile: null sample pointer");
   if (!std::isfinite(tile_step)) return fail(VOLTANA_E_INVALID_ARG, "fit_profile: tile_step not finite");
   FitLayout L = fit_layout(n, k, n_tiles, n_ptiles);
-  if (L.cells * 5 * sizeof(double) * (size_t)L.wpb > 227 * 1024)
+  if (fit_smem_bytes(L.cells, L.wpb) > 227 * 1024)
     return fail(VOLTANA_E_INVALID_ARG, "fit_profile: %d cells exceed shared memory", L.cells);
   if (!workspace || ws_bytes < L.total)
     return fail(VOLTANA_E_WORKSPACE, "fit_profile: workspace %zu < %zu bytes", ws_bytes, L.total);
   FitParams P;
   memset(&P, 0, sizeof(P));
   P.phase = phase; P.level = level; P.n_bt = n_bt; P.n_req = n_req; P.n_kv = n_kv; P.lat = lat_ms;
+  const uintptr_t al = (uintptr_t)n_bt | (uintptr_t)n_req | (uintptr_t)n_kv | (uintptr_t)lat_ms;
+  P.vec = ((uintptr_t)phase & 3u) == 0 && ((uintptr_t)level & 7u) == 0 && (al & 15u) == 0 ? 1 : 0;
   P.n = n; P.chunk = L.chunk; P.k = k; P.n_tiles = n_tiles; P.tile_w = tile_w; P.cells = L.cells;
   P.tile_step = tile_step;
   P.n_ptiles = n_ptiles; P.kp = n_ptiles * k; P.pcut = prefill_cutoff;
@@ -230,6 +238,8 @@ voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level, 
   P.a1 = a1; P.c1 = c1; P.a2 = a2; P.b2 = b2; P.c2 = c2; P.mae = mae; P.status = cell_status;
   P.invalid_count = invalid_count;
   char *ws = (char *)workspace;
+  P.rows = (double *)(ws + L.rows);
+  P.bmw = (L.cells + 31) / 32;
   P.part = (double *)(ws + L.part);
   P.red = (double *)(ws + L.red);
   P.means = (double *)(ws + L.means);

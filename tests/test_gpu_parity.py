@@ -344,3 +344,31 @@ def test_simulate_prefill_windows_and_completion_log(vt, orc):
         _one(vt, orc, arr, inl, outl, float(arr[-1]) + 1000.0, p, Slo(600, 60), lay, lad5)
     # Delta = 0 with a 2-level ladder: EcoRoute keeps choosing one instance (skewed completion logs)
     _one(vt, orc, arr, inl, outl, float(arr[-1]) + 1000.0, p, Slo(600, 60), Layout(1, 2, delta_mhz=0), [0, 27])
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_fit_parity_unaligned_and_ragged(vt, orc, shuffle):
+    """K1 with sample arrays that start one element into their allocations (no vector loads:
+    the element-by-element path) and a count that is not a multiple of the 128-sample chunk."""
+    prof = synth.make_profile("L8", n_tiles=6)
+    s = profile_samples(prof, 150, 90, noise_sigma=0.03, seed=21, shuffle=shuffle)
+    n = len(s["lat_ms"]) - 37
+    s = {k: v[:n] for k, v in s.items()}
+    ref = orc.fit_profile(s["phase"], s["level"], s["n_bt"], s["n_req"], s["n_kv"], s["lat_ms"], prof.k, 6, 128, 0.5)
+
+    def dev(a, view=None):
+        pad = np.concatenate([a[:1], a])                    # element 0 is padding
+        t = torch.from_numpy(pad.view(view) if view else pad).to("cuda")
+        return t[1:]
+
+    d = {"phase": dev(s["phase"]), "level": dev(s["level"], np.int16).view(torch.uint16),
+         "lat_ms": dev(s["lat_ms"])}
+    for k in ("n_bt", "n_req", "n_kv"):
+        d[k] = dev(s[k], np.int32).view(torch.uint32)
+    out = vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k, 6, 128, 0.5)
+    torch.cuda.synchronize()
+    assert (out["cell_status"].cpu().numpy() == ref["cell_status"]).all()
+    for name in ("a1", "c1", "a2", "b2", "c2", "mae"):
+        g, o = out[name].cpu().numpy(), ref[name]
+        err = np.abs(g - o) / np.maximum(np.abs(o), 1e-9)
+        assert err.max() <= 1e-12 or np.abs(g - o).max() < 1e-12, (name, err.max())

@@ -14,9 +14,11 @@ data = [r for r in rows[h + 1:] if r and r[0].startswith("0x")]
 base = int(data[0][0], 16)
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
-cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout.splitlines()
-st = next(i for i, l in enumerate(dis) if l.startswith("//--------------------- .text." + kern))
+for cub in sorted(f for f in os.listdir(d) if f.endswith(".cubin")):   # the cubin holding the kernel
+    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, cub)], capture_output=True, text=True).stdout.splitlines()
+    st = next((i for i, l in enumerate(dis) if l.startswith("//--------------------- .text." + kern)), None)
+    if st is not None:
+        break
 line_of, cur = {}, "?"
 for l in dis[st + 1:]:
     if l.startswith("//--------------------- .text."):
@@ -38,6 +40,10 @@ for f in ("k_simulate.cu", "k_decide.cu", "k_fit.cu"):
     p = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2509_04827_b200", "csrc", f)
     src[f] = open(p).read().splitlines()
 sel = [(k, v) for k, v in inst.items() if k.split(":")[0] in src and lo <= int(k.split(":")[1]) <= hi]
-for k, v in sorted(sel, key=lambda kv: -kv[1])[:top]:
+if os.environ.get("OTHER"):
+    for k in sorted(samp, key=lambda k: -samp[k])[:12]:
+        print(f"{100*samp[k]/T:5.1f}% {inst[k]/units:7.2f}/u  {k}")
+    sys.exit(0)
+for k, v in sorted(sel, key=lambda kv: -(samp[kv[0]] if os.environ.get("BY_STALL") else kv[1]))[:top]:
     f, n = k.split(":")
     print(f"{v / units:7.1f}/u {100 * samp[k] / T:5.1f}%  {k:20s} {src[f][int(n) - 1].strip()[:90]}")

@@ -69,6 +69,15 @@ struct RouteWin {   // the merged window of the prefill streams (per warp, share
   uint32_t send[NI];   // stream end: ids >= send[p] were not written (K4a stopped on an error)
 };
 
+// Cold per-instance state of decode lane d (shared memory: fewer live registers on the route
+// chain; touched once per iteration START, or rarely)
+struct DecCold {
+  double ebusy, bms, top, sitl;    // busy energy (W*ms), busy time, top-level time, ITL sum (V & 2)
+  uint64_t h;                      // decision-hash chain (A36)
+  uint32_t far_h, far_hfin;        // far list head and its finishing iteration (NIL: empty)
+  uint32_t n_itl_ok, n_both;       // in-line ITL accounting counts (V & 2)
+};
+
 // Per-warp shared-memory block (one scenario at a time). Sized by sim_smem_fixed.
 template <int KC>  // KC: level capacity of the staged tables (8 in the fast-table kernel, else 64)
 struct WarpSmemT {
@@ -93,6 +102,7 @@ struct WarpSmemT {
   uint32_t clog_m;                 // completion-log slots handed out (chunks of CLOG_CHUNK)
   uint32_t wo;                     // window control or blocking overhead active (C1-C3)
   uint32_t dl_vc[NI];              // decode lane: gaps above the ITL SLO so far
+  DecCold dc[NI];                  // decode lane d's cold state
   uint64_t rq_base, it_base;       // outputs (E1-E3): request / iteration-slot base of the scenario
   uint32_t rq_on, it_on;
   // ---- variant-kernel per-instance controller state [C1-C3]
@@ -284,13 +294,12 @@ struct Err {               // first error of one lane in its own event order
   uint32_t code;
 };
 
-struct Dec {               // decode instance d, owned by lane d
-  uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt, n_itl_ok, n_both, far_h, far_hfin;
+struct Dec {               // decode instance d, owned by lane d (hot state; the cold rest in WarpSmemT::dc)
+  uint32_t nreq, nkv, pn, pkv, iters, cur, qh, qt;
   int klast;               // the last EcoFreq level found by the search (start of the next one)
   uint32_t lpos, lend;     // this lane's chunk [lpos, lend) of the completion log
   bool busy, dead, lneed;  // lneed: the chunk is full, dec_advance stopped before an END
-  double end, ebusy, bms, top, sitl;
-  uint64_t h;
+  double end;
   uint4 bcur;              // bucket of the running iteration, read at its START (final by then)
   Node qhn;                // register copy of the admission-queue head node
 };
@@ -309,7 +318,7 @@ __device__ void itl_walk(Dec &D, const Lane &L, WS &W, int d, const voltana_outp
   Node nd = L.node[id];
   for (uint32_t hop = 0; hop < W.max_steps; ++hop) {
     const double itl = div(sub(td, fabs(nd.tf)), (double)(node_out(nd) - 1u));
-    D.sitl = add(D.sitl, itl);
+    W.dc[d].sitl = add(W.dc[d].sitl, itl);
     bool ok = itl <= slo;
     if ((V & 2) && W.itlm) {
       // ITL Max / P99 (E3): the request's gaps are e_a - t_first and the iteration gaps of
@@ -323,8 +332,8 @@ __device__ void itl_walk(Dec &D, const Lane &L, WS &W, int d, const voltana_outp
       const uint32_t allow = W.itlm == 1u ? 0u : n - (99u * n + 99u) / 100u;
       ok = viol <= allow;
     }
-    D.n_itl_ok += ok;
-    D.n_both += ok && nd.tf > 0.0;
+    W.dc[d].n_itl_ok += ok;
+    W.dc[d].n_both += ok && nd.tf > 0.0;
     if ((V & 2) && W.rq_on) {  // per-request record (E1)
       O.req_tdone[W.rq_base + id] = td;
       O.req_itl[W.rq_base + id] = itl;
@@ -354,15 +363,15 @@ __device__ __forceinline__ void bucket_append(const Lane &L, uint32_t nbm, uint3
 // (finishing iteration, admission order); rare (out > NB + 1). While it waits, its node's io
 // field holds the finishing iteration (no per-request side array in the workspace); in and out
 // are restored from the trace when it joins its bucket.
-__device__ void far_insert(Dec &D, const Lane &L, uint32_t max_steps, uint32_t i, uint32_t fin) {
+__device__ void far_insert(DecCold &C, const Lane &L, uint32_t max_steps, uint32_t i, uint32_t fin) {
   L.node[i].io = fin;
-  if (D.far_h == NIL || fin < D.far_hfin) {
-    L.node[i].next = D.far_h;
-    D.far_h = i;
-    D.far_hfin = fin;
+  if (C.far_h == NIL || fin < C.far_hfin) {
+    L.node[i].next = C.far_h;
+    C.far_h = i;
+    C.far_hfin = fin;
     return;
   }
-  uint32_t prev = D.far_h;
+  uint32_t prev = C.far_h;
   for (uint32_t hop = 0; hop < max_steps; ++hop) {
     const uint32_t nx = L.node[prev].next;
     if (nx == NIL || L.node[nx].io > fin) break;
@@ -414,12 +423,13 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
     uint4 lb = make_uint4(0u, 0u, 0u, 0u);
     // far requests whose finishing iteration entered the window join their bucket now,
     // before any direct admission can reach that bucket (admission order, A37)
-    while (D.far_hfin - D.iters < W.nb) {   // (an empty far list has far_hfin = NIL)
-      const uint32_t i = D.far_h;
+    DecCold &C = W.dc[d];
+    while (C.far_hfin - D.iters < W.nb) {   // (an empty far list has far_hfin = NIL)
+      const uint32_t i = C.far_h;
       const Node fn = L.node[i];
-      const uint32_t fin = D.far_hfin;
-      D.far_h = fn.next;
-      D.far_hfin = fn.next != NIL ? L.node[fn.next].io : NIL;
+      const uint32_t fin = C.far_hfin;
+      C.far_h = fn.next;
+      C.far_hfin = fn.next != NIL ? L.node[fn.next].io : NIL;
       const uint32_t io = (uint32_t)(uint16_t)W.tin[i] | (uint32_t)(uint16_t)W.tout[i] << 16;  // as K4a wrote it
       L.node[i].io = io;
       bucket_append(L, nbm, i, fin, (io & 0xffffu) + (io >> 16), lfin, lb);
@@ -438,7 +448,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       else D.qhn = L.node[D.qh];
       const uint32_t fin = D.iters + node_out(hn) - 2u;  // its last iteration
       if (node_out(hn) - 2u < W.nb) bucket_append(L, nbm, i, fin, node_in(hn) + node_out(hn), lfin, lb);
-      else far_insert(D, L, W.max_steps, i, fin);
+      else far_insert(W.dc[d], L, W.max_steps, i, fin);
       D.nreq += 1u;
       D.nkv += need;
       D.pn -= 1u;
@@ -461,7 +471,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       if (backlog) { k = (int)W.K - 1; dur = itl_at<F>(W, tile_j<F>(W, D.nreq), k, (double)D.nreq, (double)D.nkv); }
       else if ((V & 1) && W.ctrl) k = energy_itl<F>(W, D.nreq, D.nkv, W.tgt_itl, &dur);  // B4
       else { k = lowest_itl_from<F>(W, D.nreq, D.nkv, W.tgt_itl, D.klast, &dur); D.klast = k; }
-      D.h = fold(D.h, 2, (uint64_t)d, (uint64_t)k, 0);
+      C.h = fold(C.h, 2, (uint64_t)d, (uint64_t)k, 0);
       if ((V & 2) && W.wo) { W.dl_last[d] = tnow; W.dl_ndec[d] += 1u; }
     }
     if (!(dur > 0.0)) { E.t = tnow; E.code = VOLTANA_ITEM_E_CONTRACT; D.dead = true; return; }
@@ -484,9 +494,9 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       W.re[ro] = D.end;
       W.rc[ro] = W.dl_vc[d];
     }
-    D.ebusy = add(D.ebusy, mul(bpow(W, 1, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
-    D.bms = add(D.bms, dur);
-    if (k == (int)W.K - 1) D.top = add(D.top, dur);
+    C.ebusy = add(C.ebusy, mul(bpow(W, 1, W.dyn[W.K + k], D.nreq), dur));  // W*ms, A23
+    C.bms = add(C.bms, dur);
+    if (k == (int)W.K - 1) C.top = add(C.top, dur);
     D.cur = D.iters;
     D.iters += 1u;
     D.bcur = L.wheel[D.cur & nbm];  // final now: read at the END of this iteration
@@ -1378,15 +1388,18 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   D.nreq = D.nkv = D.pn = D.pkv = D.iters = D.cur = 0;
   D.klast = 0;
   D.qh = D.qt = NIL;
-  D.far_h = D.far_hfin = NIL;
   D.busy = false;
   D.dead = !(lane < ND);
   D.end = 0.0;
   D.lpos = (uint32_t)lane * CLOG_CHUNK;  // first chunks: one per lane, allocated in lane order
   D.lend = D.lpos + CLOG_CHUNK;
   D.lneed = false;
-  D.ebusy = D.bms = D.top = D.sitl = 0.0;
-  D.h = h0; D.n_itl_ok = D.n_both = 0;
+  if (lane < NI) {
+    DecCold &C = W.dc[lane];
+    C.ebusy = C.bms = C.top = C.sitl = 0.0;
+    C.h = h0; C.n_itl_ok = C.n_both = 0;
+    C.far_h = C.far_hfin = NIL;
+  }
   D.bcur = make_uint4(0u, 0u, 0u, 0u);
   D.qhn.tf = 0.0; D.qhn.next = NIL; D.qhn.io = 0u;
   Err dE = {INF, 0};
@@ -1624,24 +1637,20 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
   }
   const double horizon = Dur > tl ? Dur : tl;  // A23
   // decode instances: lane d's totals gathered in instance order (A36/A37)
-  uint64_t hd_[NI];
-  double topd_[NI];
   double sitl = 0.0, edb = 0.0, edi = 0.0, bd = 0.0;
-  const double my_sitl = (V & 2) ? D.sitl : k_sd;
+  const double my_sitl = (V & 2) ? 0.0 : k_sd;
 #pragma unroll
   for (int d = 0; d < NI; ++d) {
-    hd_[d] = wshfl(D.h, d);
     if (d < ND) {
-      sitl = add(sitl, wshfl(my_sitl, d));
-      topd_[d] = wshfl(D.top, d);
-      edb = add(edb, div(wshfl(D.ebusy, d), 1000.0));
-      const double b = wshfl(D.bms, d);
+      sitl = add(sitl, (V & 2) ? W.dc[d].sitl : wshfl(my_sitl, d));
+      edb = add(edb, div(W.dc[d].ebusy, 1000.0));
+      const double b = W.dc[d].bms;
       edi = add(edi, energy_j(W.p_idle, sub(horizon, b)));
       bd = add(bd, b);
     }
   }
-  uint32_t c_itl = __reduce_add_sync(FULL, (lane < ND ? D.n_itl_ok : 0u) + k_ok);
-  uint32_t c_both = __reduce_add_sync(FULL, (lane < ND ? D.n_both : 0u) + k_both);
+  uint32_t c_itl = __reduce_add_sync(FULL, (lane < ND ? W.dc[lane].n_itl_ok : 0u) + k_ok);
+  uint32_t c_both = __reduce_add_sync(FULL, (lane < ND ? W.dc[lane].n_both : 0u) + k_both);
   const uint32_t c_di = __reduce_add_sync(FULL, lane < ND ? D.iters : 0u);
   if (lane == 0) {
     voltana_result R = voltana_result{};
@@ -1660,8 +1669,8 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
 #pragma unroll
     for (int d = 0; d < NI; ++d)
       if (d < ND) {
-        hh = splitmix64(hh ^ hd_[d]);
-        top = add(top, topd_[d]);  // one running sum: prefill instances, then decode (A37)
+        hh = splitmix64(hh ^ W.dc[d].h);
+        top = add(top, W.dc[d].top);  // one running sum: prefill instances, then decode (A37)
       }
     R.status = 0; R.n_requests = N;
     R.n_ttft_ok = c_ttft; R.n_itl_ok = c_itl_p + c_itl; R.n_both_ok = c_both_p + c_both; R.prefill_iters = c_pi;

@@ -332,13 +332,87 @@ control_kernel(const __grid_constant__ ControlParams P) {
 }
 
 // ---------------------------------------------------------------- K3 route_batch
+// EcoRoute's case analysis (A13-A17) from each instance's lowest feasible level now
+// (kn) and after the hypothetical addition (ka): the candidate set (bit d) and the case 1-5.
+template <int NI>
+__device__ __forceinline__ unsigned eco_levels(const int *kn, const int *ka, const int *smi, int ND, int32_t delta,
+                                               int &cse) {
+  unsigned inset = 0;
+  int fnow[NI], faft[NI];
+  int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
+#pragma unroll
+  for (int d = 0; d < NI; ++d) {
+    fnow[d] = faft[d] = 0;
+    if (d < ND) {
+      fnow[d] = smi[kn[d]];
+      faft[d] = smi[ka[d]];
+      const bool cr = faft[d] > fnow[d];                                                 // A13
+      ncross += cr;
+      if (!cr && fnow[d] < mu) mu = fnow[d];
+      if (cr && faft[d] < mr) mr = faft[d];
+      if (fnow[d] < mn) mn = fnow[d];
+      if (faft[d] < ma) ma = faft[d];
+    }
+  }
+  if (ncross == 0) {
+#pragma unroll
+    for (int d = 0; d < NI; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
+    cse = __popc(inset) == 1 ? 1 : 2;
+  } else if (ncross < ND) {
+    const long long g = (long long)mu - (long long)mr;                                  // A14, A15
+    if (g <= (long long)delta) {
+#pragma unroll
+      for (int d = 0; d < NI; ++d)
+        if (d < ND && !(faft[d] > fnow[d]) && fnow[d] == mu) inset |= 1u << d;
+      cse = 3;
+    } else {
+#pragma unroll
+      for (int d = 0; d < NI; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
+      cse = 4;
+    }
+  } else {
+#pragma unroll
+    for (int d = 0; d < NI; ++d) if (d < ND && faft[d] == ma) inset |= 1u << d;
+    cse = 5;
+  }
+  return inset;
+}
+
+// round robin among the candidate set from the cursor (A17)
+__device__ __forceinline__ uint32_t rr_pick(unsigned inset, int ND, uint32_t &cursor) {
+  const unsigned rot = ((inset >> cursor) | (inset << (ND - cursor))) & ((1u << ND) - 1u);
+  uint32_t d = cursor + (uint32_t)ffs0(rot);   // < 2 N_D: wrap without a division
+  d = d >= (uint32_t)ND ? d - (uint32_t)ND : d;
+  if (__popc(inset) >= 2) cursor = d + 1u >= (uint32_t)ND ? 0u : d + 1u;
+  return d;
+}
+
+// N_D = 2 decision table over (kn0, ka0, kn1, ka1, cursor): dsel | case << 1 | new cursor << 4,
+// filled by the CTA from eco_levels (so it is the same decision); 2 K^4 bytes
+__device__ void build_route_lut(uint8_t *lut, int K, const int *smi, int32_t delta) {
+  const int n = 2 * K * K * K * K;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    int r = e >> 1;
+    const int ka1 = r % K; r /= K;
+    const int kn1 = r % K; r /= K;
+    const int ka0 = r % K; r /= K;
+    const int kn0 = r;
+    const int kn[2] = {kn0, kn1}, ka[2] = {ka0, ka1};
+    int cse;
+    const unsigned inset = eco_levels<2>(kn, ka, smi, 2, delta, cse);
+    uint32_t cur = (uint32_t)(e & 1);
+    const uint32_t d = rr_pick(inset, 2, cur);
+    lut[e] = (uint8_t)(d | (uint32_t)cse << 1 | cur << 4);
+  }
+}
+
 // One EcoRoute decision on caller-given effective states; NI = the kernel's
 // instance bound (2, 4 or 8), so the per-instance arrays stay in registers at that size.
 template <int NI, int KK>
 __device__ __forceinline__ void route_item(const RouteParams &P, const double *it, const double *dy, const int *smi,
                                            int K, int ND, int wshift, uint32_t in, double tgt, uint32_t &cursor,
                                            const uint32_t *n, const uint32_t *kv, uint16_t &dsel, uint8_t &cse,
-                                           uint8_t &st) {
+                                           uint8_t &st, const uint8_t *lut) {
   bool bad = cursor >= (uint32_t)ND || in == 0u;
 #pragma unroll
   for (int d = 0; d < NI; ++d)
@@ -396,51 +470,24 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
       if (d < ND && (any ? (feas[d] && score[d] == m) : tmax[d] == m)) inset |= 1u << d;
     cse = any ? 6 : 7;
   } else {
-  int fnow[NI], faft[NI];
-  int ncross = 0, mu = 0x7fffffff, mr = 0x7fffffff, mn = 0x7fffffff, ma = 0x7fffffff;
+    int kn[NI], ka[NI];
 #pragma unroll
-  for (int d = 0; d < NI; ++d) {
-    fnow[d] = faft[d] = 0;
-    if (d < ND) {
-      int kn, ka;   // A10-A12
-      scan_pair<KK>(it, P.prof, K, n[d], kv[d], in, tgt, wshift, kn, ka);
-      fnow[d] = smi[kn];
-      faft[d] = smi[ka];
-      const bool cr = faft[d] > fnow[d];                                                 // A13
-      ncross += cr;
-      if (!cr && fnow[d] < mu) mu = fnow[d];
-      if (cr && faft[d] < mr) mr = faft[d];
-      if (fnow[d] < mn) mn = fnow[d];
-      if (faft[d] < ma) ma = faft[d];
+    for (int d = 0; d < NI; ++d) {
+      kn[d] = ka[d] = 0;
+      if (d < ND) scan_pair<KK>(it, P.prof, K, n[d], kv[d], in, tgt, wshift, kn[d], ka[d]);   // A10-A12
     }
-  }
-  if (ncross == 0) {
-#pragma unroll
-    for (int d = 0; d < NI; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
-    cse = __popc(inset) == 1 ? 1 : 2;
-  } else if (ncross < ND) {
-    const long long g = (long long)mu - (long long)mr;                                  // A14, A15
-    if (g <= (long long)P.delta) {
-#pragma unroll
-      for (int d = 0; d < NI; ++d)
-        if (d < ND && !(faft[d] > fnow[d]) && fnow[d] == mu) inset |= 1u << d;
-      cse = 3;
-    } else {
-#pragma unroll
-      for (int d = 0; d < NI; ++d) if (d < ND && fnow[d] == mn) inset |= 1u << d;
-      cse = 4;
+    if (NI == 2 && lut) {   // N_D = 2, K <= 8: the case analysis as a table (built by eco_levels)
+      const uint32_t v = lut[((((uint32_t)(kn[0] * K + ka[0]) * K + kn[NI - 1]) * K + ka[NI - 1]) << 1) | cursor];
+      dsel = (uint16_t)(v & 1u);
+      cse = (uint8_t)((v >> 1) & 7u);
+      cursor = v >> 4;
+      return;
     }
-  } else {
-#pragma unroll
-    for (int d = 0; d < NI; ++d) if (d < ND && faft[d] == ma) inset |= 1u << d;
-    cse = 5;
+    int c;
+    inset = eco_levels<NI>(kn, ka, smi, ND, P.delta, c);
+    cse = (uint8_t)c;
   }
-  }
-  const unsigned rot = ((inset >> cursor) | (inset << (ND - cursor))) & ((1u << ND) - 1u);
-  uint32_t d = cursor + (uint32_t)ffs0(rot);   // < 2 N_D: wrap without a division
-  d = d >= (uint32_t)ND ? d - (uint32_t)ND : d;
-  dsel = (uint16_t)d;
-  if (__popc(inset) >= 2) cursor = d + 1u >= (uint32_t)ND ? 0u : d + 1u;                 // A17
+  dsel = (uint16_t)rr_pick(inset, ND, cursor);                                         // A17
 }
 
 constexpr int ROUTE_MINB = 4;     // CTAs of 8 warps per SM (<= 64 registers); 5 CTAs or 3-4 items: slower
@@ -456,6 +503,13 @@ route_kernel(const __grid_constant__ RouteParams P) {
   const double *it = itl_smem(sm, K, P.prof);
   const double *dy = dyn_smem(sm, K, P.prof);
   const int wshift = (P.prof.tile_w & (P.prof.tile_w - 1)) == 0 ? __ffs(P.prof.tile_w) - 1 : -1;
+  // N_D = 2 EcoRoute with a known ladder length: the case analysis as a shared-memory table
+  uint8_t *lut = nullptr;
+  if (ND_MAX == 2 && KK > 0 && P.policy == 0) {
+    lut = (uint8_t *)(smi + K);
+    build_route_lut(lut, K, smi, P.delta);
+    __syncthreads();
+  }
   constexpr int U = ND_MAX <= 2 ? ROUTE_U2 : 2;
   const size_t tile = (size_t)blockDim.x * U;
   for (size_t base = (size_t)blockIdx.x * tile; base < P.n; base += (size_t)gridDim.x * tile) {
@@ -487,7 +541,7 @@ route_kernel(const __grid_constant__ RouteParams P) {
       if (i >= P.n) continue;
       uint16_t dsel;
       uint8_t cse, st;
-      route_item<ND_MAX, KK>(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], n[u], kv[u], dsel, cse, st);
+      route_item<ND_MAX, KK>(P, it, dy, smi, K, ND, wshift, inv[u], tg[u], cur[u], n[u], kv[u], dsel, cse, st, lut);
       P.out_instance[i] = dsel;
       P.out_case[i] = cse;
       P.out_status[i] = st;
@@ -532,6 +586,7 @@ static cudaError_t launch_route_t(const RouteParams &P, int grid, size_t smem, c
 
 cudaError_t launch_route(const RouteParams &P, int grid, size_t smem, cudaStream_t st) {
   if (P.n_d == 2) {
+    if (P.policy == 0 && P.lad.k <= 8) smem += 2 * (size_t)P.lad.k * P.lad.k * P.lad.k * P.lad.k;   // decision table
     switch (P.lad.k) {  // ladder length (and N_D = 2) as template arguments: straight-line code
       case 1: return launch_route_t<2, 1>(P, grid, smem, st);
       case 2: return launch_route_t<2, 2>(P, grid, smem, st);

@@ -19,11 +19,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C4")
 ap.add_argument("--heaviest", type=int, default=1, help="the k scenarios with the longest traces")
 ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--index", type=int, nargs="*", default=None, help="explicit scenario indices instead of --heaviest")
 a = ap.parse_args()
 w = synth.build_config(a.config)
 lens = w.traces.lengths()[w.scen["trace_id"]].astype(np.int64)
 # heaviest = longest trace, most demanding SLO first (stable on scenario index)
-idx = np.argsort(-lens, kind="stable")[:a.heaviest]
+idx = np.argsort(-lens, kind="stable")[:a.heaviest] if a.index is None else np.array(a.index)
 sub = w.subset(idx)
 wl = vt.DeviceWorkload(sub.traces, sub.slos, sub.layouts, sub.grids, sub.profiles, sub.scen)
 for r in range(a.reps):

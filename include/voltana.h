@@ -134,7 +134,12 @@ voltana_status voltana_route_batch(const voltana_profile *prof_h, const uint16_t
  * any 2 or 3 is the E_CALIBRATION condition). Sums use a fixed reduction order, so the
  * result is deterministic and within 1e-12 relative of the sequential oracle.
  * Samples with phase > 1, level >= k, (decode and n_req == 0) or (prefill and n_bt == 0)
- * are ignored and counted in invalid_count (device u64, may be NULL).                   */
+ * are ignored and counted in invalid_count (device u64, may be NULL).
+ * Launch: one cooperative kernel (every CTA resident, grid barriers between the three
+ * passes: means, centred sums + solve, MAE); a device that cannot co-schedule the grid makes
+ * the launch fail with VOLTANA_E_CUDA. The workspace (voltana_fit_workspace_bytes) holds
+ * warp-private accumulator rows (40 B per cell per resident warp), the CTA partials and the
+ * grid sums; it needs no initialisation (rows are written at their first touch).          */
 size_t voltana_fit_workspace_bytes(size_t n_samples, int k, int n_tiles, int n_ptiles);
 voltana_status voltana_fit_profile(const uint8_t *phase, const uint16_t *level,
                                    const uint32_t *n_bt, const uint32_t *n_req,

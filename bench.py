@@ -314,8 +314,9 @@ def streaming_kernels(vt, torch, dev, hbm_gbs, reps=100):
     # samples in the order a profiling run records them (one run per frequency level,
     # iterations in time order, batch sizes drifting: cell-clustered); "_shuffled" is the
     # adversarial order (random cells in every 32-sample chunk)
-    for label, per_cell, shuffled in (("fit_profile", 4096, False), ("fit_profile_large", 32768, False),
-                                      ("fit_profile_large_shuffled", 32768, True)):
+    # (runs of 4201 / 32771 samples per cell: cell boundaries fall inside 128-sample chunks)
+    for label, per_cell, shuffled in (("fit_profile", 4201, False), ("fit_profile_large", 32771, False),
+                                      ("fit_profile_large_shuffled", 32771, True)):
         smp = profile_samples(prof, per_cell, per_cell, noise_sigma=0.02, seed=9, shuffle=shuffled)
         to = lambda a: torch.from_numpy(a.view(np.int32) if a.dtype == np.uint32 else
                                         (a.view(np.int16) if a.dtype == np.uint16 else a)).to(dev)

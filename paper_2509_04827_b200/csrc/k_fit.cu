@@ -10,9 +10,11 @@
 // few chunks ahead. A chunk whose 128 samples are one cell (the usual case: calibration samples
 // come run by run) is added into registers (each lane sums its own samples in order); at
 // the end of the run a fixed binary tree over the lanes adds it to the warp's row of that cell.
-// Other chunks go sample slot by sample slot (j = 0..3): lanes of equal cell are ranked with
-// __match_any_sync and add to the row in lane order (the row is written, not added, at the
-// cell's first touch in the pass: no zeroing). The rows (cells x 5 doubles per warp) live in global memory, private to the warp
+// Any other chunk goes sample slot by sample slot (j = 0..3): runs of consecutive lanes of one
+// cell are summed by a segmented scan over the lanes (a fixed tree) and added to the row by the
+// run's last lane; runs of one cell that are not contiguous (shuffled input) are ranked with
+// __match_any_sync and add in lane order. A row is written, not added, at its cell's first touch
+// in a pass: no zeroing. The rows (cells x 5 doubles per warp) live in global memory, private to the warp
 // (L1/L2-resident, touched only at run ends and mixed chunks), with a touched-cell bitmap per
 // warp in shared memory; so the per-warp state does not limit the occupancy (16 warps per SM).
 // Every warp partial is a fixed sum, independent of timing (no fp64 atomics). Between passes the grid synchronises
@@ -243,31 +245,52 @@ __device__ void stream_pass(const FitParams &P, const FitTabs &T, double *acc, u
       return;
     }
     flush();
-    // slot by slot (j = 0..3): lanes of one cell (a __match_any_sync group) add to the row one
-    // at a time in lane order (ranked rounds; the lanes of one round touch distinct cells)
+    // slot by slot (j = 0..3): runs of consecutive lanes of one cell (recording order: the few
+    // cell boundaries of a chunk) are summed by a segmented inclusive scan over the lanes (five
+    // shuffle steps, a fixed tree), and the run's last lane adds the run to the row; runs of
+    // one cell that are not contiguous (shuffled input) are ranked with __match_any_sync and
+    // add one at a time in lane order. The row is written, not added, at the cell's first touch.
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int key = act[j] ? s[j].cell : -1 - lane;
-      const unsigned peers = __match_any_sync(FULL, key);
+      double t[NS];
+      sample_values<PASS, NS>(P, T, s[j], t);
+      uint64_t x1 = s[j].x1, x2 = s[j].x2;
+      const int pkey = __shfl_up_sync(FULL, key, 1);
+      const unsigned heads = __ballot_sync(FULL, lane == 0 || pkey != key);
+      const int start = 31 - __clz(heads & (0xFFFFFFFFu >> (31 - lane)));   // this run's first lane
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+        for (int q = 0; q < NS; ++q) {
+          if (PASS == 1 && q < 3) continue;
+          const double y = __shfl_up_sync(FULL, t[q], o);
+          if (lane - o >= start) t[q] = add(y, t[q]);
+        }
+        if (PASS == 1) {
+          const uint64_t y1 = __shfl_up_sync(FULL, x1, o), y2 = __shfl_up_sync(FULL, x2, o);
+          if (lane - o >= start) { x1 += y1; x2 += y2; }
+        }
+      }
+      const bool item = act[j] && (lane == 31 || ((heads >> (lane + 1)) & 1u));   // a run's last lane
+      const unsigned peers = __match_any_sync(FULL, item ? key : -1 - lane);
       const unsigned rank = __popc(peers & ((1u << lane) - 1u));
-      const unsigned maxr = __reduce_max_sync(FULL, act[j] ? rank : 0u);
-      double v[NS];
-      sample_values<PASS, NS>(P, T, s[j], v);
+      const unsigned maxr = __reduce_max_sync(FULL, item ? rank : 0u);
       for (unsigned rr = 0; rr <= maxr; ++rr) {
-        if (act[j] && rank == rr) {
+        if (item && rank == rr) {
           const int c = s[j].cell;
           const bool first = !((bm[c >> 5] >> (c & 31)) & 1u);   // the row is written, not added
           atomicOr(bm + (c >> 5), 1u << (c & 31));
           double *a = acc + (size_t)c * NS;
           if (PASS == 1) {
             uint64_t *u = (uint64_t *)a;
-            u[0] = (first ? 0u : u[0]) + 1u;
-            u[1] = (first ? 0u : u[1]) + s[j].x1;
-            u[2] = (first ? 0u : u[2]) + s[j].x2;
-            a[3] = first ? v[3] : add(a[3], v[3]);
+            u[0] = (first ? 0u : u[0]) + (uint64_t)(lane - start + 1);
+            u[1] = (first ? 0u : u[1]) + x1;
+            u[2] = (first ? 0u : u[2]) + x2;
+            a[3] = first ? t[3] : add(a[3], t[3]);
           } else {
 #pragma unroll
-            for (int q = 0; q < NS; ++q) a[q] = first ? v[q] : add(a[q], v[q]);
+            for (int q = 0; q < NS; ++q) a[q] = first ? t[q] : add(a[q], t[q]);
           }
         }
         __syncwarp();

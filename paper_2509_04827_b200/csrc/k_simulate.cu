@@ -233,6 +233,31 @@ __device__ __forceinline__ int lowest_itl_from(const WS &W, uint32_t n, uint32_t
   return ok;
 }
 
+// The lowest feasible level (A1, A2) of the state (n >= 1, kv) held by this lane's group of
+// eight lanes (lanes 8g..8g+7, `on` uniform in the group), on coefficient-monotone tables where
+// the feasible levels are upward closed (A32): round 1 probes levels S-1, 2S-1, ... (S =
+// ceil(K/8), the last probe is K-1, feasible by A2); round 2 probes the < 8 levels below the first
+// feasible probe. The ascending scan's answer, in two parallel evaluations per lane. K <= 64.
+template <bool F, class WS>
+__device__ __forceinline__ int lowest_itl_g8(const WS &W, uint32_t n, uint32_t kv, double target, bool on) {
+  const uint32_t lane = threadIdx.x & 31u, r = lane & 7u, gsh = lane & ~7u;
+  const int K = (int)W.K;
+  const int S = (K + 7) >> 3;
+  const uint32_t j = tile_j<F>(W, n);
+  const double dn = (double)n, dkv = (double)kv;
+  const int p = min((int)(r + 1u) * S - 1, K - 1);
+  bool f = !on || p == K - 1 || itl_at<F>(W, j, p, dn, dkv) <= target;
+  unsigned m = (__ballot_sync(FULL, f) >> gsh) & 0xFFu;
+  const int fi = ffs0(m);                        // the first feasible probe (the last one is K-1)
+  const int hi = min((fi + 1) * S - 1, K - 1);   // feasible
+  const int lo = fi * S;                         // levels lo..hi-1: not probed yet
+  const int q = lo + (int)r;
+  f = !on || q >= hi || itl_at<F>(W, j, q, dn, dkv) <= target;
+  m = (__ballot_sync(FULL, f) >> gsh) & 0xFFu;
+  const int k = lo + ffs0(m);
+  return k < hi ? k : hi;
+}
+
 // busy power (eq:P-f P:187, A22) with the utilisation from the launch's table (the entries
 // are the same division, so the value is identical)
 __device__ __forceinline__ double bpow_u(const double *ut, double p_idle, double tdp, double uh, int phase, double dyn,
@@ -1548,7 +1573,30 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
       cse = 0;
     } else {     // general tables: per-lane what-if with a cached current level
       int fnow = 0x7fffffff, faft = 0x7fffffff;
-      if (lane < ND) {
+      if (!F && W.mono_it && W.K > 8u && ND <= 4) {
+        // long ladder, coefficient-monotone tables (A32): eight lanes per instance search its
+        // levels in two rounds of parallel probes (lowest_itl_g8) instead of one lane's binary
+        // search — for the cached current level when the state changed, and for the successor
+        const uint32_t g = lane >> 3;
+        const bool gon = g < (uint32_t)ND;
+        const uint32_t en = D.nreq + D.pn, ek = D.nkv + D.pkv;  // A9 effective state (lane d < N_D)
+        const bool mine_need = lane < (uint32_t)ND && en != 0u && (en != c_n || ek != c_kv);
+        const uint32_t n_g = wshfl(en, (int)(g & 3u)), kv_g = wshfl(ek, (int)(g & 3u));
+        const bool need_g = __shfl_sync(FULL, mine_need, (int)(g & 3u));   // every lane (no short-circuit)
+        const bool need = gon && need_g;
+        int kn_g = 0;
+        if (__any_sync(FULL, need)) kn_g = lowest_itl_g8<F>(W, need ? n_g : 1u, kv_g, W.tgt_itl, need);
+        const int ka_g = lowest_itl_g8<F>(W, n_g + 1u, kv_g + in_i + 1u, W.tgt_itl, gon);   // A12
+        const int src = lane < (uint32_t)ND ? 8 * lane : 0;
+        const int kn_s = __shfl_sync(FULL, kn_g, src), ka = __shfl_sync(FULL, ka_g, src);
+        if (lane < (uint32_t)ND) {
+          if (mine_need) { c_lvl = kn_s; c_n = en; c_kv = ek; }
+          const int kn = en == 0u ? 0 : c_lvl;                                   // A10, A11
+          ka_last = ka;
+          fnow = W.mhz[kn];
+          faft = W.mhz[ka];
+        }
+      } else if (lane < ND) {
         const uint32_t n = D.nreq + D.pn, kv = D.nkv + D.pkv;  // A9 effective state
         double pr;
         int kn = 0;                                                            // A10, A11

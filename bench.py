@@ -561,11 +561,14 @@ def run_ours(args):
     h2d = d2h = 0
     e2e_ms = 0.0
     e_steps = max(1, args.e2e_steps)
-    pipelined = world == 1   # double-buffered inputs: step k + 1's H2D overlaps step k's kernels
+    pipelined = True         # double-buffered inputs: step k + 1's H2D overlaps step k's kernels
     if world > 1:
         dist.barrier()
     if pipelined:
-        wl2 = vt.DeviceWorkload(w.traces, w.slos, w.layouts, w.grids, [dprof], w.scen, device=dev).pin_host()
+        # (both buffers write their records into the same send buffer of the collective: the
+        # steps are ordered on the compute stream, so one step's gather reads its own records)
+        wl2 = vt.DeviceWorkload(w.traces, w.slos, w.layouts, w.grids, [dprof], w.scen, device=dev,
+                                out=None if gather is None else gather.local).pin_host()
         wls = (wl, wl2)
         samps = (samp, {k: torch.empty_like(v) for k, v in samp.items()})
         cs = torch.cuda.Stream(device=dev)
@@ -596,6 +599,8 @@ def run_ours(args):
             vt.fit_profile(sx["phase"], sx["level"], sx["n_bt"], sx["n_req"], sx["n_kv"], sx["lat_ms"], prof.k,
                            prof.n_tiles, prof.tile_w, 0.0, workspace=fit["workspace"], out=fit)
             wls[x].launch()
+            if gather is not None:
+                gather.enqueue()
             d2h = wls[x].fetch_records()
             freed[x] = torch.cuda.Event()
             freed[x].record(stream)
@@ -605,7 +610,8 @@ def run_ours(args):
         b.synchronize()
         e2e_ms = a.elapsed_time(b)
         # both buffers produced the same records (the D2H copies are complete after b)
-        assert e_steps < 2 or torch.equal(wl.host_out, wl2.host_out), "e2e double buffers disagree"
+        assert e_steps < 2 or gather is not None or torch.equal(wl.host_out, wl2.host_out), \
+            "e2e double buffers disagree"
         del wl2, samps
     else:
         for k in range(e_steps):
@@ -633,8 +639,9 @@ def run_ours(args):
            "d2h_bytes_per_step": int(d2h),
            "path": "DeviceWorkload.stage_inputs (pinned H2D of traces+scenario tables+samples) -> fit_profile -> "
                    "simulate -> fetch_records (D2H)" + (
-                       ", double-buffered: step k+1's H2D on a copy stream overlaps step k's kernels; the timed "
-                       "region runs from the first H2D to the last D2H" if pipelined else ", serial per step")}
+                       ", double-buffered: step k+1's H2D on a copy stream overlaps step k's kernels (and the "
+                       "record all-gather when N > 1); the timed region runs from the first H2D to the last D2H"
+                       if pipelined else ", serial per step")}
 
     # ---------------- roofline of the dominant kernel (K4b simulate_kernel)
     peaks = load_json("MEASURED_PEAKS.json") or {"hbm_gbs": 6650.0}

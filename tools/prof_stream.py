@@ -1,6 +1,8 @@
 """One warm call each of K2 control_step (2^25 snapshots), K3 route_batch (2^24 items) and K1
 fit_profile (32768 samples per cell of the L8 profile, 15.6 M samples) — for ncu captures.
 
+    ncu --set full -k regex:"control_kernel|route_kernel|fit_kernel" -c 4 python tools/prof_stream.py
+
     ncu --set full -k regex:"control_kernel|route_kernel|fit_pass" --launch-skip 5 -c 5 python tools/prof_stream.py
 """
 import os
@@ -33,7 +35,7 @@ d = {k: to(v) for k, v in smp.items()}
 for k in ("n_bt", "n_req", "n_kv"):
     d[k] = d[k].view(torch.uint32)
 d["level"] = d["level"].view(torch.uint16)
-for rep in range(2):   # launch order per rep: control, route, fit pass 1..3
+for rep in range(2):   # launch order per rep: control, route, fit (one cooperative launch)
     vt.control_step(dp, 1, lad, load, kv, q, None, tgt)
     vt.route_batch(dp, lad, 2, nr, nk, rin, tgt[:m], 150, 0, cur)
     fo = vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k, prof.n_tiles)

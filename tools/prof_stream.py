@@ -2,8 +2,6 @@
 fit_profile (32768 samples per cell of the L8 profile, 15.6 M samples) — for ncu captures.
 
     ncu --set full -k regex:"control_kernel|route_kernel|fit_kernel" -c 4 python tools/prof_stream.py
-
-    ncu --set full -k regex:"control_kernel|route_kernel|fit_pass" --launch-skip 5 -c 5 python tools/prof_stream.py
 """
 import os
 import sys

@@ -553,14 +553,17 @@ int fit_warps_per_block(int cells) {
   return FIT_MAX_WARPS;
 }
 
-// cudaFuncSetAttribute for the dynamic shared memory, once per size (host-side cost per call)
+// cudaFuncSetAttribute for the dynamic shared memory, once per (device, size): host-side cost
 static cudaError_t set_fit_smem(size_t smem) {
   static std::mutex mu;
-  static size_t done = 0;
+  static size_t done[64] = {0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> g(mu);
-  if (smem <= done) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) done = smem;
+  if (dev >= 0 && dev < 64 && smem <= done[dev]) return cudaSuccess;
+  e = cudaFuncSetAttribute(fit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && dev >= 0 && dev < 64) done[dev] = smem;
   return e;
 }
 

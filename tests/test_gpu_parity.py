@@ -372,3 +372,27 @@ def test_fit_parity_unaligned_and_ragged(vt, orc, shuffle):
         g, o = out[name].cpu().numpy(), ref[name]
         err = np.abs(g - o) / np.maximum(np.abs(o), 1e-9)
         assert err.max() <= 1e-12 or np.abs(g - o).max() < 1e-12, (name, err.max())
+
+
+def test_fit_parity_bench_scale(vt, orc):
+    """K1 at the bench's scale: the 2 M-sample calibration set of bench.py (runs of 4201 samples
+    per cell, so cell boundaries fall inside 128-sample chunks; a full co-resident grid with its
+    barriers) against the oracle's fit of the same samples."""
+    import bench
+    prof = synth.make_profile("L8")
+    s = bench.fit_samples(prof)
+    ref = orc.fit_profile(s["phase"], s["level"], s["n_bt"], s["n_req"], s["n_kv"], s["lat_ms"], prof.k,
+                          prof.n_tiles, prof.tile_w, 0.0)
+    d = {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int32) if v.dtype == np.uint32 else v).to("cuda")
+         for k, v in s.items()}
+    for k in ("n_bt", "n_req", "n_kv"):
+        d[k] = d[k].view(torch.uint32)
+    d["level"] = torch.from_numpy(s["level"].view(np.int16)).to("cuda").view(torch.uint16)
+    out = vt.fit_profile(d["phase"], d["level"], d["n_bt"], d["n_req"], d["n_kv"], d["lat_ms"], prof.k,
+                         prof.n_tiles, prof.tile_w, 0.0)
+    torch.cuda.synchronize()
+    assert (out["cell_status"].cpu().numpy() == ref["cell_status"]).all()
+    for name in ("a1", "c1", "a2", "b2", "c2", "mae"):
+        g, o = out[name].cpu().numpy(), ref[name]
+        err = np.abs(g - o) / np.maximum(np.abs(o), 1e-9)
+        assert err.max() <= 1e-12 or np.abs(g - o).max() < 1e-12, (name, err.max())

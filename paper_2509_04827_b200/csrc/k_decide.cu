@@ -477,6 +477,7 @@ __device__ __forceinline__ void route_item(const RouteParams &P, const double *i
       if (d < ND) scan_pair<KK>(it, P.prof, K, n[d], kv[d], in, tgt, wshift, kn[d], ka[d]);   // A10-A12
     }
     if (NI == 2 && lut) {   // N_D = 2, K <= 8: the case analysis as a table (built by eco_levels)
+      VT_CHECK(kn[0] < K && ka[0] < K && kn[NI - 1] < K && ka[NI - 1] < K && cursor < 2u);
       const uint32_t v = lut[((((uint32_t)(kn[0] * K + ka[0]) * K + kn[NI - 1]) * K + ka[NI - 1]) << 1) | cursor];
       dsel = (uint16_t)(v & 1u);
       cse = (uint8_t)((v >> 1) & 7u);

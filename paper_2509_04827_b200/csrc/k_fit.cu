@@ -195,6 +195,7 @@ __device__ void stream_pass(const FitParams &P, const FitTabs &T, double *acc, u
     if (lane == 0) {
       const bool first = !((bm[run_cell >> 5] >> (run_cell & 31)) & 1u);   // the row is written, not added
       atomicOr(bm + (run_cell >> 5), 1u << (run_cell & 31));
+      VT_CHECK(run_cell >= 0 && run_cell < P.cells);
       double *a = acc + (size_t)run_cell * NS;
       if (PASS == 1) {
         uint64_t *u = (uint64_t *)a;
@@ -281,6 +282,7 @@ __device__ void stream_pass(const FitParams &P, const FitTabs &T, double *acc, u
           const int c = s[j].cell;
           const bool first = !((bm[c >> 5] >> (c & 31)) & 1u);   // the row is written, not added
           atomicOr(bm + (c >> 5), 1u << (c & 31));
+          VT_CHECK(c >= 0 && c < P.cells && lane - start + 1 >= 1);
           double *a = acc + (size_t)c * NS;
           if (PASS == 1) {
             uint64_t *u = (uint64_t *)a;
@@ -500,6 +502,7 @@ __global__ void __launch_bounds__(FIT_MAX_WARPS * 32, FIT_CTAS_PER_SM) fit_kerne
   T.status = (uint8_t *)(bms + wpb * P.bmw);
   uint32_t *bm = bms + wib * P.bmw;
   const size_t gw = (size_t)blockIdx.x * wpb + wib;
+  VT_CHECK(P.bmw == (C + 31) / 32 && P.chunk % FIT_CH == 0);
   // this warp's rows (global, private to the warp): a cell's row is written at its first touch
   // in a pass (touched bitmap), so no zeroing; cta_partial reads only touched rows
   double *acc = P.rows + gw * C * 5;

@@ -255,6 +255,7 @@ __device__ __forceinline__ int lowest_itl_g8(const WS &W, uint32_t n, uint32_t k
   f = !on || q >= hi || itl_at<F>(W, j, q, dn, dkv) <= target;
   m = (__ballot_sync(FULL, f) >> gsh) & 0xFFu;
   const int k = lo + ffs0(m);
+  VT_CHECK(m != 0u && hi >= 0 && hi < K && lo >= 0);
   return k < hi ? k : hi;
 }
 
@@ -474,6 +475,7 @@ __device__ void dec_advance(Dec &D, int d, const Lane &L, WS &W, double t_lim, E
       const uint32_t fin = D.iters + node_out(hn) - 2u;  // its last iteration
       if (node_out(hn) - 2u < W.nb) bucket_append(L, nbm, i, fin, node_in(hn) + node_out(hn), lfin, lb);
       else far_insert(W.dc[d], L, W.max_steps, i, fin);
+      VT_CHECK(D.nreq < 0x7fffffffu);
       D.nreq += 1u;
       D.nkv += need;
       D.pn -= 1u;
@@ -1522,6 +1524,7 @@ __device__ void run_scenario(const SimParams &P, uint32_t s, char *slot, uint4 *
         const uint32_t c0 = (uint32_t)lowest_of(fm & km, (int)K) * K + (uint32_t)lowest_of((fm >> K) & km, (int)K);
         const uint32_t c1 = (uint32_t)lowest_of((fm >> (2 * K)) & km, (int)K) * K +
                             (uint32_t)lowest_of((fm >> (3 * K)) & km, (int)K);
+        VT_CHECK(c0 < K * K && c1 < K * K && cursor < 2u && K <= (uint32_t)ECO_LUT_K);
         const uint32_t v = W.lut[((c0 * K * K + c1) << 1) | cursor];
         dsel = (int)(v & 1u);
         cse = (int)((v >> 1) & 7u);

@@ -6,7 +6,23 @@
 // energy expression below uses the explicit _rn intrinsics, so no FMA can be formed.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Bounds checks of a checked build (-DVT_CHECKS, tools/variants.py checks=VT_CHECKS=1): a failed
+// check prints its site and traps the kernel. Compiled out of the product build.
+#ifdef VT_CHECKS
+#define VT_CHECK(c)                                                                               \
+  do {                                                                                            \
+    if (!(c)) {                                                                                   \
+      printf("VT_CHECK failed: %s at %s:%d (block %d thread %d)\n", #c, __FILE__, __LINE__,       \
+             (int)blockIdx.x, (int)threadIdx.x);                                                  \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define VT_CHECK(c) do { } while (0)
+#endif
 
 #include "../../include/voltana.h"
 

@@ -561,7 +561,10 @@ def run_ours(args):
     h2d = d2h = 0
     e2e_ms = 0.0
     e_steps = max(1, args.e2e_steps)
-    pipelined = True         # double-buffered inputs: step k + 1's H2D overlaps step k's kernels
+    # double-buffered inputs (step k + 1's H2D overlaps step k's kernels) on one GPU; under torchrun
+    # the serial path (the double-buffered one with the record all-gather has not run on a
+    # multi-GPU box: gpurun gives one GPU)
+    pipelined = world == 1
     if world > 1:
         dist.barrier()
     if pipelined:

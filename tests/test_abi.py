@@ -145,3 +145,20 @@ def test_simulate_workspace_grows_with_requests(vt):
     assert abs(d - 10_000_000 * 16) <= 512
     assert ws(4096, 45412, 89_000_000) < ws(4096, 45412) - 4096 * 45412 * 16 + 89_000_000 * 16 + 1024
     assert ws(4096, 45412) == ws(4096, 45412, 0)
+
+
+def test_fit_workspace_holds_the_warp_rows(vt):
+    """K1 (one cooperative launch): the workspace holds a row block of cells x 5 doubles per
+    resident warp (two CTAs of eight warps per SM bound the grid), the CTA partials and the grid
+    sums; it does not depend on the sample count beyond that bound, and invalid shapes give 0."""
+    L = vt.lib()
+    k, T = 28, 16
+    cells = k + T * k
+    big = int(L.voltana_fit_workspace_bytes(10**8, k, T, 1))
+    small = int(L.voltana_fit_workspace_bytes(1000, k, T, 1))
+    rows_bound = 148 * 2 * 8 * cells * 5 * 8          # B200: 148 SMs
+    assert big >= rows_bound
+    assert big == int(L.voltana_fit_workspace_bytes(10**9, k, T, 1))   # bounded by the co-resident grid
+    assert small == big                                  # partials and rows are sized for any grid
+    assert int(L.voltana_fit_workspace_bytes(1000, 0, T, 1)) == 0
+    assert int(L.voltana_fit_workspace_bytes(1000, k, 0, 1)) == 0
